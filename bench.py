@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""DuetServe mixed-iteration hot path on B200 — benchmark (driver contract, one JSON line).
+
+A step = one pass of the whole hot path over one mixed batch:
+  a1/a2  duet_choose_split (roofline predictor + Alg. 1, host C++, against the tables measured by
+         duet_calibrate at start-up),
+  a3-a7  duet_step: metadata staging, partition binding, k decode steps (CUDA-graph replays on the
+         S_d partition) concurrently with the prefill chunk (S_p partition), join.
+Workload (N=1): cfg2 of BASELINE.json — Llama-3-8B layer shapes, bf16, prefill chunk 2048 + 64
+decodes at ctx 4096, TBT SLO 50 ms / 32 layers = 1.5625 ms per layer.  Synthetic seeded inputs
+(synth/), random weights of that architecture.
+
+metric: tokens/s per mixed iteration = (k T_dec + T_pre) / window, summed over ranks (each rank
+runs an independent replica: "replicas only" data parallelism, weak scaling).
+
+--impl reference runs the CPU oracle (oracle/, numpy float64) on a bounded sample of the same
+workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s per mixed iteration at TBT SLO vs SM split; % HBM/TC roofline"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return FALLBACK_PEAKS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.samples = []
+        self.proc = None
+        self.index = index
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 5.0:   # first sample before timing starts
+                time.sleep(0.02)
+            self.samples.clear()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[3 + i]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_init():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lrank = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(lrank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
+    else:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(0)
+    return ws, rank, lrank
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ----------------------------------------------------------------------------- oracle arm
+
+class OracleSample:
+    """The CPU oracle on a bounded sample of the workload: the first n_pre tokens of the prompt (exact,
+    by causality) and n_dec of the decode requests, one layer.  Inputs are prepared once (not timed);
+    run() times one oracle mixed iteration and returns (tokens, seconds)."""
+
+    def __init__(self, cfg_name: str, n_pre: int, n_dec: int):
+        import numpy as np
+        from synth import configs, workload
+        from tests.oracle_run import make_kv
+        from oracle import layer as OL
+        cfg = configs.get_config(cfg_name)
+        wl = workload.build(cfg, pre_seqs=[(n_pre, 0)], dec_ctx=list(cfg.batch.decode)[:n_dec], k=1)
+        wl.weights = [{k_: (None if v is None else np.asarray(v, dtype=np.float64)) for k_, v in w.items()}
+                      for w in wl.weights]
+        self.wl, self.kv, self.OL = wl, make_kv(wl), OL
+        self.mdl = OL.Model.from_cfg(wl.cfg.model)
+        self.tokens = n_pre + n_dec
+        self.desc = (f"oracle (numpy float64) on {cfg_name}: prompt rows 0..{n_pre - 1} of the 2048-token chunk "
+                     f"(exact by causality) + {n_dec} of the 64 decodes at ctx 4096, one layer")
+
+    def run(self):
+        wl = self.wl
+        t = time.perf_counter()
+        self.OL.mixed_iteration(self.mdl, wl.weights, wl.x_pre, wl.pre_seqs, wl.pre_tables, wl.x_dec, wl.dec_ctx,
+                                wl.dec_tables, self.kv, wl.k)
+        return self.tokens, time.perf_counter() - t
+
+
+def oracle_baseline(cfg_name: str, budget_s: float = 12.0):
+    """cpu_baseline: repeat the (256 prompt rows + 8 decodes) sample for about budget_s seconds."""
+    smp = OracleSample(cfg_name, 256, 8)
+    tok = sec = 0.0
+    n = 0
+    while sec < budget_s or n < 2:
+        a, b = smp.run()
+        tok += a
+        sec += b
+        n += 1
+    return tok / sec, f"{smp.desc}; {n} repetitions, {sec:.1f} s"
+
+
+def oracle_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        th = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        th = os.cpu_count()
+    return int(th)
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    # per-step sample sized so that warmup + steps stay within ~2-3 minutes of CPU time
+    n_steps = args.steps + args.warmup
+    smp = OracleSample(args.config, 128, 4) if n_steps <= 120 else OracleSample(args.config, 32, 2)
+    for _ in range(args.warmup):
+        smp.run()
+    tok = sec = 0.0
+    for _ in range(args.steps):
+        a, b = smp.run()
+        tok += a
+        sec += b
+    v = tok / sec
+    desc = smp.desc + ", per step"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "sample": desc},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": oracle_cores(), "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- duet arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="duet", choices=["duet", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--mode", default="auto", choices=["auto", "temporal", "spatial"])
+    ap.add_argument("--tau", type=float, default=None, help="TBT SLO per iteration, seconds")
+    ap.add_argument("--sweep", action="store_true", help="also time every SM split")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="a few steps, no extras (for ncu)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3 if not args.profile_only else args.warmup)
+
+    ws, rank, lrank = dist_init()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+
+    import numpy as np
+    import torch
+    import paper_2511_04791_b200 as D
+    from synth import configs, workload
+    from synth.gpu import inputs_gpu, kv_pools_gpu, layer_weights_gpu
+
+    cfg = configs.get_config(args.config)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    m = cfg.model
+    k_max = 32
+    wl = workload.build(cfg, k=8, with_weights=False)     # pages for up to 8 look-ahead steps
+    W = [layer_weights_gpu(m, l, cfg.seed, dev, tdt) for l in range(m.n_layers)]
+    Kp, Vp = kv_pools_gpu(wl, dev, tdt)
+    x_pre, x_dec = inputs_gpu(wl, dev, tdt)
+    n_p, n_d = x_pre.shape[0], x_dec.shape[0]
+    y_pre = torch.empty_like(x_pre)
+    y_dec = torch.empty((8,) + tuple(x_dec.shape), dtype=tdt, device=dev)
+    spec = D.make_spec(m.n_layers, m.d_model, m.ffn_dim, m.n_q_heads, m.n_kv_heads, m.head_dim, m.vocab,
+                       2 if cfg.dtype == "bf16" else 4, 1, int(m.qkv_bias), 1, m.rope_theta, m.norm_eps)
+    max_pages = max(wl.pre_tables.shape[1], wl.dec_tables.shape[1])
+    max_pos = max([c + q for q, c in wl.pre_seqs] + [c + 8 for c in wl.dec_ctx]) + 16
+    ctx = D.Ctx(spec, n_p, len(wl.pre_seqs), n_d, 8, max_pages, max_pos,
+                D.DUET_DTYPE_BF16 if cfg.dtype == "bf16" else D.DUET_DTYPE_FP32)
+    parts, total = ctx.partitions()
+
+    # L0 calibration: Pi_SM(S), B_HBM(S) on this GPU with our kernels
+    t0 = time.perf_counter()
+    fl, bw = ctx.calibrate(total)
+    t_cal = time.perf_counter() - t0
+    hw = D.HwProfile(total, parts, fl, bw)
+    tau = args.tau if args.tau is not None else cfg.batch.tbt_slo_s
+    batch = [(q, c, 0 if c == 0 else 1, 1) for q, c in wl.pre_seqs] + [(1, c, 2, 1) for c in wl.dec_ctx]
+    opts = D.DUET_OPT_FORCE_SPATIAL if args.mode == "spatial" else 0
+
+    def decide():
+        if args.mode == "temporal":
+            return D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1)
+        return D.duet_choose_split(spec, hw, batch, tau, k_max, opts)
+
+    def prefill_arg():
+        return dict(q=[q for q, _ in wl.pre_seqs], c=[c for _, c in wl.pre_seqs], table=wl.pre_tables, x=x_pre,
+                    y=y_pre)
+
+    def decode_arg(k):
+        return dict(c=wl.dec_ctx, table=wl.dec_tables, x=x_dec, y=y_dec[:k])
+
+    def one_step(split=None):
+        s = decide() if split is None else split
+        k = s.k if s.mode == D.DUET_MODE_SPATIAL else 1
+        if k > 8:
+            s = D.split_struct(s.mode, s.s_p, s.s_d, 8, s.flags, s.t_mixed, s.t_p, s.t_d, s.rho)
+            k = 8
+        ctx.step(W, prefill_arg(), decode_arg(k), Kp, Vp, wl.n_pages, s)
+        return s, k
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+
+    # ------------------------------------------------ timed region
+    barrier(ws)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(lrank)
+    clocks.start()
+    ctx.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tokens = 0
+    kernels = 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        s, k = one_step()
+        tokens += k * n_d + n_p
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = clocks.stop()
+    t_ms = e0.elapsed_time(e1)
+    kstats = ctx.profile_read()
+    ctx.profile_enable(False)
+    times = ctx.last_step_times()
+    kernels = times["kernels"] * args.steps
+    t_max = max_over_ranks(t_ms, ws)
+    value = tokens * ws / (t_max * 1e-3)
+    ms_per_step = t_max / args.steps
+    split = s
+
+    # ------------------------------------------------ per-side times & predictor error (one step)
+    one_step(split)
+    torch.cuda.synchronize()
+    side = ctx.last_step_times()
+    if split.mode == D.DUET_MODE_SPATIAL:
+        t_pred = max(split.k * split.t_d, split.t_p)
+    else:
+        t_pred = split.t_mixed
+    pred_err = abs(t_pred - side["t_window"]) / side["t_window"]
+
+    # ------------------------------------------------ aggregated vs partitioned (same kernels, same batch)
+    comp = {}
+    if not args.profile_only:
+        def timed(split_fn, n=max(5, args.steps // 2)):
+            for _ in range(2):
+                one_step(split_fn())
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            tok = 0
+            wins, tds = [], []
+            a.record(stream)
+            for _ in range(n):
+                s_, k_ = one_step(split_fn())
+                tok += k_ * n_d + n_p
+            b.record(stream)
+            torch.cuda.synchronize()
+            for _ in range(3):
+                one_step(split_fn())
+                torch.cuda.synchronize()
+                st = ctx.last_step_times()
+                wins.append(st["t_window"])
+                tds.append(st["t_decode"] / max(1, st["k"]))
+            return tok / (a.elapsed_time(b) * 1e-3), float(np.median(wins)), float(np.median(tds))
+
+        agg = timed(lambda: D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1))
+        forced = D.duet_choose_split(spec, hw, batch, tau, k_max, D.DUET_OPT_FORCE_SPATIAL)
+        if forced.k > 8:
+            forced = D.split_struct(1, forced.s_p, forced.s_d, 8, forced.flags, forced.t_mixed, forced.t_p,
+                                    forced.t_d, forced.rho)
+        spa = timed(lambda: forced)
+        comp = {
+            "aggregated": {"tok_s": agg[0], "tbt_ms": agg[2] * 1e3, "window_ms": agg[1] * 1e3,
+                           "t_pred_ms": forced.t_mixed * 1e3},
+            "partitioned_optimizer": {"s_d": forced.s_d, "s_p": forced.s_p, "k": forced.k, "tok_s": spa[0],
+                                      "tbt_ms": spa[2] * 1e3, "window_ms": spa[1] * 1e3,
+                                      "t_pred_window_ms": max(forced.k * forced.t_d, forced.t_p) * 1e3,
+                                      "t_pred_d_ms": forced.t_d * 1e3, "t_pred_p_ms": forced.t_p * 1e3},
+            "tau_ms": tau * 1e3,
+        }
+        if args.sweep:
+            rows = []
+            for sd in parts:
+                sp_ = D.split_struct(1, total - sd, sd, 1)
+                r = timed(lambda: sp_, n=3)
+                rows.append({"s_d": sd, "tok_s": r[0], "window_ms": r[1] * 1e3, "tbt_ms": r[2] * 1e3})
+            comp["sweep_k1"] = rows
+
+    # ------------------------------------------------ e2e through the C ABI with host buffers
+    e2e = None
+    if not args.profile_only:
+        hx_pre = torch.empty(x_pre.shape, dtype=tdt, pin_memory=True)
+        hx_dec = torch.empty(x_dec.shape, dtype=tdt, pin_memory=True)
+        hx_pre.copy_(x_pre)
+        hx_dec.copy_(x_dec)
+        hy_pre = torch.empty(y_pre.shape, dtype=tdt, pin_memory=True)
+        hy_dec = torch.empty(y_dec.shape, dtype=tdt, pin_memory=True)
+        n_e2e = max(5, args.steps // 2)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tok = 0
+        h2d = d2h = 0
+        a.record(stream)
+        for _ in range(n_e2e):
+            x_pre.copy_(hx_pre, non_blocking=True)
+            x_dec.copy_(hx_dec, non_blocking=True)
+            s_, k_ = one_step()
+            hy_pre.copy_(y_pre, non_blocking=True)
+            hy_dec[:k_].copy_(y_dec[:k_], non_blocking=True)
+            tok += k_ * n_d + n_p
+            h2d = hx_pre.numel() * hx_pre.element_size() + hx_dec.numel() * hx_dec.element_size()
+            d2h = hy_pre.numel() * hy_pre.element_size() + k_ * n_d * m.d_model * hy_dec.element_size()
+        b.record(stream)
+        torch.cuda.synchronize()
+        te = max_over_ranks(a.elapsed_time(b), ws)
+        e2e = {"value": tok * ws / (te * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    # ------------------------------------------------ roofline of the dominant kernel class
+    pk, pk_src = peaks()
+    dom = max(kstats, key=lambda kname: kstats[kname]["seconds"])
+    st_ = kstats[dom]
+    tensor_bound = dom in ("gemm", "prefill_attn")
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(f"{args.config}:{dom}")
+    if st_["launches"] and st_["seconds"] > 0:
+        if tensor_bound:
+            ach = st_["flops"] / st_["seconds"] / 1e12
+            peak = float(pk["bf16_tflops"])
+            roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": traffic, "kernel": dom, "launches": st_["launches"],
+                    "avg_launch_us": st_["seconds"] / st_["launches"] * 1e6, "peak_source": pk_src + " burst bf16"}
+        else:
+            ach = st_["bytes"] / st_["seconds"] / 1e9
+            peak = float(pk["hbm_gbs"])
+            roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "traffic": traffic, "kernel": dom, "launches": st_["launches"], "peak_source": pk_src}
+    else:
+        roof = {"bound": "tensor", "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None,
+                "kernel": dom}
+    share = {kname: v["seconds"] for kname, v in kstats.items()}
+
+    # ------------------------------------------------ CPU baseline (oracle), rank 0, N=1 only
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile_only:
+        v_c, desc_c = oracle_baseline(args.config)
+        cpu = {"value": v_c, "unit": "tokens/s", "cores": oracle_cores(), "kind": "oracle", "sample": desc_c}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded counter generator, random weights)",
+            "config": {"workload": f"{args.config}: {cfg.note}", "mode": ["temporal", "spatial"][split.mode],
+                       "s_p": split.s_p, "s_d": split.s_d, "k": split.k, "flags": split.flags,
+                       "tau_ms": tau * 1e3, "prefill_tokens": n_p, "decode_reqs": n_d,
+                       "l2": "inputs > L2 (1.5 GB of weights + KV read per step), no flush",
+                       "parallelism": f"dp{ws} (independent replicas)", "calibration_s": round(t_cal, 2)},
+            "predictor": {"t_pred_ms": t_pred * 1e3, "t_meas_ms": side["t_window"] * 1e3, "err": pred_err,
+                          "t_meas_decode_ms": side["t_decode"] * 1e3, "t_meas_prefill_ms": side["t_prefill"] * 1e3},
+            "comparison": comp,
+            "roofline": roof,
+            "kernel_seconds_in_timed_region": share,
+            "gpu_launches": int(kernels),
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "profile_tables": {"sms": [parts[0], parts[len(parts) // 2], total],
+                               "tflops": [fl[parts[0]] / 1e12, fl[parts[len(parts) // 2]] / 1e12, fl[total] / 1e12],
+                               "hbm_gbs": [bw[parts[0]] / 1e9, bw[parts[len(parts) // 2]] / 1e9, bw[total] / 1e9]},
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

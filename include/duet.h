@@ -1,0 +1,273 @@
+/*
+ * duet.h — C ABI of libduet.so: the data-parallel hot path of DuetServe (arXiv 2511.04791)
+ * on one B200 (sm_100a).
+ *
+ * Citations: "P:n" is line n of the paper text, with its section / equation /
+ * algorithm; "S:n" a line of the CPU-simulator spec, used only for interface and
+ * error conventions.  Readings of ambiguous passages are numbered as in DESIGN.md §Readings.
+ *
+ * Conventions (all entry points)
+ *  - Status: DUET_OK (0) or a negative duet_status.  The message of the last failure on the
+ *    calling thread is returned by duet_last_error(); it names the offending value.
+ *  - Ownership: the caller owns every buffer it passes (host or device).  The library owns
+ *    only a duet_ctx and the device workspace / pinned staging it sizes at duet_ctx_create
+ *    from duet_ctx_limits; duet_step never allocates.
+ *  - Host vs device: every pointer documented "host" is read by the CPU before the call
+ *    returns; every pointer documented "device" is a CUDA device address on ctx's device.
+ *  - Validation happens on the host before any launch; on error nothing is enqueued.
+ *  - Thread safety: duet_predict_latency / duet_choose_split are pure and thread-safe
+ *    (S:97).  A duet_ctx is used by one thread at a time.
+ */
+#ifndef DUET_H
+#define DUET_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DUET_OK = 0,
+  DUET_ERR_INVALID_ARG = -1,   /* null pointer, negative size, unknown enum value              */
+  DUET_ERR_OUT_OF_RANGE = -2,  /* an index / count outside its bound, bad page table    */
+  DUET_ERR_CONFIG = -3,        /* non-positive profile entry, tp=0 or tp not
+                                  dividing heads/ffn, inconsistent model spec          */
+  DUET_ERR_UNSUPPORTED = -4,   /* a shape the kernels do not implement (e.g. head_dim != 64/128) */
+  DUET_ERR_CUDA = -5,          /* a CUDA runtime / driver call failed                          */
+  DUET_ERR_CAPACITY = -6       /* a request exceeds the limits the ctx was created with        */
+} duet_status;
+
+/* Message of the last failure on this thread ("" if none).  Library-owned, valid until the
+ * next call on this thread. */
+const char* duet_last_error(void);
+/* ABI version (bumped on any struct change). */
+int32_t duet_abi_version(void);
+
+/* ----------------------------------------------------------------- model & hardware */
+
+/* Transformer dimensions (P:90-99 with readings #1-#6).
+ *  d_model = n_q_heads * head_dim;  n_q_heads % n_kv_heads == 0;  elem_bytes s in {1,2,4}
+ *  is the element size the roofline counts bytes with; ffn_gated=1 is SwiGLU
+ *  (reading #3: gate-up projection d_o = 2m); tp = tensor-parallel degree N. */
+typedef struct {
+  int32_t n_layers, d_model, ffn_dim, n_q_heads, n_kv_heads, head_dim, vocab;
+  int32_t elem_bytes, ffn_gated, qkv_bias, tp;
+  double rope_theta, norm_eps;
+} duet_model_spec;
+
+/* Per-partition throughput tables Pi_SM(S), B_HBM(S) measured at init (§4.2).
+ *  flops_at_sms / bw_at_sms: host arrays of total_sms+1 doubles indexed by SM count S
+ *  (index 0 unused); FLOP/s and bytes/s; must be > 0 at every S the call evaluates.
+ *  cand_sd_sms: host array of n_cand achievable decode-partition sizes S_d, ascending
+ *  (reading #16: Alg. 1's range(1, S+1, 2) is replaced by what the partition launcher can
+ *  provision; entries >= total_sms are skipped).
+ *  nvlink_bw (B/s, per direction) and allreduce_alpha (s) feed the ring allreduce term
+ *  (P:236-239); unused when tp == 1. */
+typedef struct {
+  int32_t total_sms;
+  int32_t n_cand;
+  const int32_t* cand_sd_sms;
+  const double* flops_at_sms;
+  const double* bw_at_sms;
+  double nvlink_bw;
+  double allreduce_alpha;
+} duet_hw_profile;
+
+enum { DUET_PHASE_PREFILL_FULL = 0, DUET_PHASE_PREFILL_CHUNK = 1, DUET_PHASE_DECODE = 2 };
+
+/* One scheduled request: q new query tokens, c cached tokens.
+ * Phase invariants: decode q==1 && c>0; prefill-full q>=1 && c==0; prefill-chunk q>=1 && c>0.
+ * emits_logits: 1 if this entry produces logits (counts toward t_cls, reading #12). */
+typedef struct { int32_t q, c, phase, emits_logits; } duet_req;
+
+/* Latency breakdown in seconds.  t_block = ((t_linear + t_norm_act) + t_attn)
+ * + t_allreduce ; t_total = L * t_block + t_cls. */
+typedef struct {
+  double t_linear, t_norm_act, t_attn, t_allreduce, t_block, t_cls, t_total;
+} duet_latency;
+
+enum { DUET_OPT_FORCE_SPATIAL = 1u, DUET_OPT_INCLUDE_CLS = 2u };
+
+/* f_roofline(batch, Pi_SM(sms), B_HBM(sms)) — the attention-aware roofline model of §4.1
+ * (P:194-250): token-level operators max(F/Pi, B/B) with F_lin = 2 n d_i d_o,
+ * B_lin = (n d_i + d_i d_o + n d_o) s; attention per request
+ * F = 4 h_q q (q+c) d_h + 2 h_q q (q+c), B = 2 h_q q d_h s + 2 h_kv (q+c) d_h s, max taken
+ * per request then summed (reading #8: B_SM read as B_HBM(S)); two ring
+ * allreduces per block when tp > 1; t_cls when opts has INCLUDE_CLS.
+ * Evaluation order is fixed and the result is bit-identical to the
+ * oracle (fp64, no contraction).
+ *  batch: host array of n entries (n may be 0 -> all-zero result).
+ *  sms: partition size S in [1, hw->total_sms].
+ * Errors: INVALID_ARG (null), OUT_OF_RANGE (sms, an entry violating its phase invariant),
+ *         CONFIG (spec invariants, tp divisibility, non-positive profile entry at sms). */
+duet_status duet_predict_latency(const duet_model_spec* spec, const duet_hw_profile* hw,
+                                 const duet_req* batch, int32_t n, int32_t sms, uint32_t opts,
+                                 duet_latency* out);
+
+enum { DUET_MODE_TEMPORAL = 0, DUET_MODE_SPATIAL = 1 };
+enum { DUET_FLAG_INFEASIBLE = 1, DUET_FLAG_DEGENERATE = 2 };
+
+/* Partition configuration C* = (S_p, S_d, k) of Alg. 1 with its predictions.
+ * Temporal: s_p = total_sms, s_d = 0, k = 1, t_p = t_d = t_mixed, rho = sum(q)/t_mixed. */
+typedef struct {
+  int32_t mode, s_p, s_d, k, flags;
+  double t_mixed, t_p, t_d, rho;
+} duet_split;
+
+/* Algorithm 1: t_mixed = f_roofline(all, S); temporal if t_mixed <= tau
+ * (reading #19) unless FORCE_SPATIAL; else for S_d in cand ascending: t_d(S_d), skip if
+ * > tau; t_p(S - S_d); k in {floor(t_p/t_d), floor(t_p/t_d)+1} clamped to [1, k_max]
+ * (reading #17); rho = (k T_dec + T_pre) / max(k t_d, t_p); strict ">" keeps the
+ * first maximum (reading #18).  Fallbacks are flagged, never silent: DEGENERATE
+ * (one phase absent -> temporal), INFEASIBLE (no S_d meets tau -> argmin t_d).
+ * Errors: as duet_predict_latency, plus CONFIG for tbt_slo_s <= 0 or k_max < 1. */
+duet_status duet_choose_split(const duet_model_spec* spec, const duet_hw_profile* hw,
+                              const duet_req* batch, int32_t n, double tbt_slo_s, int32_t k_max,
+                              uint32_t opts, duet_split* out);
+
+/* ----------------------------------------------------------------- execution context */
+
+typedef struct duet_ctx duet_ctx;
+
+enum { DUET_DTYPE_BF16 = 0, DUET_DTYPE_FP32 = 1 };
+enum {
+  DUET_CTX_FINE_SPLIT = 1u,  /* 2-SM (TPC) partitions: CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING;
+                                default is the driver's 8-SM granularity (cuda.h green contexts) */
+  DUET_CTX_NO_GRAPH = 2u     /* launch decode kernels directly instead of replaying a CUDA graph */
+};
+
+/* Capacity the workspace is sized for.  max_pos bounds every absolute token position
+ * (RoPE table length).  dtype: element type of weights, activations and KV pools
+ * (DUET_DTYPE_BF16 or DUET_DTYPE_FP32; fp32 runs SIMT kernels, bf16 tensor-core kernels). */
+typedef struct {
+  int32_t max_prefill_tokens, max_prefill_seqs, max_decode_reqs, max_k;
+  int32_t max_pages_per_seq, max_pos;
+  int32_t dtype;
+  uint32_t flags;
+} duet_ctx_limits;
+
+/* Creates streams bound to disjoint SM partitions (green contexts: one pre-created pair per
+ * achievable S_d — the pool P:112 describes), a full-device stream for temporal mode,
+ * events, the RoPE table and the workspace.  device: CUDA ordinal.
+ * Errors: INVALID_ARG, CONFIG (spec), UNSUPPORTED (head_dim, dtype), CUDA. */
+duet_status duet_ctx_create(int32_t device, const duet_model_spec* spec,
+                            const duet_ctx_limits* limits, duet_ctx** out);
+duet_status duet_ctx_destroy(duet_ctx* ctx);
+
+/* The achievable decode-partition sizes, ascending (host array of capacity *n on input;
+ * *n is set to the count).  total_sms: SMs of the device. */
+duet_status duet_ctx_partitions(duet_ctx* ctx, int32_t* sd_sms, int32_t* n, int32_t* total_sms);
+
+/* Per-layer weights, all device, dtype of the ctx, nn.Linear layout [out][in] (K-major):
+ *  w_qkv [(h_q + 2 h_kv) d_h][d] (rows: q heads, k heads, v heads; reading #4)
+ *  b_qkv [(h_q + 2 h_kv) d_h] or NULL;  w_o [d][h_q d_h];
+ *  w_gate_up [2m][d] (rows: gate(m) then up(m); reading #3);  w_down [d][m];
+ *  g_norm1, g_norm2 [d] (RMSNorm gains; reading #1). */
+typedef struct {
+  const void *w_qkv, *b_qkv, *w_o, *w_gate_up, *w_down, *g_norm1, *g_norm2;
+} duet_layer_weights;
+
+/* Prefill side (R_prefill): n_seqs sequences, rows grouped by sequence in order.
+ *  q, c: host [n_seqs] new / cached tokens; sequence s occupies positions c[s]..c[s]+q[s]-1.
+ *  page_table: host [n_seqs][max_pages] int32 pool pages; must cover c+q tokens.
+ *  x: device [sum q][d] input rows; y: device [sum q][d] output rows (last layer). */
+typedef struct {
+  int32_t n_seqs;
+  const int32_t* q;
+  const int32_t* c;
+  const int32_t* page_table;
+  int32_t max_pages;
+  const void* x;
+  void* y;
+} duet_prefill;
+
+/* Decode side (R_decode) for a look-ahead window of k steps.
+ *  c: host [n_reqs] cached tokens before step 1; step j (1..k) is at position c + j - 1.
+ *  page_table: host [n_reqs][max_pages]; must cover c + k tokens (look-ahead slots).
+ *  x: device [n_reqs][d] step-1 input; y: device [k][n_reqs][d] per-step outputs.  Step j>1
+ *  takes step j-1's last-layer output as input (reading #26). */
+typedef struct {
+  int32_t n_reqs;
+  const int32_t* c;
+  const int32_t* page_table;
+  int32_t max_pages;
+  const void* x;
+  void* y;
+} duet_decode;
+
+/* Paged KV cache (vLLM-style pages).  k_pool / v_pool: host arrays of
+ * n_layers device pointers, each pool [n_pages][h_kv][page_size][d_h] of the ctx dtype.
+ * slot(r, p) = (page_table[r][p / page_size], p % page_size) (C-3).  Pages must be distinct
+ * within and across all requests of one call and < n_pages.  page_size must be 16. */
+typedef struct {
+  void* const* k_pool;
+  void* const* v_pool;
+  int32_t n_pages;
+  int32_t page_size;
+} duet_kv_pages;
+
+/* One mixed serving iteration (the hot path).
+ *  split->mode == TEMPORAL: GPU_temporal_sharing_execute (Alg. 1 l.4): one full-device
+ *    stream runs the layer stack over the concatenated rows [prefill ; decode], k = 1.
+ *  split->mode == SPATIAL: GPU_spatial_sharing_execute (Alg. 1 l.22, §4.3): the decode side
+ *    runs k steps on the S_d-SM partition (launched first, as replays of a captured CUDA
+ *    graph) while the prefill side runs on the remaining S_p SMs; both join on an
+ *    event.  split->s_d must be one of duet_ctx_partitions.
+ *  pre or dec may be NULL (or have 0 rows).  w: host array of n_layers weight sets.
+ *  stream: the caller's cudaStream_t (NULL = legacy default stream).  All work is ordered
+ *  after work already on `stream`, and `stream` waits for the step's completion: the call
+ *  is asynchronous and never synchronizes the host.
+ * Errors: INVALID_ARG, OUT_OF_RANGE (page tables, s_d not achievable), CAPACITY (limits),
+ *         CUDA. */
+duet_status duet_step(duet_ctx* ctx, const duet_layer_weights* w, const duet_prefill* pre,
+                      const duet_decode* dec, const duet_kv_pages* kv, const duet_split* split,
+                      void* stream);
+
+/* Device-measured times of the last completed duet_step (CUDA events on the partition
+ * streams; requires the step to have completed, e.g. after synchronizing `stream`).
+ * Times in seconds: t_window = first launch -> join; t_decode = decode side (k steps);
+ * t_prefill = prefill side.  Temporal: t_window = t_decode = t_prefill. */
+typedef struct { double t_window, t_decode, t_prefill; int32_t mode, k, kernels; } duet_step_times;
+duet_status duet_last_step_times(duet_ctx* ctx, duet_step_times* out);
+
+/* Measures Pi_SM(S) and B_HBM(S) for S = every partition size the ctx can provision (both
+ * sides of every split, and the full device) with the library's own kernels, the recipe of
+ * a streaming-read kernel over a >= 1 GiB buffer and a bf16 GEMM.
+ * flops_at_sms / bw_at_sms: host arrays of total_sms+1 doubles; entries for sizes that
+ * cannot be provisioned are filled by linear interpolation between measured neighbours.
+ * Errors: INVALID_ARG, CUDA. */
+duet_status duet_calibrate(duet_ctx* ctx, double* flops_at_sms, double* bw_at_sms, int32_t len);
+
+/* Live kernel timing (measurement, §8(d)): while enabled, duet_step records CUDA events on the
+ * launching stream around every kernel it launches outside CUDA graphs (the prefill side of a
+ * spatial step and every kernel of a temporal step), per kernel class, together with the
+ * algorithmic FLOPs and bytes of each launch (causal attention FLOPs,
+ * weights/activations read once).  duet_profile_enable(ctx, 1) resets the counters;
+ * duet_profile_read synchronizes on the recorded events and returns DUET_KCLASS_N entries. */
+enum { DUET_KCLASS_GEMM = 0, DUET_KCLASS_PREFILL_ATTN = 1, DUET_KCLASS_DECODE_ATTN = 2, DUET_KCLASS_OTHER = 3,
+       DUET_KCLASS_N = 4 };
+typedef struct { int32_t launches; double seconds, flops, bytes; } duet_kernel_stats;
+duet_status duet_profile_enable(duet_ctx* ctx, int32_t enable);
+duet_status duet_profile_read(duet_ctx* ctx, duet_kernel_stats* out);
+
+/* ----------------------------------------------------------------- single operators
+ * The kernels of duet_step, exposed for parity tests and microbenchmarks.  All pointers are
+ * device; dtype is the ctx dtype; launched on `stream` over the full device. */
+
+/* C[M][N] = epilogue(A[M][K] . B[N][K]^T); epi: 0 store (+ bias[N] if bias), 1 residual
+ * C = R + acc, 2 SwiGLU: B has 2N rows [gate; up], C[m][j] = silu(acc_g) * acc_u. */
+enum { DUET_EPI_STORE = 0, DUET_EPI_RESIDUAL = 1, DUET_EPI_SWIGLU = 2 };
+duet_status duet_op_gemm(duet_ctx* ctx, const void* A, const void* B, void* C, const void* R,
+                         const void* bias, int32_t M, int32_t N, int32_t K, int32_t epi,
+                         void* stream);
+
+/* h[n][d] = x * (mean(x^2) + eps)^(-1/2) * g   (reading #1). */
+duet_status duet_op_rmsnorm(duet_ctx* ctx, const void* x, const void* g, void* h, int32_t n,
+                            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DUET_H */

@@ -1,0 +1,1027 @@
+// Execution context and the mixed-iteration step of DuetServe on one B200.
+//
+//  * SM partitions (§4.3): a pre-created pool of green-context pairs, one pair per
+//    achievable decode size S_d (the CUDA driver provisions disjoint SM sets; probe evidence in
+//    profiles/r01_probe_green_ctx.txt).  libsmctrl is prior art resting on driver
+//    internals and is not used.
+//  * Interruption-free dispatch: decode is launched first as k replays of one
+//    captured CUDA graph per (partition, batch shape); the graph reads positions and the step
+//    index from device memory, so the k steps need no host synchronization; prefill kernels
+//    are launched one by one on the other partition's stream; both sides join on events.
+//  * Temporal mode (Alg. 1 l.4): the same kernels on one full-device stream over the
+//    concatenated rows [prefill ; decode].
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <tuple>
+#include <vector>
+
+#include "duet_common.h"
+#include "kernels.h"
+
+using namespace duet;
+
+#define CUDA_TRY(expr)                                                                              \
+  do {                                                                                              \
+    cudaError_t e_ = (expr);                                                                        \
+    if (e_ != cudaSuccess)                                                                          \
+      DUET_FAIL(DUET_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define CU_TRY(expr)                                                                                \
+  do {                                                                                              \
+    CUresult r_ = (expr);                                                                           \
+    if (r_ != CUDA_SUCCESS) {                                                                       \
+      const char* s_ = nullptr;                                                                     \
+      DRV.GetErrorString(r_, &s_);                                                                    \
+      DUET_FAIL(DUET_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, s_ ? s_ : "?", __FILE__, __LINE__); \
+    }                                                                                               \
+  } while (0)
+
+namespace {
+
+// Driver entry points, resolved through the runtime (no link-time dependency on libcuda, so
+// the library also loads on a GPU-less host for the predictor / optimizer).
+struct Driver {
+  bool ok = false;
+  CUresult (*Init)(unsigned) = nullptr;
+  CUresult (*DeviceGet)(CUdevice*, int) = nullptr;
+  CUresult (*DeviceGetDevResource)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+  CUresult (*DevSmResourceSplitByCount)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned,
+                                        unsigned) = nullptr;
+  CUresult (*DevResourceGenerateDesc)(CUdevResourceDesc*, CUdevResource*, unsigned) = nullptr;
+  CUresult (*GreenCtxCreate)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned) = nullptr;
+  CUresult (*GreenCtxStreamCreate)(CUstream*, CUgreenCtx, unsigned, int) = nullptr;
+  CUresult (*GreenCtxDestroy)(CUgreenCtx) = nullptr;
+  CUresult (*StreamDestroy)(CUstream) = nullptr;
+  CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+};
+Driver DRV;
+
+duet_status load_driver() {
+  if (DRV.ok) return DUET_OK;
+  auto get = [](const char* name, void** fn) -> duet_status {
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPointByVersion(name, fn, 12080, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !*fn)
+      DUET_FAIL(DUET_ERR_CUDA, "driver entry point %s unavailable", name);
+    return DUET_OK;
+  };
+  DUET_TRY(get("cuInit", (void**)&DRV.Init));
+  DUET_TRY(get("cuDeviceGet", (void**)&DRV.DeviceGet));
+  DUET_TRY(get("cuDeviceGetDevResource", (void**)&DRV.DeviceGetDevResource));
+  DUET_TRY(get("cuDevSmResourceSplitByCount", (void**)&DRV.DevSmResourceSplitByCount));
+  DUET_TRY(get("cuDevResourceGenerateDesc", (void**)&DRV.DevResourceGenerateDesc));
+  DUET_TRY(get("cuGreenCtxCreate", (void**)&DRV.GreenCtxCreate));
+  DUET_TRY(get("cuGreenCtxStreamCreate", (void**)&DRV.GreenCtxStreamCreate));
+  DUET_TRY(get("cuGreenCtxDestroy", (void**)&DRV.GreenCtxDestroy));
+  DUET_TRY(get("cuStreamDestroy", (void**)&DRV.StreamDestroy));
+  DUET_TRY(get("cuGetErrorString", (void**)&DRV.GetErrorString));
+  DRV.ok = true;
+  return DUET_OK;
+}
+
+constexpr int kPageSize = 16;
+constexpr int kStageSlots = 4;
+constexpr int kMaxSplits = 32;
+
+struct Partition {
+  int s_d = 0, s_p = 0;  // actual SM counts of the decode group and the remainder
+  bool created = false;
+  CUgreenCtx g_dec = nullptr, g_pre = nullptr;
+  cudaStream_t s_dec = nullptr, s_pre = nullptr;
+};
+
+// Device workspace of one side (decode or prefill/temporal).
+struct Side {
+  int cap_rows = 0, cap_seqs = 0, cap_table_rows = 0, pitch = 0;
+  void *xa = nullptr, *xb = nullptr, *h = nullptr, *qkv = nullptr, *o = nullptr, *x1 = nullptr, *h2 = nullptr,
+       *act = nullptr, *xin = nullptr, *ylast = nullptr;
+  int* meta = nullptr;  // [pos | tok_row | row0 | qlen | cpre | seq_row | step | table]
+  float *part_o = nullptr, *part_ml = nullptr;
+  int part_rows = 0;
+  // offsets into meta (ints)
+  size_t o_pos = 0, o_tok = 0, o_row0 = 0, o_qlen = 0, o_cpre = 0, o_seqrow = 0, o_step = 0, o_table = 0, n_meta = 0;
+  int* pos() const { return meta + o_pos; }
+  int* tok() const { return meta + o_tok; }
+  int* row0() const { return meta + o_row0; }
+  int* qlen() const { return meta + o_qlen; }
+  int* cpre() const { return meta + o_cpre; }
+  int* seqrow() const { return meta + o_seqrow; }
+  int* step() const { return meta + o_step; }
+  int* table() const { return meta + o_table; }
+};
+
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  int kernels = 0;
+};
+
+}  // namespace
+
+struct duet_ctx {
+  int device = 0;
+  duet_model_spec spec{};
+  duet_ctx_limits lim{};
+  DT dt = DT::BF16;
+  int total_sms = 0;
+  CUdevice cudev = 0;
+  CUdevResource sm_all{};
+  std::vector<Partition> parts;
+  cudaStream_t s_full = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_dec0 = nullptr, ev_dec1 = nullptr, ev_pre0 = nullptr, ev_pre1 = nullptr;
+  float2* rope = nullptr;
+  Side dec, pre;
+  int* stage = nullptr;  // pinned [kStageSlots][stage_ints]
+  size_t stage_ints = 0;
+  cudaEvent_t stage_ev[kStageSlots] = {};
+  int stage_next = 0;
+  std::vector<uint32_t> page_mark;
+  uint32_t page_gen = 0;
+  std::map<std::tuple<int, int, int, uint64_t>, GraphEntry> graphs;
+  // last step
+  int last_mode = -1, last_k = 0, last_kernels = 0;
+  bool last_has_dec = false, last_has_pre = false;
+  // live kernel timing
+  bool prof_on = false, capturing = false;
+  struct ProfRec {
+    int cls, idx;
+    double flops, bytes;
+  };
+  std::vector<ProfRec> prof_pending;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_pool;
+  size_t prof_used = 0;
+  duet_kernel_stats prof_acc[DUET_KCLASS_N] = {};
+};
+
+static int prof_begin(duet_ctx* c, cudaStream_t st) {
+  if (!c->prof_on || c->capturing) return -1;
+  if (c->prof_used == c->prof_pool.size()) {
+    cudaEvent_t a, b;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return -1;
+    c->prof_pool.emplace_back(a, b);
+  }
+  const int idx = (int)c->prof_used++;
+  cudaEventRecord(c->prof_pool[idx].first, st);
+  return idx;
+}
+static void prof_end(duet_ctx* c, cudaStream_t st, int idx, int cls, double flops, double bytes) {
+  if (idx < 0) return;
+  cudaEventRecord(c->prof_pool[idx].second, st);
+  c->prof_pending.push_back({cls, idx, flops, bytes});
+}
+
+// ---------------------------------------------------------------------------------- helpers
+
+static duet_status side_alloc(duet_ctx* c, Side& s, int cap_rows, int cap_seqs, int cap_table_rows, int part_rows) {
+  const auto& sp = c->spec;
+  const size_t es = dt_size(c->dt);
+  const size_t d = sp.d_model, nqkv = (size_t)(sp.n_q_heads + 2 * sp.n_kv_heads) * sp.head_dim;
+  const size_t nq = (size_t)sp.n_q_heads * sp.head_dim, m = sp.ffn_dim;
+  s.cap_rows = cap_rows;
+  s.cap_seqs = cap_seqs;
+  s.cap_table_rows = cap_table_rows;
+  s.pitch = c->lim.max_pages_per_seq;
+  const size_t R = std::max(cap_rows, 1);
+  CUDA_TRY(cudaMalloc(&s.xa, R * d * es));
+  CUDA_TRY(cudaMalloc(&s.xb, R * d * es));
+  CUDA_TRY(cudaMalloc(&s.h, R * d * es));
+  CUDA_TRY(cudaMalloc(&s.x1, R * d * es));
+  CUDA_TRY(cudaMalloc(&s.h2, R * d * es));
+  CUDA_TRY(cudaMalloc(&s.xin, R * d * es));
+  CUDA_TRY(cudaMalloc(&s.ylast, R * d * es));
+  CUDA_TRY(cudaMalloc(&s.qkv, R * nqkv * es));
+  CUDA_TRY(cudaMalloc(&s.o, R * nq * es));
+  CUDA_TRY(cudaMalloc(&s.act, R * m * es));
+  s.part_rows = std::max(part_rows, 1);
+  CUDA_TRY(cudaMalloc(&s.part_o, (size_t)s.part_rows * sp.n_q_heads * kMaxSplits * sp.head_dim * sizeof(float)));
+  CUDA_TRY(cudaMalloc(&s.part_ml, (size_t)s.part_rows * sp.n_q_heads * kMaxSplits * 2 * sizeof(float)));
+  size_t off = 0;
+  s.o_pos = off; off += R;
+  s.o_tok = off; off += R;
+  s.o_row0 = off; off += cap_seqs + 1;
+  s.o_qlen = off; off += cap_seqs + 1;
+  s.o_cpre = off; off += cap_seqs + 1;
+  s.o_seqrow = off; off += cap_seqs + 1;
+  s.o_step = off; off += 4;
+  s.o_table = off; off += (size_t)std::max(cap_table_rows, 1) * s.pitch;
+  s.n_meta = off;
+  CUDA_TRY(cudaMalloc(&s.meta, s.n_meta * sizeof(int)));
+  CUDA_TRY(cudaMemset(s.meta, 0, s.n_meta * sizeof(int)));
+  return DUET_OK;
+}
+
+static void side_free(Side& s) {
+  void* ptrs[] = {s.xa, s.xb, s.h, s.x1, s.h2, s.xin, s.ylast, s.qkv, s.o, s.act, s.part_o, s.part_ml, s.meta};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  s = Side{};
+}
+
+static duet_status ensure_partition(duet_ctx* c, Partition& p) {
+  if (p.created) return DUET_OK;
+  const unsigned flags = (c->lim.flags & DUET_CTX_FINE_SPLIT) ? CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING : 0;
+  CUdevResource grp[1], rem;
+  unsigned n = 1;
+  CU_TRY(DRV.DevSmResourceSplitByCount(grp, &n, &c->sm_all, &rem, flags, (unsigned)p.s_d));
+  if (n != 1 || (int)grp[0].sm.smCount != p.s_d)
+    DUET_FAIL(DUET_ERR_CUDA, "green-context split for S_d = %d gave %u SMs", p.s_d, grp[0].sm.smCount);
+  CUdevResourceDesc d1, d2;
+  CU_TRY(DRV.DevResourceGenerateDesc(&d1, grp, 1));
+  CU_TRY(DRV.DevResourceGenerateDesc(&d2, &rem, 1));
+  CU_TRY(DRV.GreenCtxCreate(&p.g_dec, d1, c->cudev, CU_GREEN_CTX_DEFAULT_STREAM));
+  CU_TRY(DRV.GreenCtxCreate(&p.g_pre, d2, c->cudev, CU_GREEN_CTX_DEFAULT_STREAM));
+  CUstream s1, s2;
+  CU_TRY(DRV.GreenCtxStreamCreate(&s1, p.g_dec, CU_STREAM_NON_BLOCKING, 0));
+  CU_TRY(DRV.GreenCtxStreamCreate(&s2, p.g_pre, CU_STREAM_NON_BLOCKING, 0));
+  p.s_dec = (cudaStream_t)s1;
+  p.s_pre = (cudaStream_t)s2;
+  p.s_p = (int)rem.sm.smCount;
+  p.created = true;
+  return DUET_OK;
+}
+
+static duet_status check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) DUET_FAIL(DUET_ERR_CUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
+  return DUET_OK;
+}
+
+// Attention plan of one layer-stack run: prefill rows [0, n_pre), decode rows [n_pre, n_pre + n_dec).
+struct AttnPlan {
+  int n_pre = 0, n_seqs = 0, max_q = 0, max_len_pre = 0;
+  int n_dec = 0, max_len_dec = 0;
+  // algorithmic work of one attention launch: causal FLOPs 4 h_q d_h (pos + 1) per query row;
+  // bytes = q + o + each KV head read once per sequence
+  double attn_flops_pre = 0, attn_bytes_pre = 0, attn_flops_dec = 0, attn_bytes_dec = 0;
+};
+
+static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms, int n_rows, const void* x_in,
+                              void* y_final, const duet_layer_weights* w, const duet_kv_pages* kv, const AttnPlan& ap,
+                              int* kernels) {
+  const auto& sp = c->spec;
+  const DT dt = c->dt;
+  const size_t es = dt_size(dt);
+  const int d = sp.d_model, hq = sp.n_q_heads, hkv = sp.n_kv_heads, dh = sp.head_dim, m = sp.ffn_dim;
+  const int nqkv = (hq + 2 * hkv) * dh;
+  const float eps = (float)sp.norm_eps;
+  int nk = 0;
+  const double n = n_rows, e = (double)es;
+  // algorithmic work per launch: FLOPs 2MNK; bytes = operands read once + output
+  auto gemm_fl = [&](double N, double K) { return 2.0 * n * N * K; };
+  auto gemm_by = [&](double N, double K, double Nout, bool resid) {
+    return (n * K + N * K + n * Nout + (resid ? n * Nout : 0.0)) * e;
+  };
+#define TIMED(cls, fl, by, call)            \
+  do {                                      \
+    const int pi_ = prof_begin(c, st);      \
+    nk += (call);                           \
+    prof_end(c, st, pi_, cls, fl, by);      \
+  } while (0)
+  for (int l = 0; l < sp.n_layers; ++l) {
+    const void* X = l == 0 ? x_in : ((l & 1) ? S.xa : S.xb);
+    void* Y = l == sp.n_layers - 1 ? y_final : ((l & 1) ? S.xb : S.xa);
+    const duet_layer_weights& W = w[l];
+    // 1. h = RMSNorm(x) g1
+    TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e, launch_rmsnorm(dt, X, W.g_norm1, S.h, n_rows, d, eps, st));
+    // 2. qkv = h W_qkv^T (+ b)
+    GemmArgs g{S.h, W.w_qkv, S.qkv, nullptr, W.b_qkv, n_rows, nqkv, d, d, d, nqkv, 0, EPI_STORE};
+    TIMED(DUET_KCLASS_GEMM, gemm_fl(nqkv, d), gemm_by(nqkv, d, nqkv, false), launch_gemm(dt, g, num_sms, st));
+    // 3. RoPE + paged KV append (before attention)
+    RopeKvArgs ra{S.qkv, nullptr, n_rows, hq, hkv, dh, S.pos(), S.tok(), S.table(), S.pitch, kPageSize,
+                  kv->k_pool[l], kv->v_pool[l], c->rope};
+    TIMED(DUET_KCLASS_OTHER, 6.0 * n * (hq + hkv) * dh, n * (nqkv + (hq + 2.0 * hkv) * dh) * e,
+          launch_rope_kv(dt, ra, st));
+    // 4. attention
+    if (ap.n_pre > 0) {
+      PrefillAttnArgs pa{};
+      pa.q = S.qkv;
+      pa.q_stride = nqkv;
+      pa.o = S.o;
+      pa.n_seqs = ap.n_seqs;
+      pa.hq = hq;
+      pa.hkv = hkv;
+      pa.dh = dh;
+      pa.row0 = S.row0();
+      pa.qlen = S.qlen();
+      pa.cpre = S.cpre();
+      pa.seq_row = S.seqrow();
+      pa.table = S.table();
+      pa.max_pages = S.pitch;
+      pa.page_size = kPageSize;
+      pa.k_pool = kv->k_pool[l];
+      pa.v_pool = kv->v_pool[l];
+      pa.max_q = ap.max_q;
+      pa.total_q = ap.n_pre;
+      pa.num_sms = num_sms;
+      pa.tok_pos = S.pos();
+      pa.tok_row = S.tok();
+      pa.max_len = ap.max_len_pre;
+      const int pi = prof_begin(c, st);
+      const int r = launch_prefill_attn(dt, pa, st);
+      if (r < 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "prefill attention: unsupported head layout");
+      prof_end(c, st, pi, DUET_KCLASS_PREFILL_ATTN, ap.attn_flops_pre, ap.attn_bytes_pre);
+      nk += r;
+    }
+    if (ap.n_dec > 0) {
+      DecodeAttnArgs da{};
+      da.q = (const char*)S.qkv + (size_t)ap.n_pre * nqkv * es;
+      da.q_stride = nqkv;
+      da.o = (char*)S.o + (size_t)ap.n_pre * hq * dh * es;
+      da.n = ap.n_dec;
+      da.hq = hq;
+      da.hkv = hkv;
+      da.dh = dh;
+      da.pos = S.pos() + ap.n_pre;
+      da.tok_row = S.tok() + ap.n_pre;
+      da.table = S.table();
+      da.max_pages = S.pitch;
+      da.page_size = kPageSize;
+      da.k_pool = kv->k_pool[l];
+      da.v_pool = kv->v_pool[l];
+      da.part_o = S.part_o;
+      da.part_ml = S.part_ml;
+      da.max_splits = kMaxSplits;
+      da.num_sms = num_sms;
+      da.max_len = ((ap.max_len_dec + 1023) / 1024) * 1024;  // same bucket in both modes
+      const int pi = prof_begin(c, st);
+      const int r = launch_decode_attn(dt, da, st);
+      if (r < 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "decode attention: unsupported head layout");
+      prof_end(c, st, pi, DUET_KCLASS_DECODE_ATTN, ap.attn_flops_dec, ap.attn_bytes_dec);
+      nk += r;
+    }
+    // 5. x1 = x + o W_o^T
+    GemmArgs go{S.o, W.w_o, S.x1, X, nullptr, n_rows, d, hq * dh, hq * dh, hq * dh, d, d, EPI_RESIDUAL};
+    TIMED(DUET_KCLASS_GEMM, gemm_fl(d, hq * dh), gemm_by(d, hq * dh, d, true), launch_gemm(dt, go, num_sms, st));
+    // 6. h2 = RMSNorm(x1) g2
+    TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e, launch_rmsnorm(dt, S.x1, W.g_norm2, S.h2, n_rows, d, eps, st));
+    // 7. act = silu(h2 W_g^T) * (h2 W_u^T)
+    GemmArgs gg{S.h2, W.w_gate_up, S.act, nullptr, nullptr, n_rows, m, d, d, d, m, 0, EPI_SWIGLU};
+    TIMED(DUET_KCLASS_GEMM, gemm_fl(2.0 * m, d), gemm_by(2.0 * m, d, m, false), launch_gemm(dt, gg, num_sms, st));
+    // 8. y = x1 + act W_d^T
+    GemmArgs gd{S.act, W.w_down, Y, S.x1, nullptr, n_rows, d, m, m, m, d, d, EPI_RESIDUAL};
+    TIMED(DUET_KCLASS_GEMM, gemm_fl(d, m), gemm_by(d, m, d, true), launch_gemm(dt, gd, num_sms, st));
+  }
+#undef TIMED
+  DUET_TRY(check_launch("layer stack"));
+  *kernels += nk;
+  return DUET_OK;
+}
+
+// Pinned staging slot (ring of kStageSlots; waits only if the host runs kStageSlots steps ahead).
+static duet_status stage_slot(duet_ctx* c, int** out, int* slot) {
+  const int s = c->stage_next;
+  c->stage_next = (s + 1) % kStageSlots;
+  CUDA_TRY(cudaEventSynchronize(c->stage_ev[s]));
+  *out = c->stage + (size_t)s * c->stage_ints;
+  *slot = s;
+  return DUET_OK;
+}
+
+// ---------------------------------------------------------------------------------- C ABI
+
+extern "C" duet_status duet_ctx_create(int32_t device, const duet_model_spec* spec, const duet_ctx_limits* lim,
+                                       duet_ctx** out) {
+  clear_error();
+  if (!spec || !lim || !out) DUET_FAIL(DUET_ERR_INVALID_ARG, "spec/limits/out is NULL");
+  *out = nullptr;
+  if (spec->n_layers <= 0 || spec->d_model <= 0 || spec->n_q_heads <= 0 || spec->n_kv_heads <= 0 ||
+      spec->ffn_dim <= 0 || spec->head_dim <= 0 || spec->n_q_heads % spec->n_kv_heads ||
+      spec->d_model != spec->n_q_heads * spec->head_dim)
+    DUET_FAIL(DUET_ERR_CONFIG, "model spec is inconsistent (d_model = n_q_heads * head_dim, h_q %% h_kv == 0)");
+  if (spec->head_dim != 64 && spec->head_dim != 128)
+    DUET_FAIL(DUET_ERR_UNSUPPORTED, "head_dim = %d (kernels implement 64 and 128)", spec->head_dim);
+  const int G = spec->n_q_heads / spec->n_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 5 && G != 8)
+    DUET_FAIL(DUET_ERR_UNSUPPORTED, "GQA group %d (kernels implement 1, 2, 4, 5, 8)", G);
+  if (spec->d_model % 16 || spec->ffn_dim % 16)
+    DUET_FAIL(DUET_ERR_UNSUPPORTED, "d_model and ffn_dim must be multiples of 16");
+  if (lim->dtype != DUET_DTYPE_BF16 && lim->dtype != DUET_DTYPE_FP32)
+    DUET_FAIL(DUET_ERR_INVALID_ARG, "dtype = %d", lim->dtype);
+  if (lim->max_prefill_tokens < 0 || lim->max_decode_reqs < 0 || lim->max_k < 1 || lim->max_pages_per_seq < 1 ||
+      lim->max_pos < 1 || lim->max_prefill_seqs < 0)
+    DUET_FAIL(DUET_ERR_INVALID_ARG, "limits out of range");
+  duet_ctx* c = new duet_ctx();
+  c->device = device;
+  c->spec = *spec;
+  c->lim = *lim;
+  c->dt = lim->dtype == DUET_DTYPE_BF16 ? DT::BF16 : DT::F32;
+  auto fail = [&](duet_status s) {
+    duet_ctx_destroy(c);
+    return s;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) {
+    set_error("cudaSetDevice(%d) failed", device);
+    return fail(DUET_ERR_CUDA);
+  }
+  cudaFree(nullptr);
+  cudaDeviceGetAttribute(&c->total_sms, cudaDevAttrMultiProcessorCount, device);
+  duet_status st;
+#define STEP(expr)               \
+  do {                           \
+    st = (expr);                 \
+    if (st != DUET_OK) return fail(st); \
+  } while (0)
+  auto init_cu = [&]() -> duet_status {
+    DUET_TRY(load_driver());
+    CU_TRY(DRV.Init(0));
+    CU_TRY(DRV.DeviceGet(&c->cudev, device));
+    CU_TRY(DRV.DeviceGetDevResource(c->cudev, &c->sm_all, CU_DEV_RESOURCE_TYPE_SM));
+    // achievable decode sizes: simulate splits for every request count
+    const unsigned flags = (lim->flags & DUET_CTX_FINE_SPLIT) ? CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING : 0;
+    std::vector<int> seen;
+    for (int want = 1; want < c->total_sms; ++want) {
+      CUdevResource grp[1], rem;
+      unsigned n = 1;
+      if (DRV.DevSmResourceSplitByCount(grp, &n, &c->sm_all, &rem, flags, (unsigned)want) != CUDA_SUCCESS) continue;
+      if (n != 1) continue;
+      const int got = (int)grp[0].sm.smCount;
+      if (got >= c->total_sms || rem.sm.smCount == 0) continue;
+      if (std::find(seen.begin(), seen.end(), got) == seen.end()) seen.push_back(got);
+    }
+    std::sort(seen.begin(), seen.end());
+    for (int s : seen) {
+      Partition p;
+      p.s_d = s;
+      c->parts.push_back(p);
+    }
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->s_full, cudaStreamNonBlocking));
+    cudaEvent_t* evs[] = {&c->ev_in, &c->ev_dec0, &c->ev_dec1, &c->ev_pre0, &c->ev_pre1};
+    for (auto e : evs) CUDA_TRY(cudaEventCreate(e));
+    for (int i = 0; i < kStageSlots; ++i) {
+      CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(c->stage_ev[i], c->s_full));
+    }
+    // RoPE table (reading #5): theta_i = theta^(-2i/d_h), phi = p theta_i, computed in double
+    const int half = spec->head_dim / 2;
+    std::vector<float2> tab((size_t)lim->max_pos * half);
+    for (int p = 0; p < lim->max_pos; ++p)
+      for (int i = 0; i < half; ++i) {
+        const double inv = std::pow(spec->rope_theta, -2.0 * i / spec->head_dim);
+        const double phi = (double)p * inv;
+        tab[(size_t)p * half + i] = make_float2((float)std::cos(phi), (float)std::sin(phi));
+      }
+    CUDA_TRY(cudaMalloc(&c->rope, tab.size() * sizeof(float2)));
+    CUDA_TRY(cudaMemcpy(c->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    return DUET_OK;
+  };
+  STEP(init_cu());
+  const int nd = lim->max_decode_reqs, np = lim->max_prefill_tokens, ns = lim->max_prefill_seqs;
+  STEP(side_alloc(c, c->dec, nd, 0, nd, nd));
+  STEP(side_alloc(c, c->pre, np + nd, ns, ns + nd, nd));
+  // pinned staging ring: large enough for the bigger side's metadata
+  c->stage_ints = std::max(c->dec.n_meta, c->pre.n_meta) * 2;
+  if (cudaMallocHost(&c->stage, kStageSlots * c->stage_ints * sizeof(int)) != cudaSuccess) {
+    set_error("cudaMallocHost of the staging ring failed");
+    return fail(DUET_ERR_CUDA);
+  }
+  // decode rows use identity page-table rows (row r of the decode table)
+  {
+    std::vector<int> ident(std::max(nd, 1));
+    for (int i = 0; i < nd; ++i) ident[i] = i;
+    if (nd > 0 && cudaMemcpy(c->dec.tok(), ident.data(), nd * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+      set_error("metadata init failed");
+      return fail(DUET_ERR_CUDA);
+    }
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    set_error("ctx init failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(DUET_ERR_CUDA);
+  }
+#undef STEP
+  *out = c;
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_ctx_destroy(duet_ctx* c) {
+  if (!c) return DUET_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : c->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  for (auto& p : c->parts) {
+    if (!p.created) continue;
+    DRV.StreamDestroy((CUstream)p.s_dec);
+    DRV.StreamDestroy((CUstream)p.s_pre);
+    DRV.GreenCtxDestroy(p.g_dec);
+    DRV.GreenCtxDestroy(p.g_pre);
+  }
+  side_free(c->dec);
+  side_free(c->pre);
+  if (c->rope) cudaFree(c->rope);
+  if (c->stage) cudaFreeHost(c->stage);
+  cudaEvent_t evs[] = {c->ev_in, c->ev_dec0, c->ev_dec1, c->ev_pre0, c->ev_pre1};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+  for (auto e : c->stage_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& pr : c->prof_pool) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  if (c->s_full) cudaStreamDestroy(c->s_full);
+  delete c;
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_ctx_partitions(duet_ctx* c, int32_t* sd, int32_t* n, int32_t* total) {
+  clear_error();
+  if (!c || !n) DUET_FAIL(DUET_ERR_INVALID_ARG, "ctx/n is NULL");
+  const int cnt = (int)c->parts.size();
+  if (sd) {
+    if (*n < cnt) DUET_FAIL(DUET_ERR_CAPACITY, "sd_sms capacity %d < %d partitions", *n, cnt);
+    for (int i = 0; i < cnt; ++i) sd[i] = c->parts[i].s_d;
+  }
+  *n = cnt;
+  if (total) *total = c->total_sms;
+  return DUET_OK;
+}
+
+// ---------------------------------------------------------------------------------- validation
+
+static duet_status check_pages(duet_ctx* c, const int32_t* table, int32_t max_pages, int row, int n_tokens,
+                               int n_pages, const char* side) {
+  const int need = (n_tokens + kPageSize - 1) / kPageSize;
+  if (need > max_pages)
+    DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "%s request %d needs %d pages > max_pages %d", side, row, need, max_pages);
+  if (need > c->lim.max_pages_per_seq)
+    DUET_FAIL(DUET_ERR_CAPACITY, "%s request %d needs %d pages > ctx max_pages_per_seq %d", side, row, need,
+              c->lim.max_pages_per_seq);
+  for (int j = 0; j < need; ++j) {
+    const int pg = table[(size_t)row * max_pages + j];
+    if (pg < 0 || pg >= n_pages)
+      DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "%s request %d page %d = %d outside [0, %d)", side, row, j, pg, n_pages);
+    if (c->page_mark[pg] == c->page_gen)
+      DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "%s request %d page %d = %d is used twice", side, row, j, pg);
+    c->page_mark[pg] = c->page_gen;
+  }
+  return DUET_OK;
+}
+
+static duet_status validate_step(duet_ctx* c, const duet_layer_weights* w, const duet_prefill* pre,
+                                 const duet_decode* dec, const duet_kv_pages* kv, int k) {
+  if (!w) DUET_FAIL(DUET_ERR_INVALID_ARG, "weights are NULL");
+  for (int l = 0; l < c->spec.n_layers; ++l) {
+    const auto& W = w[l];
+    if (!W.w_qkv || !W.w_o || !W.w_gate_up || !W.w_down || !W.g_norm1 || !W.g_norm2)
+      DUET_FAIL(DUET_ERR_INVALID_ARG, "layer %d: a weight pointer is NULL", l);
+    if (c->spec.qkv_bias && !W.b_qkv) DUET_FAIL(DUET_ERR_INVALID_ARG, "layer %d: qkv_bias set but b_qkv NULL", l);
+  }
+  if (!kv || !kv->k_pool || !kv->v_pool) DUET_FAIL(DUET_ERR_INVALID_ARG, "kv pools are NULL");
+  if (kv->page_size != kPageSize) DUET_FAIL(DUET_ERR_UNSUPPORTED, "page_size = %d (must be 16)", kv->page_size);
+  for (int l = 0; l < c->spec.n_layers; ++l)
+    if (!kv->k_pool[l] || !kv->v_pool[l]) DUET_FAIL(DUET_ERR_INVALID_ARG, "layer %d: kv pool NULL", l);
+  if (kv->n_pages <= 0) DUET_FAIL(DUET_ERR_INVALID_ARG, "n_pages = %d", kv->n_pages);
+  if ((int)c->page_mark.size() < kv->n_pages) c->page_mark.assign(kv->n_pages, 0);
+  if (++c->page_gen == 0) {
+    std::fill(c->page_mark.begin(), c->page_mark.end(), 0);
+    c->page_gen = 1;
+  }
+  if (pre && pre->n_seqs > 0) {
+    if (pre->n_seqs > c->lim.max_prefill_seqs)
+      DUET_FAIL(DUET_ERR_CAPACITY, "n_seqs = %d > max_prefill_seqs %d", pre->n_seqs, c->lim.max_prefill_seqs);
+    if (!pre->q || !pre->c || !pre->page_table || !pre->x || !pre->y)
+      DUET_FAIL(DUET_ERR_INVALID_ARG, "prefill: a pointer is NULL");
+    long tot = 0;
+    for (int s = 0; s < pre->n_seqs; ++s) {
+      if (pre->q[s] < 1 || pre->c[s] < 0)
+        DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "prefill seq %d: q = %d, c = %d", s, pre->q[s], pre->c[s]);
+      if ((long)pre->c[s] + pre->q[s] > c->lim.max_pos)
+        DUET_FAIL(DUET_ERR_CAPACITY, "prefill seq %d: c + q = %ld > max_pos %d", s, (long)pre->c[s] + pre->q[s],
+                  c->lim.max_pos);
+      tot += pre->q[s];
+      DUET_TRY(check_pages(c, pre->page_table, pre->max_pages, s, pre->c[s] + pre->q[s], kv->n_pages, "prefill"));
+    }
+    if (tot > c->lim.max_prefill_tokens)
+      DUET_FAIL(DUET_ERR_CAPACITY, "prefill tokens %ld > max_prefill_tokens %d", tot, c->lim.max_prefill_tokens);
+  }
+  if (dec && dec->n_reqs > 0) {
+    if (dec->n_reqs > c->lim.max_decode_reqs)
+      DUET_FAIL(DUET_ERR_CAPACITY, "n_reqs = %d > max_decode_reqs %d", dec->n_reqs, c->lim.max_decode_reqs);
+    if (!dec->c || !dec->page_table || !dec->x || !dec->y) DUET_FAIL(DUET_ERR_INVALID_ARG, "decode: a pointer is NULL");
+    if (k > c->lim.max_k) DUET_FAIL(DUET_ERR_CAPACITY, "k = %d > max_k %d", k, c->lim.max_k);
+    for (int r = 0; r < dec->n_reqs; ++r) {
+      if (dec->c[r] < 1) DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "decode request %d: c = %d must be >= 1", r, dec->c[r]);
+      if ((long)dec->c[r] + k > c->lim.max_pos)
+        DUET_FAIL(DUET_ERR_CAPACITY, "decode request %d: c + k > max_pos %d", r, c->lim.max_pos);
+      DUET_TRY(check_pages(c, dec->page_table, dec->max_pages, r, dec->c[r] + k, kv->n_pages, "decode"));
+    }
+  }
+  return DUET_OK;
+}
+
+// ---------------------------------------------------------------------------------- metadata
+
+// Fill a side's metadata image (host) for prefill rows followed by decode rows.
+// Returns the number of ints to copy (prefix of the image up to the end of the used table rows).
+static size_t build_meta(duet_ctx* c, const Side& S, int* img, const duet_prefill* pre, const duet_decode* dec,
+                         AttnPlan* ap) {
+  int n_pre = 0, n_seqs = 0;
+  int max_q = 0, max_len_pre = 0;
+  if (pre && pre->n_seqs > 0) {
+    n_seqs = pre->n_seqs;
+    for (int s = 0; s < n_seqs; ++s) {
+      const int q = pre->q[s], cc = pre->c[s];
+      img[S.o_row0 + s] = n_pre;
+      img[S.o_qlen + s] = q;
+      img[S.o_cpre + s] = cc;
+      img[S.o_seqrow + s] = s;
+      for (int i = 0; i < q; ++i) {
+        img[S.o_pos + n_pre + i] = cc + i;
+        img[S.o_tok + n_pre + i] = s;
+      }
+      for (int j = 0; j < S.pitch; ++j)
+        img[S.o_table + (size_t)s * S.pitch + j] = j < pre->max_pages ? pre->page_table[(size_t)s * pre->max_pages + j] : 0;
+      n_pre += q;
+      max_q = std::max(max_q, q);
+      max_len_pre = std::max(max_len_pre, cc + q);
+    }
+  }
+  int n_dec = 0, max_len_dec = 0;
+  if (dec && dec->n_reqs > 0) {
+    n_dec = dec->n_reqs;
+    for (int r = 0; r < n_dec; ++r) {
+      img[S.o_pos + n_pre + r] = dec->c[r];
+      img[S.o_tok + n_pre + r] = n_seqs + r;
+      for (int j = 0; j < S.pitch; ++j)
+        img[S.o_table + (size_t)(n_seqs + r) * S.pitch + j] =
+            j < dec->max_pages ? dec->page_table[(size_t)r * dec->max_pages + j] : 0;
+      max_len_dec = std::max(max_len_dec, dec->c[r] + 1);
+    }
+  }
+  img[S.o_step] = 0;
+  {
+    const double hq = c->spec.n_q_heads, hkv = c->spec.n_kv_heads, dh = c->spec.head_dim, e = (double)dt_size(c->dt);
+    double fl = 0, by = 0;
+    if (pre)
+      for (int s = 0; s < n_seqs; ++s) {
+        const double q = pre->q[s], cc = pre->c[s];
+        fl += 4.0 * hq * dh * (q * cc + q * (q + 1) / 2);
+        by += 2.0 * q * hq * dh * e + 2.0 * hkv * dh * (cc + q) * e;
+      }
+    ap->attn_flops_pre = fl;
+    ap->attn_bytes_pre = by;
+    fl = by = 0;
+    if (dec)
+      for (int r = 0; r < n_dec; ++r) {
+        fl += 4.0 * hq * dh * (dec->c[r] + 1.0);
+        by += 2.0 * hq * dh * e + 2.0 * hkv * dh * (dec->c[r] + 1.0) * e;
+      }
+    ap->attn_flops_dec = fl;
+    ap->attn_bytes_dec = by;
+  }
+  ap->n_pre = n_pre;
+  ap->n_seqs = n_seqs;
+  ap->max_q = max_q;
+  ap->max_len_pre = max_len_pre;
+  ap->n_dec = n_dec;
+  ap->max_len_dec = max_len_dec;
+  return S.o_table + (size_t)(n_seqs + n_dec) * S.pitch;
+}
+
+static uint64_t hash_ptrs(const duet_layer_weights* w, int L, const duet_kv_pages* kv, const void* y, int maxlen_bucket) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p) {
+    h ^= (uint64_t)(uintptr_t)p;
+    h *= 1099511628211ull;
+  };
+  for (int l = 0; l < L; ++l) {
+    mix(w[l].w_qkv); mix(w[l].b_qkv); mix(w[l].w_o); mix(w[l].w_gate_up); mix(w[l].w_down);
+    mix(w[l].g_norm1); mix(w[l].g_norm2); mix(kv->k_pool[l]); mix(kv->v_pool[l]);
+  }
+  mix(y);
+  h ^= (uint64_t)maxlen_bucket * 0x9E3779B97F4A7C15ull;
+  return h;
+}
+
+// One decode step on the decode side (all layers + advance), launched on st.
+static duet_status decode_step_kernels(duet_ctx* c, cudaStream_t st, int num_sms, const duet_layer_weights* w,
+                                       const duet_kv_pages* kv, int n, int max_len, void* y_out, int* kernels) {
+  Side& S = c->dec;
+  AttnPlan ap;
+  ap.n_dec = n;
+  ap.max_len_dec = max_len;
+  DUET_TRY(run_layers(c, S, st, num_sms, n, S.xin, S.ylast, w, kv, ap, kernels));
+  *kernels += launch_decode_advance(c->dt, S.ylast, S.xin, y_out, n, c->spec.d_model, S.pos(), S.step(), st);
+  DUET_TRY(check_launch("decode advance"));
+  return DUET_OK;
+}
+
+// ---------------------------------------------------------------------------------- step
+
+extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const duet_prefill* pre,
+                                 const duet_decode* dec, const duet_kv_pages* kv, const duet_split* split,
+                                 void* stream) {
+  clear_error();
+  if (!c || !split) DUET_FAIL(DUET_ERR_INVALID_ARG, "ctx/split is NULL");
+  if (split->mode != DUET_MODE_TEMPORAL && split->mode != DUET_MODE_SPATIAL)
+    DUET_FAIL(DUET_ERR_INVALID_ARG, "split mode = %d", split->mode);
+  const bool spatial = split->mode == DUET_MODE_SPATIAL;
+  const int k = spatial ? split->k : 1;
+  if (k < 1) DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "k = %d must be >= 1", k);
+  DUET_TRY(validate_step(c, w, pre, dec, kv, k));
+  cudaStream_t ust = (cudaStream_t)stream;
+  const bool has_pre = pre && pre->n_seqs > 0;
+  const bool has_dec = dec && dec->n_reqs > 0;
+  const size_t es = dt_size(c->dt);
+  const int d = c->spec.d_model;
+  int kernels = 0;
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->last_has_dec = has_dec;
+  c->last_has_pre = has_pre;
+  c->last_mode = split->mode;
+  c->last_k = k;
+
+  if (!spatial) {
+    // ---------------- temporal (aggregated) mode: one full-device stream, k = 1
+    int* img;
+    int slot;
+    DUET_TRY(stage_slot(c, &img, &slot));
+    AttnPlan ap;
+    const size_t n_int = build_meta(c, c->pre, img, pre, dec, &ap);
+    const int n_rows = ap.n_pre + ap.n_dec;
+    cudaStream_t st = c->s_full;
+    CUDA_TRY(cudaEventRecord(c->ev_in, ust));
+    CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in, 0));
+    CUDA_TRY(cudaEventRecord(c->ev_pre0, st));
+    CUDA_TRY(cudaMemcpyAsync(c->pre.meta, img, n_int * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaEventRecord(c->stage_ev[slot], st));
+    if (n_rows > 0) {
+      if (has_pre) CUDA_TRY(cudaMemcpyAsync(c->pre.xin, pre->x, (size_t)ap.n_pre * d * es, cudaMemcpyDeviceToDevice, st));
+      if (has_dec)
+        CUDA_TRY(cudaMemcpyAsync((char*)c->pre.xin + (size_t)ap.n_pre * d * es, dec->x, (size_t)ap.n_dec * d * es,
+                                 cudaMemcpyDeviceToDevice, st));
+      DUET_TRY(run_layers(c, c->pre, st, c->total_sms, n_rows, c->pre.xin, c->pre.ylast, w, kv, ap, &kernels));
+      if (has_pre) CUDA_TRY(cudaMemcpyAsync(pre->y, c->pre.ylast, (size_t)ap.n_pre * d * es, cudaMemcpyDeviceToDevice, st));
+      if (has_dec)
+        CUDA_TRY(cudaMemcpyAsync(dec->y, (char*)c->pre.ylast + (size_t)ap.n_pre * d * es, (size_t)ap.n_dec * d * es,
+                                 cudaMemcpyDeviceToDevice, st));
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_pre1, st));
+    CUDA_TRY(cudaStreamWaitEvent(ust, c->ev_pre1, 0));
+    c->last_kernels = kernels;
+    return DUET_OK;
+  }
+
+  // ---------------- spatial mode (Alg. 1 l.22; §4.3)
+  Partition* P = nullptr;
+  for (auto& p : c->parts)
+    if (p.s_d == split->s_d) P = &p;
+  if (!P) DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "s_d = %d is not an achievable partition size", split->s_d);
+  DUET_TRY(ensure_partition(c, *P));
+  CUDA_TRY(cudaEventRecord(c->ev_in, ust));
+
+  if (has_dec) {
+    // decode FIRST: metadata, input copy, then k graph replays with no host sync
+    int* img;
+    int slot;
+    DUET_TRY(stage_slot(c, &img, &slot));
+    AttnPlan ap;
+    const size_t n_int = build_meta(c, c->dec, img, nullptr, dec, &ap);
+    cudaStream_t st = P->s_dec;
+    CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in, 0));
+    CUDA_TRY(cudaEventRecord(c->ev_dec0, st));
+    CUDA_TRY(cudaMemcpyAsync(c->dec.meta, img, n_int * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaEventRecord(c->stage_ev[slot], st));
+    const int n = ap.n_dec;
+    CUDA_TRY(cudaMemcpyAsync(c->dec.xin, dec->x, (size_t)n * d * es, cudaMemcpyDeviceToDevice, st));
+    int max_c = 0;
+    for (int r = 0; r < n; ++r) max_c = std::max(max_c, dec->c[r]);
+    const int max_len = ((max_c + k + 1023) / 1024) * 1024;  // bucket: graphs survive context growth
+    if (c->lim.flags & DUET_CTX_NO_GRAPH) {
+      for (int j = 0; j < k; ++j)
+        DUET_TRY(decode_step_kernels(c, st, P->s_d, w, kv, n, max_len, dec->y, &kernels));
+    } else {
+      auto key = std::make_tuple(P->s_d, n, c->spec.n_layers, hash_ptrs(w, c->spec.n_layers, kv, dec->y, max_len));
+      auto it = c->graphs.find(key);
+      if (it == c->graphs.end()) {
+        cudaStream_t cap = P->s_dec;
+        cudaGraph_t graph;
+        int nk = 0;
+        CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        c->capturing = true;
+        duet_status s = decode_step_kernels(c, cap, P->s_d, w, kv, n, max_len, dec->y, &nk);
+        c->capturing = false;
+        cudaError_t e = cudaStreamEndCapture(cap, &graph);
+        if (s != DUET_OK) return s;
+        if (e != cudaSuccess) DUET_FAIL(DUET_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+        GraphEntry ge;
+        ge.kernels = nk;
+        e = cudaGraphInstantiate(&ge.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) DUET_FAIL(DUET_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+        it = c->graphs.emplace(key, ge).first;
+      }
+      for (int j = 0; j < k; ++j) CUDA_TRY(cudaGraphLaunch(it->second.exec, st));
+      kernels += k * it->second.kernels;
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_dec1, st));
+  }
+  if (has_pre) {
+    int* img;
+    int slot;
+    DUET_TRY(stage_slot(c, &img, &slot));
+    AttnPlan ap;
+    const size_t n_int = build_meta(c, c->pre, img, pre, nullptr, &ap);
+    cudaStream_t st = P->s_pre;
+    CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in, 0));
+    CUDA_TRY(cudaEventRecord(c->ev_pre0, st));
+    CUDA_TRY(cudaMemcpyAsync(c->pre.meta, img, n_int * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaEventRecord(c->stage_ev[slot], st));
+    DUET_TRY(run_layers(c, c->pre, st, P->s_p, ap.n_pre, pre->x, pre->y, w, kv, ap, &kernels));
+    CUDA_TRY(cudaEventRecord(c->ev_pre1, st));
+  }
+  // join (a7): the caller's stream waits for both sides; no host sync
+  if (has_dec) CUDA_TRY(cudaStreamWaitEvent(ust, c->ev_dec1, 0));
+  if (has_pre) CUDA_TRY(cudaStreamWaitEvent(ust, c->ev_pre1, 0));
+  c->last_kernels = kernels;
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_last_step_times(duet_ctx* c, duet_step_times* out) {
+  clear_error();
+  if (!c || !out) DUET_FAIL(DUET_ERR_INVALID_ARG, "ctx/out is NULL");
+  if (c->last_mode < 0) DUET_FAIL(DUET_ERR_INVALID_ARG, "no step has run");
+  std::memset(out, 0, sizeof *out);
+  out->mode = c->last_mode;
+  out->k = c->last_k;
+  out->kernels = c->last_kernels;
+  float ms = 0;
+  if (c->last_mode == DUET_MODE_TEMPORAL) {
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_pre0, c->ev_pre1));
+    out->t_window = out->t_decode = out->t_prefill = ms * 1e-3;
+    return DUET_OK;
+  }
+  float td = 0, tp = 0, w = 0;
+  if (c->last_has_dec) CUDA_TRY(cudaEventElapsedTime(&td, c->ev_dec0, c->ev_dec1));
+  if (c->last_has_pre) CUDA_TRY(cudaEventElapsedTime(&tp, c->ev_pre0, c->ev_pre1));
+  if (c->last_has_dec && c->last_has_pre) {
+    // window: first start -> last end
+    float a = 0, b = 0;
+    CUDA_TRY(cudaEventElapsedTime(&a, c->ev_dec0, c->ev_pre1));  // pre end rel. dec start
+    CUDA_TRY(cudaEventElapsedTime(&b, c->ev_dec0, c->ev_pre0));  // pre start rel. dec start
+    const float start = std::min(0.f, b);
+    const float end = std::max(td, a);
+    w = end - start;
+  } else {
+    w = c->last_has_dec ? td : tp;
+  }
+  out->t_window = w * 1e-3;
+  out->t_decode = td * 1e-3;
+  out->t_prefill = tp * 1e-3;
+  return DUET_OK;
+}
+
+// ---------------------------------------------------------------------------------- single ops
+
+extern "C" duet_status duet_op_gemm(duet_ctx* c, const void* A, const void* B, void* C, const void* R,
+                                    const void* bias, int32_t M, int32_t N, int32_t K, int32_t epi, void* stream) {
+  clear_error();
+  if (!c || !A || !B || !C) DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL operand");
+  if (M < 0 || N <= 0 || K <= 0 || K % 16) DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "shape M=%d N=%d K=%d (K %% 16 == 0)", M, N, K);
+  if (epi < 0 || epi > 2) DUET_FAIL(DUET_ERR_INVALID_ARG, "epi = %d", epi);
+  if (epi == DUET_EPI_RESIDUAL && !R) DUET_FAIL(DUET_ERR_INVALID_ARG, "residual epilogue needs R");
+  GemmArgs g{A, B, C, R, bias, M, N, K, K, K, N, N, epi};
+  launch_gemm(c->dt, g, c->total_sms, (cudaStream_t)stream);
+  DUET_TRY(check_launch("gemm"));
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_op_rmsnorm(duet_ctx* c, const void* x, const void* g, void* h, int32_t n, void* stream) {
+  clear_error();
+  if (!c || !x || !g || !h) DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL operand");
+  launch_rmsnorm(c->dt, x, g, h, n, c->spec.d_model, (float)c->spec.norm_eps, (cudaStream_t)stream);
+  DUET_TRY(check_launch("rmsnorm"));
+  return DUET_OK;
+}
+
+// ---------------------------------------------------------------------------------- calibration
+
+extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, int32_t len) {
+  clear_error();
+  if (!c || !flops || !bw) DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL argument");
+  if (len < c->total_sms + 1) DUET_FAIL(DUET_ERR_CAPACITY, "tables need %d entries", c->total_sms + 1);
+  for (auto& p : c->parts) DUET_TRY(ensure_partition(c, p));
+  const size_t n_bytes = (size_t)2 << 30;
+  void* buf = nullptr;
+  unsigned long long* sink = nullptr;
+  CUDA_TRY(cudaMalloc(&buf, n_bytes));
+  CUDA_TRY(cudaMemset(buf, 1, n_bytes));
+  CUDA_TRY(cudaMalloc(&sink, 4096 * sizeof(unsigned long long)));
+  const int G = 8192;
+  const size_t es = dt_size(c->dt);
+  void *A = nullptr, *B = nullptr, *C = nullptr;
+  CUDA_TRY(cudaMalloc(&A, (size_t)G * G * es));
+  CUDA_TRY(cudaMalloc(&B, (size_t)G * G * es));
+  CUDA_TRY(cudaMalloc(&C, (size_t)G * G * es));
+  CUDA_TRY(cudaMemset(A, 0, (size_t)G * G * es));
+  CUDA_TRY(cudaMemset(B, 0, (size_t)G * G * es));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  std::vector<double> mf(c->total_sms + 1, 0.0), mb(c->total_sms + 1, 0.0);
+  auto measure = [&](cudaStream_t st, int sms) -> duet_status {
+    if (mf[sms] > 0) return DUET_OK;
+    std::vector<float> tb, tf;
+    for (int rep = 0; rep < 7; ++rep) {
+      CUDA_TRY(cudaEventRecord(e0, st));
+      launch_stream_read(buf, n_bytes, sink, sms, st);
+      CUDA_TRY(cudaEventRecord(e1, st));
+      CUDA_TRY(cudaEventSynchronize(e1));
+      float ms;
+      CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+      tb.push_back(ms);
+    }
+    GemmArgs g{A, B, C, nullptr, nullptr, G, G, G, G, G, G, 0, EPI_STORE};
+    const int reps = c->dt == DT::BF16 ? 5 : 1;
+    for (int rep = 0; rep < reps; ++rep) {
+      CUDA_TRY(cudaEventRecord(e0, st));
+      launch_gemm(c->dt, g, sms, st);
+      CUDA_TRY(cudaEventRecord(e1, st));
+      CUDA_TRY(cudaEventSynchronize(e1));
+      float ms;
+      CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+      tf.push_back(ms);
+    }
+    DUET_TRY(check_launch("calibration"));
+    std::sort(tb.begin(), tb.end());
+    std::sort(tf.begin(), tf.end());
+    mb[sms] = (double)n_bytes / (tb[tb.size() / 2] * 1e-3);
+    mf[sms] = 2.0 * G * (double)G * G / (tf[tf.size() / 2] * 1e-3);
+    return DUET_OK;
+  };
+  DUET_TRY(measure(c->s_full, c->total_sms));
+  for (auto& p : c->parts) {
+    DUET_TRY(measure(p.s_dec, p.s_d));
+    DUET_TRY(measure(p.s_pre, p.s_p));
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  cudaFree(sink);
+  cudaFree(A);
+  cudaFree(B);
+  cudaFree(C);
+  // fill unmeasured sizes by linear interpolation (from 0 at S = 0)
+  std::vector<int> known;
+  for (int s = 1; s <= c->total_sms; ++s)
+    if (mf[s] > 0) known.push_back(s);
+  for (int s = 0; s <= c->total_sms; ++s) {
+    if (s == 0) {
+      flops[0] = bw[0] = 0.0;
+      continue;
+    }
+    if (mf[s] > 0) {
+      flops[s] = mf[s];
+      bw[s] = mb[s];
+      continue;
+    }
+    int lo = 0, hi = -1;
+    for (int kx : known) {
+      if (kx < s) lo = kx;
+      if (kx > s && hi < 0) hi = kx;
+    }
+    if (hi < 0) hi = known.back();
+    const double f_lo = lo ? mf[lo] : 0.0, b_lo = lo ? mb[lo] : 0.0;
+    const double t = (double)(s - lo) / (double)(hi - lo);
+    flops[s] = f_lo + t * (mf[hi] - f_lo);
+    bw[s] = b_lo + t * (mb[hi] - b_lo);
+  }
+  for (int s = c->total_sms + 1; s < len; ++s) flops[s] = bw[s] = 0.0;
+  return DUET_OK;
+}
+
+// ---------------------------------------------------------------------------------- live timing
+
+extern "C" duet_status duet_profile_enable(duet_ctx* c, int32_t enable) {
+  clear_error();
+  if (!c) DUET_FAIL(DUET_ERR_INVALID_ARG, "ctx is NULL");
+  c->prof_on = enable != 0;
+  c->prof_pending.clear();
+  c->prof_used = 0;
+  for (auto& s : c->prof_acc) s = duet_kernel_stats{};
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_profile_read(duet_ctx* c, duet_kernel_stats* out) {
+  clear_error();
+  if (!c || !out) DUET_FAIL(DUET_ERR_INVALID_ARG, "ctx/out is NULL");
+  for (const auto& r : c->prof_pending) {
+    const auto& ev = c->prof_pool[r.idx];
+    CUDA_TRY(cudaEventSynchronize(ev.second));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, ev.first, ev.second));
+    auto& a = c->prof_acc[r.cls];
+    a.launches += 1;
+    a.seconds += ms * 1e-3;
+    a.flops += r.flops;
+    a.bytes += r.bytes;
+  }
+  c->prof_pending.clear();
+  c->prof_used = 0;
+  for (int i = 0; i < DUET_KCLASS_N; ++i) out[i] = c->prof_acc[i];
+  return DUET_OK;
+}

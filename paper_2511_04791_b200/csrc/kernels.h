@@ -1,0 +1,121 @@
+// Internal launcher interface between the step orchestration (duet_ctx.cu) and the sm_100a
+// kernels (kernels_*.cu).  Not part of the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace duet {
+
+enum class DT : int { BF16 = 0, F32 = 1 };
+
+inline size_t dt_size(DT t) { return t == DT::BF16 ? 2 : 4; }
+
+// ---------------------------------------------------------------- GEMM
+// C[M][N] (ldc) = epi(A[M][K] (lda) . B[N][K]^T (ldb)).  Both operands K-major (nn.Linear).
+//  EPI_STORE:    C = acc (+ bias[n])
+//  EPI_RESIDUAL: C = R[m][n] (ldr) + acc
+//  EPI_SWIGLU:   B has rows [gate(N) ; up(N)] (gate row j at j, up row j at N + j);
+//                C[m][j] = silu(acc_gate) * acc_up
+enum { EPI_STORE = 0, EPI_RESIDUAL = 1, EPI_SWIGLU = 2 };
+
+struct GemmArgs {
+  const void* A;
+  const void* B;
+  void* C;
+  const void* R;
+  const void* bias;
+  int M, N, K;
+  int lda, ldb, ldc, ldr;
+  int epi;
+};
+
+// num_sms: SMs of the partition the launch runs in (persistent grid sizing).
+// Returns the number of kernels launched (0 on a launch error, checked by the caller).
+int launch_gemm(DT dt, const GemmArgs& a, int num_sms, cudaStream_t st);
+int launch_gemm_simt(DT dt, const GemmArgs& a, cudaStream_t st);
+int launch_gemm_tc(const GemmArgs& a, int num_sms, cudaStream_t st);
+bool gemm_tc_supported(const GemmArgs& a);
+
+// ---------------------------------------------------------------- RMSNorm
+// h[n][d] = x * rsqrt(mean(x^2) + eps) * g     (reading #1)
+int launch_rmsnorm(DT dt, const void* x, const void* g, void* h, int n, int d, float eps, cudaStream_t st);
+
+// ---------------------------------------------------------------- RoPE + paged KV append
+// qkv rows [n][(hq + 2 hkv) dh]; row i at position pos[i], page-table row tok_row[i].
+// q heads are rotated in place; rotated k and v go to slot (table[row][p/P], p%P) of the
+// layer's pools [n_pages][hkv][P][dh].  rope: [max_pos][dh/2] float2 (cos, sin).
+struct RopeKvArgs {
+  void* qkv;
+  const void* bias;  // [(hq + 2 hkv) dh] or nullptr: added before rotation
+  int n, hq, hkv, dh;
+  const int* pos;
+  const int* tok_row;
+  const int* table;
+  int max_pages, page_size;
+  void* k_pool;
+  void* v_pool;
+  const float2* rope;
+};
+int launch_rope_kv(DT dt, const RopeKvArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- decode attention
+// o[r][hq*dh] = softmax(q_r . K / sqrt(dh)) . V over positions 0..pos[r] of request r
+// (tok_row[r] selects its page-table row).  Split-K over pages with an LSE combine.
+struct DecodeAttnArgs {
+  const void* q;  // row stride q_stride (elements); head j at column j*dh
+  int q_stride;
+  void* o;        // [n][hq*dh]
+  int n, hq, hkv, dh;
+  const int* pos;
+  const int* tok_row;
+  const int* table;
+  int max_pages, page_size;
+  const void* k_pool;
+  const void* v_pool;
+  float* part_o;    // workspace [n][hq][max_splits][dh]
+  float* part_ml;   // workspace [n][hq][max_splits][2]
+  int max_splits;
+  int num_sms;
+  int max_len;      // upper bound of pos[r] + 1 over the batch (host-known), for split sizing
+};
+int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- prefill attention
+// Causal attention of the chunk rows over prefix + chunk (reading #7): sequence s has rows
+// [row0[s], row0[s] + qlen[s]) at positions cpre[s] + i and reads KV from page-table row
+// seq_row[s]; the chunk's own K/V are already in the pages.
+struct PrefillAttnArgs {
+  const void* q;
+  int q_stride;
+  void* o;
+  int n_seqs, hq, hkv, dh;
+  const int* row0;
+  const int* qlen;
+  const int* cpre;
+  const int* seq_row;
+  const int* table;
+  int max_pages, page_size;
+  const void* k_pool;
+  const void* v_pool;
+  int max_q;   // host-known max qlen (grid sizing)
+  int total_q; // host-known sum of qlen
+  int num_sms;
+  // per-row view (SIMT path): row i at position tok_pos[i], page-table row tok_row[i]
+  const int* tok_pos;
+  const int* tok_row;
+  int max_len;  // host-known max(c + q) over the sequences
+};
+int launch_prefill_attn(DT dt, const PrefillAttnArgs& a, cudaStream_t st);
+bool fa_prefill_supported(const PrefillAttnArgs& a);
+int launch_fa_prefill(const PrefillAttnArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- decode window bookkeeping
+// End of one decode step (P:335 look-ahead): y_out[step][r] = y[r]; xin[r] = y[r];
+// pos[r] += 1; step += 1.  Reads *step on device so a captured graph can be replayed k times.
+int launch_decode_advance(DT dt, const void* y, void* xin, void* y_out, int n, int d, int* pos, int* step,
+                          cudaStream_t st);
+
+// Streaming-read kernel for B_HBM(S) calibration: reads n_bytes, writes one word per CTA.
+int launch_stream_read(const void* buf, size_t n_bytes, unsigned long long* sink, int num_sms, cudaStream_t st);
+
+}  // namespace duet

@@ -1,0 +1,169 @@
+// Row / element kernels of the layer: RMSNorm (reading #1), RoPE + paged KV append
+// (readings #5, C-3), decode-window bookkeeping and the streaming-read
+// calibration kernel.
+#include "dev_common.cuh"
+#include "kernels.h"
+
+namespace duet {
+
+// ---------------------------------------------------------------- RMSNorm
+// One CTA per row; 16-byte vector loads; fp32 sum of squares; h stored in T.
+template <typename T, int THREADS>
+__global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const T* __restrict__ x, const T* __restrict__ g,
+                                                          T* __restrict__ h, int d, float eps) {
+  constexpr int E = 16 / sizeof(T);
+  const int row = blockIdx.x;
+  const T* xr = x + (size_t)row * d;
+  T* hr = h + (size_t)row * d;
+  const int nv = d / E;
+  float ss = 0.f;
+  for (int v = threadIdx.x; v < nv; v += THREADS) {
+    float f[E];
+    load16<T>(xr + v * E, f);
+#pragma unroll
+    for (int e = 0; e < E; ++e) ss += f[e] * f[e];
+  }
+  __shared__ float red[THREADS / 32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < THREADS / 32 ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float r = rsqrtf(red[0] / (float)d + eps);
+  for (int v = threadIdx.x; v < nv; v += THREADS) {
+    float f[E], gg[E];
+    load16<T>(xr + v * E, f);
+    load16<T>(g + v * E, gg);
+#pragma unroll
+    for (int e = 0; e < E; ++e) f[e] = f[e] * r * gg[e];
+    store16<T>(hr + v * E, f);
+  }
+}
+
+int launch_rmsnorm(DT dt, const void* x, const void* g, void* h, int n, int d, float eps, cudaStream_t st) {
+  if (n <= 0) return 0;
+  if (dt == DT::BF16)
+    rmsnorm_kernel<bf16, 256><<<n, 256, 0, st>>>((const bf16*)x, (const bf16*)g, (bf16*)h, d, eps);
+  else
+    rmsnorm_kernel<float, 256><<<n, 256, 0, st>>>((const float*)x, (const float*)g, (float*)h, d, eps);
+  return 1;
+}
+
+// ---------------------------------------------------------------- RoPE + KV append
+// One CTA per token row.  Work items: (head, i) pairs of the q and k heads (rotation of the
+// NeoX halves i, i + dh/2) and (head, e) elements of the v heads.
+template <typename T>
+__global__ void rope_kv_kernel(RopeKvArgs a) {
+  const int row = blockIdx.x;
+  T* qkv = reinterpret_cast<T*>(a.qkv) + (size_t)row * (a.hq + 2 * a.hkv) * a.dh;
+  const T* bias = reinterpret_cast<const T*>(a.bias);
+  const int p = a.pos[row];
+  const int trow = a.tok_row[row];
+  const int page = a.table[(size_t)trow * a.max_pages + p / a.page_size];
+  const int slot = p % a.page_size;
+  const int half = a.dh / 2;
+  const float2* rp = a.rope + (size_t)p * half;
+  T* kp = reinterpret_cast<T*>(a.k_pool);
+  T* vp = reinterpret_cast<T*>(a.v_pool);
+  const int n_rot = (a.hq + a.hkv) * half;
+  const int n_all = n_rot + a.hkv * a.dh;
+  for (int t = threadIdx.x; t < n_all; t += blockDim.x) {
+    if (t < n_rot) {
+      const int head = t / half, i = t % half;
+      const int c0 = head * a.dh + i, c1 = c0 + half;
+      float x0 = to_f(qkv[c0]), x1 = to_f(qkv[c1]);
+      if (bias) {
+        x0 += to_f(bias[c0]);
+        x1 += to_f(bias[c1]);
+      }
+      const float2 cs = rp[i];
+      const float y0 = x0 * cs.x - x1 * cs.y;
+      const float y1 = x1 * cs.x + x0 * cs.y;
+      if (head < a.hq) {
+        qkv[c0] = from_f<T>(y0);
+        qkv[c1] = from_f<T>(y1);
+      } else {
+        const int kh = head - a.hq;
+        T* dst = kp + (((size_t)page * a.hkv + kh) * a.page_size + slot) * a.dh;
+        dst[i] = from_f<T>(y0);
+        dst[i + half] = from_f<T>(y1);
+      }
+    } else {
+      const int u = t - n_rot;
+      const int vh = u / a.dh, e = u % a.dh;
+      const int c = (a.hq + a.hkv + vh) * a.dh + e;
+      float v = to_f(qkv[c]);
+      if (bias) v += to_f(bias[c]);
+      vp[(((size_t)page * a.hkv + vh) * a.page_size + slot) * a.dh + e] = from_f<T>(v);
+    }
+  }
+}
+
+int launch_rope_kv(DT dt, const RopeKvArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return 0;
+  if (dt == DT::BF16)
+    rope_kv_kernel<bf16><<<a.n, 256, 0, st>>>(a);
+  else
+    rope_kv_kernel<float><<<a.n, 256, 0, st>>>(a);
+  return 1;
+}
+
+// ---------------------------------------------------------------- decode window advance
+template <typename T>
+__global__ void decode_advance_kernel(const T* __restrict__ y, T* __restrict__ xin, T* __restrict__ y_out, int n,
+                                      int d, int* pos, int* step) {
+  const int s = *step;
+  const size_t total = (size_t)n * d;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const T v = y[i];
+    y_out[(size_t)s * total + i] = v;
+    xin[i] = v;
+  }
+}
+__global__ void decode_bump_kernel(int n, int* pos, int* step) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) pos[i] += 1;
+  if (i == 0) *step += 1;
+}
+
+int launch_decode_advance(DT dt, const void* y, void* xin, void* y_out, int n, int d, int* pos, int* step,
+                          cudaStream_t st) {
+  if (n <= 0) return 0;
+  const int blocks = (int)(((size_t)n * d + 1023) / 1024) < 64 ? (int)(((size_t)n * d + 1023) / 1024) : 64;
+  if (dt == DT::BF16)
+    decode_advance_kernel<bf16><<<blocks, 1024, 0, st>>>((const bf16*)y, (bf16*)xin, (bf16*)y_out, n, d, pos, step);
+  else
+    decode_advance_kernel<float><<<blocks, 1024, 0, st>>>((const float*)y, (float*)xin, (float*)y_out, n, d, pos,
+                                                          step);
+  decode_bump_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, pos, step);
+  return 2;
+}
+
+// ---------------------------------------------------------------- calibration: streaming read
+__global__ void __launch_bounds__(512) stream_read_kernel(const uint4* __restrict__ buf, size_t n_vec,
+                                                          unsigned long long* sink) {
+  uint32_t acc = 0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n_vec; i += 4 * stride) {
+    uint4 a = ldg_nc16(buf + i), b = ldg_nc16(buf + i + stride), c = ldg_nc16(buf + i + 2 * stride),
+          e = ldg_nc16(buf + i + 3 * stride);
+    acc ^= a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w ^ c.x ^ c.y ^ c.z ^ c.w ^ e.x ^ e.y ^ e.z ^ e.w;
+  }
+  for (; i < n_vec; i += stride) {
+    uint4 a = ldg_nc16(buf + i);
+    acc ^= a.x ^ a.y ^ a.z ^ a.w;
+  }
+  if (acc == 0x9E3779B9u) sink[blockIdx.x] = acc;  // practically never taken; keeps the loads alive
+}
+
+int launch_stream_read(const void* buf, size_t n_bytes, unsigned long long* sink, int num_sms, cudaStream_t st) {
+  stream_read_kernel<<<num_sms * 4, 512, 0, st>>>((const uint4*)buf, n_bytes / 16, sink);
+  return 1;
+}
+
+}  // namespace duet

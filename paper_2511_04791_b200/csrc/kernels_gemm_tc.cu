@@ -1,0 +1,380 @@
+// tcgen05 / TMEM / TMA GEMM for sm_100a — the token-level linear operators of the layer
+// (QKV, O, gate-up, down; §2, §4.1), bf16 in, fp32 accumulation in
+// tensor memory, fused epilogues (bias, residual add, SwiGLU).
+//
+// C[M][N] = epi(A[M][K] . B[N][K]^T), A and B K-major (nn.Linear layout).
+// Persistent, warp-specialized, one CTA per SM (cta_group::1):
+//   warp 0      TMA producer: 128x64 A tile + BNx64 B tile per stage (SWIZZLE_128B), S-stage ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (UMMA 128xBNx16)
+//   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per load) -> fused op -> global
+// Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap the MMAs of i+1.
+// Tiles are assigned statically (tile = blockIdx.x + j * gridDim.x, m fastest) and every output
+// element is reduced over K in one fixed order, so results do not depend on the grid size
+// (i.e. on the SM partition the kernel runs in).
+#include <cuda.h>
+
+#include "dev_common.cuh"
+#include "kernels.h"
+
+namespace duet {
+
+namespace tc {
+
+constexpr int BM = 128, BK = 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B (rows of 128 B, 8-row atoms of 1 KiB):
+// start >> 4 | LBO = 1 (unused for swizzled K-major) | SBO = 1024 B >> 4 | version 1 | layout 2.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) |
+         ((uint64_t)2 << 61);
+}
+
+// Instruction descriptor, kind::f16: D = f32 (bits 4-5 = 1), A = B = bf16 (bits 7-9, 10-12 = 1),
+// both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct Params {
+  int M, N, K;       // N = output columns (SwiGLU: width of act)
+  int num_m, num_n, num_tiles;
+  bf16* C;
+  const bf16* R;
+  const bf16* bias;
+  int ldc, ldr;
+  int n_up_off;      // SwiGLU: row offset of the up rows in B (= N)
+};
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p) {
+  using CF = Cfg<BN>;
+  constexpr int S = CF::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * CF::A_BYTES;
+  uint64_t* full = (uint64_t*)(smem + S * CF::STAGE_BYTES);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_k = p.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_a);
+    prefetch_map(&map_b);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(CF::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const int mb = t % p.num_m, nb = t / p.num_m;
+        const int m0 = mb * BM;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], CF::STAGE_BYTES);
+          tma_load_2d(&map_a, &full[s], sA + s * CF::A_BYTES, kb * BK, m0);
+          if constexpr (EPI == EPI_SWIGLU) {
+            const int j0 = nb * (BN / 2);
+            tma_load_2d(&map_b, &full[s], sB + s * CF::B_BYTES, kb * BK, j0);
+            tma_load_2d(&map_b, &full[s], sB + s * CF::B_BYTES + (BN / 2) * BK * 2, kb * BK, p.n_up_off + j0);
+          } else {
+            tma_load_2d(&map_b, &full[s], sB + s * CF::B_BYTES, kb * BK, nb * BN);
+          }
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+      int s = 0;
+      uint32_t ph = 0;
+      int i = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++i) {
+        const int acc = i & 1;
+        const uint32_t aph = (i >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * CF::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + s * CF::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (kb | k) != 0);
+          umma_commit(&empty[s]);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5: TMEM lane quadrant = warp % 4
+    const int quad = warp & 3;
+    const int row_in_tile = quad * 32 + lane;
+    int i = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++i) {
+      const int acc = i & 1;
+      const uint32_t aph = (i >> 1) & 1;
+      const int mb = t % p.num_m, nb = t / p.num_m;
+      const int row = mb * BM + row_in_tile;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      constexpr int OUT_COLS = EPI == EPI_SWIGLU ? BN / 2 : BN;
+      const int n0 = nb * OUT_COLS;
+#pragma unroll 1
+      for (int c = 0; c < OUT_COLS; c += 32) {
+        float v[32];
+        tmem_ld32(tbase + c, v);
+        if constexpr (EPI == EPI_SWIGLU) {
+          float u[32];
+          tmem_ld32(tbase + BN / 2 + c, u);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = silu_f(v[e]) * u[e];
+        }
+        if (row < p.M && n0 + c < p.N) {
+          bf16* dst = p.C + (size_t)row * p.ldc + n0 + c;
+          if (n0 + c + 32 <= p.N) {
+            if constexpr (EPI == EPI_RESIDUAL) {
+              const bf16* rsrc = p.R + (size_t)row * p.ldr + n0 + c;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                float rf[8];
+                load16<bf16>(rsrc + q * 8, rf);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[q * 8 + e] += rf[e];
+              }
+            } else if constexpr (EPI == EPI_STORE) {
+              if (p.bias) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  float bf[8];
+                  load16<bf16>(p.bias + n0 + c + q * 8, bf);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) v[q * 8 + e] += bf[e];
+                }
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float o8[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) o8[e] = v[q * 8 + e];
+              store16<bf16>(dst + q * 8, o8);
+            }
+          } else {
+            for (int e = 0; e < 32 && n0 + c + e < p.N; ++e) {
+              float o = v[e];
+              if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)row * p.ldr + n0 + c + e]);
+              if constexpr (EPI == EPI_STORE)
+                if (p.bias) o += __bfloat162float(p.bias[n0 + c + e]);
+              dst[e] = __float2bfloat16_rn(o);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(CF::TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------------- host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  }
+  return fn;
+}
+
+// 2-D bf16 map over a row-major [rows][cols] matrix with row pitch ld (elements); box = 64 x box_rows.
+static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, int EPI>
+static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
+  using CF = Cfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+    attr_set = true;
+  }
+  CUtensorMap ma, mb;
+  const int b_rows = EPI == EPI_SWIGLU ? 2 * a.N : a.N;
+  const int b_box = EPI == EPI_SWIGLU ? BN / 2 : BN;
+  if (!make_map(&ma, a.A, a.M, a.K, a.lda, BM)) return -1;
+  if (!make_map(&mb, a.B, b_rows, a.K, a.ldb, b_box)) return -1;
+  Params p{};
+  p.M = a.M;
+  p.N = a.N;
+  p.K = a.K;
+  const int out_cols = EPI == EPI_SWIGLU ? BN / 2 : BN;
+  p.num_m = (a.M + BM - 1) / BM;
+  p.num_n = (a.N + out_cols - 1) / out_cols;
+  p.num_tiles = p.num_m * p.num_n;
+  p.C = (bf16*)a.C;
+  p.R = (const bf16*)a.R;
+  p.bias = (const bf16*)a.bias;
+  p.ldc = a.ldc;
+  p.ldr = a.ldr;
+  p.n_up_off = a.N;
+  const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
+  gemm_tc_kernel<BN, EPI><<<grid, 192, CF::SMEM, st>>>(ma, mb, p);
+  return 1;
+}
+
+}  // namespace tc
+
+bool gemm_tc_supported(const GemmArgs& a) {
+  // K in whole 64-element blocks; 16-byte aligned rows for TMA and vector epilogue loads
+  if (a.K % tc::BK || a.M <= 0) return false;
+  if (a.lda % 8 || a.ldb % 8 || a.ldc % 8 || (a.R && a.ldr % 8)) return false;
+  if (a.epi == EPI_SWIGLU && a.N % 128) return false;
+  if (!tc::encode_fn()) return false;
+  return true;
+}
+
+int launch_gemm_tc(const GemmArgs& a, int num_sms, cudaStream_t st) {
+  if (a.epi == EPI_SWIGLU) return tc::launch<256, EPI_SWIGLU>(a, num_sms, st);
+  if (a.epi == EPI_RESIDUAL) return tc::launch<256, EPI_RESIDUAL>(a, num_sms, st);
+  return tc::launch<256, EPI_STORE>(a, num_sms, st);
+}
+
+}  // namespace duet

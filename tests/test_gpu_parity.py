@@ -1,0 +1,228 @@
+"""GPU parity: libduet.so (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star; C-6): normwise max relative error <= 2e-2 for bf16
+kernels, <= 1e-4 for the fp32 path.  Bit-exact: KV slot placement (NaN-poisoned pool: exactly
+the listed slots change), and results across every SM split and mode (split invariance).
+"""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2511_04791_b200 as D
+from synth import configs, workload
+from tests.gpu_helpers import GpuWorkload, make_ctx
+from tests.oracle_run import rel_err, run
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-4, "bf16": 2e-2}
+
+
+def _check_outputs(g: GpuWorkload, y_pre, y_dec, tol):
+    if len(g.wl.pre_seqs):
+        e = rel_err(g.y_pre.float().cpu().numpy(), y_pre)
+        assert e <= tol, f"prefill rel err {e}"
+    if len(g.wl.dec_ctx):
+        for j in range(g.wl.k):
+            e = rel_err(g.y_dec[j].float().cpu().numpy(), y_dec[j])
+            assert e <= tol, f"decode step {j + 1} rel err {e}"
+
+
+def _check_kv(g: GpuWorkload, kv_oracle, tol):
+    """Written slots match the oracle's writes; every other slot keeps its poison / history."""
+    wl = g.wl
+    written = set(kv_oracle.writes)
+    for l in range(wl.n_layers):
+        Kg = g.K[l].float().cpu().numpy()
+        Vg = g.V[l].float().cpu().numpy()
+        hist = np.zeros((wl.n_pages, wl.cfg.batch.page_size), dtype=bool)
+        for (ll, trow, uid, n) in wl.history_items():
+            if ll == l:
+                p = np.arange(n)
+                hist[trow[p // 16], p % 16] = True
+        wmask = np.zeros_like(hist)
+        for (ll, page, s) in written:
+            if ll == l:
+                wmask[page, s] = True
+        untouched = ~(hist | wmask)
+        assert np.all(np.isnan(Kg.transpose(0, 2, 1, 3)[untouched])), "a slot outside the write list changed"
+        assert np.all(np.isnan(Vg.transpose(0, 2, 1, 3)[untouched]))
+        Kw = Kg.transpose(0, 2, 1, 3)[wmask]
+        Ko = kv_oracle.K[l].transpose(0, 2, 1, 3)[wmask]
+        assert not np.any(np.isnan(Kw))
+        assert rel_err(Kw, Ko) <= tol
+        Vw = Vg.transpose(0, 2, 1, 3)[wmask]
+        Vo = kv_oracle.V[l].transpose(0, 2, 1, 3)[wmask]
+        assert rel_err(Vw, Vo) <= tol
+
+
+def _run_split(wl, dtype, split_fn, flags=0):
+    g = GpuWorkload(wl, dtype)
+    ctx = make_ctx(wl, dtype, flags)
+    split = split_fn(ctx)
+    g.step(ctx, split)
+    torch.cuda.synchronize()
+    return g, ctx
+
+
+@pytest.mark.parametrize("cfg_name,k", [("cfg1", 2), ("cfg1-bf16", 2), ("cfg1-gqa", 4)])
+def test_parity_tiny_temporal_and_every_split(cfg_name, k):
+    cfg = configs.get_config(cfg_name)
+    wl = workload.build(cfg, k=k)
+    tol = TOL[cfg.dtype]
+    y_pre, y_dec, kv_o = run(wl)
+    # temporal mode runs k = 1: compare against the oracle's first decode step
+    wl1 = workload.build(cfg, k=1)
+    y_pre1, y_dec1, kv_o1 = run(wl1)
+    ctx = make_ctx(wl, cfg.dtype)
+    g = GpuWorkload(wl1, cfg.dtype)
+    g.step(ctx, D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1))
+    torch.cuda.synchronize()
+    _check_outputs(g, y_pre1, y_dec1, tol)
+    _check_kv(g, kv_o1, tol)
+    ref_pre, ref_dec = None, None
+    parts, total = ctx.partitions()
+    assert parts and total == 148
+    for s_d in parts:
+        g = GpuWorkload(wl, cfg.dtype)
+        g.step(ctx, D.split_struct(D.DUET_MODE_SPATIAL, total - s_d, s_d, k))
+        torch.cuda.synchronize()
+        _check_outputs(g, y_pre, y_dec, tol)
+        _check_kv(g, kv_o, tol)
+        # split invariance: bitwise identical across every split
+        if ref_pre is None:
+            ref_pre, ref_dec = g.y_pre.clone(), g.y_dec.clone()
+        else:
+            assert torch.equal(g.y_pre, ref_pre) and torch.equal(g.y_dec, ref_dec), f"split {s_d} differs"
+    ctx.close()
+
+
+def test_parity_llama_shapes_ragged_prefix():
+    """Llama-3-8B layer shapes (tensor-core GEMM + flash prefill attention, d_h = 128, GQA 4) on a
+    ragged batch: two prefill sequences (one chunk with a 37-token prefix), three decodes, k = 3."""
+    cfg = configs.get_config("cfg2-mini")
+    wl = workload.build(cfg)
+    y_pre, y_dec, kv_o = run(wl)
+    ctx = make_ctx(wl, "bf16")
+    parts, total = ctx.partitions()
+    for s_d in (parts[0], parts[-1]):
+        g = GpuWorkload(wl, "bf16")
+        g.step(ctx, D.split_struct(D.DUET_MODE_SPATIAL, total - s_d, s_d, wl.k))
+        torch.cuda.synchronize()
+        _check_outputs(g, y_pre, y_dec, TOL["bf16"])
+        _check_kv(g, kv_o, TOL["bf16"])
+    wl1 = workload.build(cfg, k=1)
+    y_pre1, y_dec1, _ = run(wl1)
+    g = GpuWorkload(wl1, "bf16")
+    g.step(ctx, D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1))
+    torch.cuda.synchronize()
+    _check_outputs(g, y_pre1, y_dec1, TOL["bf16"])
+
+
+def test_fine_grained_partitions_and_no_graph():
+    cfg = configs.get_config("cfg1")
+    wl = workload.build(cfg, k=3)
+    y_pre, y_dec, _ = run(wl)
+    ctx = make_ctx(wl, "fp32", D.DUET_CTX_FINE_SPLIT | D.DUET_CTX_NO_GRAPH)
+    parts, total = ctx.partitions()
+    assert parts[0] == 2 and 2 in parts and 146 in parts
+    for s_d in (2, 10, 74, 146):
+        g = GpuWorkload(wl, "fp32")
+        g.step(ctx, D.split_struct(D.DUET_MODE_SPATIAL, total - s_d, s_d, 3))
+        torch.cuda.synchronize()
+        _check_outputs(g, y_pre, y_dec, TOL["fp32"])
+
+
+def test_temporal_equals_spatial_bitwise_k1():
+    cfg = configs.get_config("cfg1-bf16")
+    wl = workload.build(cfg, k=1)
+    gt, ctx = _run_split(wl, "bf16", lambda c: D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1))
+    gs = GpuWorkload(wl, "bf16")
+    gs.step(ctx, D.split_struct(D.DUET_MODE_SPATIAL, 132, 16, 1))
+    torch.cuda.synchronize()
+    assert torch.equal(gt.y_dec, gs.y_dec)
+    assert torch.equal(gt.y_pre, gs.y_pre)
+
+
+def test_decode_after_prefill_invariant_gpu():
+    """Decoding token t after a prefill of 0..t-1 matches row t of a prefill over 0..t."""
+    cfg = configs.get_config("cfg1")
+    T = 77
+    full = workload.build(cfg, pre_seqs=[(T, 0)], dec_ctx=[], k=1)
+    g1, ctx = _run_split(full, "fp32", lambda c: D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1))
+    part = workload.build(cfg, pre_seqs=[(T - 1, 0)], dec_ctx=[], k=1)
+    g2 = GpuWorkload(part, "fp32")
+    g2.step(ctx, D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1))
+    # decode the last token against the cache the partial prefill wrote (same pages)
+    dec = dict(c=[T - 1], table=part.pre_tables, x=g1.x_pre[T - 1:T].contiguous(),
+               y=torch.zeros((1, 1, cfg.model.d_model), device="cuda"))
+    ctx.step(g2.W, None, dec, g2.K, g2.V, part.n_pages, D.split_struct(D.DUET_MODE_SPATIAL, 132, 16, 1))
+    torch.cuda.synchronize()
+    e = rel_err(dec["y"][0, 0].cpu().numpy(), g1.y_pre[T - 1].cpu().numpy())
+    assert e < 1e-4, e
+
+
+def test_page_table_errors_are_caught_before_launch():
+    cfg = configs.get_config("cfg1")
+    wl = workload.build(cfg, k=1)
+    g = GpuWorkload(wl, "fp32")
+    ctx = make_ctx(wl, "fp32")
+    bad = wl.dec_tables.copy()
+    bad[1, 0] = bad[0, 0]
+    dec = dict(c=wl.dec_ctx, table=bad, x=g.x_dec, y=g.y_dec)
+    with pytest.raises(D.DuetError) as e:
+        ctx.step(g.W, g.prefill_arg(), dec, g.K, g.V, wl.n_pages, D.split_struct(0, 148, 0, 1))
+    assert e.value.status == -2 and "used twice" in str(e.value)
+    with pytest.raises(D.DuetError) as e:
+        ctx.step(g.W, g.prefill_arg(), g.decode_arg(), g.K, g.V, wl.n_pages, D.split_struct(1, 137, 11, 1))
+    assert e.value.status == -2
+    bad = wl.dec_tables.copy()
+    bad[0, 0] = wl.n_pages + 5
+    with pytest.raises(D.DuetError):
+        ctx.step(g.W, None, dict(c=wl.dec_ctx, table=bad, x=g.x_dec, y=g.y_dec), g.K, g.V, wl.n_pages,
+                 D.split_struct(0, 148, 0, 1))
+
+
+@pytest.mark.parametrize("M,N,K,epi", [(1, 256, 256, 0), (130, 384, 512, 1), (257, 160, 1024, 2),
+                                       (2048, 6144, 4096, 0), (64, 4096, 14336, 1)])
+def test_op_gemm_bf16(M, N, K, epi):
+    torch.manual_seed(0)
+    cfg = configs.get_config("cfg2")
+    wl = workload.build(cfg, pre_seqs=[(16, 0)], dec_ctx=[], k=1, with_weights=False)
+    ctx = make_ctx(wl, "bf16")
+    A = (torch.randn(M, K, device="cuda") / 4).bfloat16()
+    Bn = 2 * N if epi == 2 else N
+    B = (torch.randn(Bn, K, device="cuda") / K ** 0.5).bfloat16()
+    R = torch.randn(M, N, device="cuda").bfloat16()
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ctx.op_gemm(A, B, C, R if epi == 1 else None, None, epi)
+    torch.cuda.synchronize()
+    acc = A.double() @ B.double().T
+    if epi == 0:
+        ref = acc
+    elif epi == 1:
+        ref = R.double() + acc
+    else:
+        g, u = acc[:, :N], acc[:, N:]
+        ref = g / (1 + torch.exp(-g)) * u
+    e = (C.double() - ref).abs().max().item() / ref.abs().max().item()
+    assert e < 1e-2, e
+
+
+@pytest.mark.slow
+def test_parity_cfg2_full_layer_temporal_and_optimizer_split():
+    """Llama-3-8B layer at BASELINE size (prefill 2048 + 64 decodes at 4k) against the oracle."""
+    cfg = configs.get_config("cfg2")
+    wl = workload.build(cfg, k=1)
+    y_pre, y_dec, kv_o = run(wl)
+    g, ctx = _run_split(wl, "bf16", lambda c: D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1))
+    _check_outputs(g, y_pre, y_dec, TOL["bf16"])
+    parts, total = ctx.partitions()
+    for s_d in (parts[0], 32, parts[-1]):
+        g = GpuWorkload(wl, "bf16")
+        g.step(ctx, D.split_struct(D.DUET_MODE_SPATIAL, total - s_d, s_d, 1))
+        torch.cuda.synchronize()
+        _check_outputs(g, y_pre, y_dec, TOL["bf16"])
+    _check_kv(g, kv_o, TOL["bf16"])
