@@ -84,7 +84,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
         mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[3 + i]})
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].strip() == "Active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
                 "samples": len(self.samples)}
 
@@ -247,7 +247,12 @@ def main():
 
     # L0 calibration: Pi_SM(S), B_HBM(S) on this GPU with our kernels
     t0 = time.perf_counter()
-    fl, bw = ctx.calibrate(total)
+    if args.profile_only:   # no calibration launches under a profiler: linear tables from the measured peaks
+        pk0, _ = peaks()
+        fl = [0.0] + [float(pk0["bf16_tflops"]) * 1e12 * s_ / total for s_ in range(1, total + 1)]
+        bw = [0.0] + [float(pk0["hbm_gbs"]) * 1e9 * min(1.0, (s_ / total) ** 0.32) for s_ in range(1, total + 1)]
+    else:
+        fl, bw = ctx.calibrate(total)
     t_cal = time.perf_counter() - t0
     hw = D.HwProfile(total, parts, fl, bw)
     tau = args.tau if args.tau is not None else cfg.batch.tbt_slo_s

@@ -79,6 +79,8 @@ struct DecodeAttnArgs {
   int max_len;      // upper bound of pos[r] + 1 over the batch (host-known), for split sizing
 };
 int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st);
+bool decode_tc_supported(const DecodeAttnArgs& a);
+int launch_decode_tc(const DecodeAttnArgs& a, int pages_per_split, int n_splits, cudaStream_t st);
 
 // ---------------------------------------------------------------- prefill attention
 // Causal attention of the chunk rows over prefix + chunk (reading #7): sequence s has rows

@@ -225,7 +225,9 @@ int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st) {
   ns = (max_pages + pps - 1) / pps;
   dim3 grid(ns, a.hkv, a.n);
   bool ok = true;
-  if (dt == DT::BF16) {
+  if (dt == DT::BF16 && decode_tc_supported(a)) {
+    launch_decode_tc(a, pps, ns, st);
+  } else if (dt == DT::BF16) {
     if (a.dh == 128) dispatch_g<bf16, 128>(a, grid, pps, ns, st, &ok);
     else if (a.dh == 64) dispatch_g<bf16, 64>(a, grid, pps, ns, st, &ok);
     else ok = false;
