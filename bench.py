@@ -109,9 +109,17 @@ def max_over_ranks(x: float, ws: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def whole_job_rate(units_local: float, seconds_local: float, ws: int) -> tuple:
+    """value = units all ranks processed / max over ranks of the device-timed region (weak scaling:
+    every rank runs the same replica workload, so units_all = units_local * ws)."""
+    t_max = max_over_ranks(seconds_local, ws)
+    return units_local * ws / t_max, t_max
 
 
 def barrier(ws):
@@ -307,9 +315,8 @@ def main():
     ctx.profile_enable(False)
     times = ctx.last_step_times()
     kernels = times["kernels"] * args.steps
-    t_max = max_over_ranks(t_ms, ws)
-    value = tokens * ws / (t_max * 1e-3)
-    ms_per_step = t_max / args.steps
+    value, t_max_s = whole_job_rate(tokens, t_ms * 1e-3, ws)
+    ms_per_step = t_max_s * 1e3 / args.steps
     split = s
 
     # ------------------------------------------------ per-side times & predictor error (one step)

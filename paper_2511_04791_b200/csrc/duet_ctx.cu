@@ -699,10 +699,11 @@ static uint64_t hash_ptrs(const duet_layer_weights* w, int L, const duet_kv_page
 
 // One decode step on the decode side (all layers + advance), launched on st.
 static duet_status decode_step_kernels(duet_ctx* c, cudaStream_t st, int num_sms, const duet_layer_weights* w,
-                                       const duet_kv_pages* kv, int n, int max_len, void* y_out, int* kernels) {
+                                       const duet_kv_pages* kv, const AttnPlan& meta, int max_len, void* y_out,
+                                       int* kernels) {
   Side& S = c->dec;
-  AttnPlan ap;
-  ap.n_dec = n;
+  const int n = meta.n_dec;
+  AttnPlan ap = meta;  // work counts of step 1 (timing statistics only)
   ap.max_len_dec = max_len;
   DUET_TRY(run_layers(c, S, st, num_sms, n, S.xin, S.ylast, w, kv, ap, kernels));
   *kernels += launch_decode_advance(c->dt, S.ylast, S.xin, y_out, n, c->spec.d_model, S.pos(), S.step(), st);
@@ -793,7 +794,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     const int max_len = ((max_c + k + 1023) / 1024) * 1024;  // bucket: graphs survive context growth
     if (c->lim.flags & DUET_CTX_NO_GRAPH) {
       for (int j = 0; j < k; ++j)
-        DUET_TRY(decode_step_kernels(c, st, P->s_d, w, kv, n, max_len, dec->y, &kernels));
+        DUET_TRY(decode_step_kernels(c, st, P->s_d, w, kv, ap, max_len, dec->y, &kernels));
     } else {
       auto key = std::make_tuple(P->s_d, n, c->spec.n_layers, hash_ptrs(w, c->spec.n_layers, kv, dec->y, max_len));
       auto it = c->graphs.find(key);
@@ -803,7 +804,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
         int nk = 0;
         CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         c->capturing = true;
-        duet_status s = decode_step_kernels(c, cap, P->s_d, w, kv, n, max_len, dec->y, &nk);
+        duet_status s = decode_step_kernels(c, cap, P->s_d, w, kv, ap, max_len, dec->y, &nk);
         c->capturing = false;
         cudaError_t e = cudaStreamEndCapture(cap, &graph);
         if (s != DUET_OK) return s;

@@ -2,15 +2,23 @@
 // (QKV, O, gate-up, down; §2, §4.1), bf16 in, fp32 accumulation in
 // tensor memory, fused epilogues (bias, residual add, SwiGLU).
 //
-// C[M][N] = epi(A[M][K] . B[N][K]^T), A and B K-major (nn.Linear layout).
+// C[M][N] = epi(X[M][K] . W[N][K]^T), X (activations) and W (weights) K-major (nn.Linear layout).
 // Persistent, warp-specialized, one CTA per SM (cta_group::1):
-//   warp 0      TMA producer: 128x64 A tile + BNx64 B tile per stage (SWIZZLE_128B), S-stage ring
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (UMMA 128xBNx16)
-//   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per load) -> fused op -> global
-// Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap the MMAs of i+1.
-// Tiles are assigned statically (tile = blockIdx.x + j * gridDim.x, m fastest) and every output
-// element is reduced over K in one fixed order, so results do not depend on the grid size
-// (i.e. on the SM partition the kernel runs in).
+//   warp 0      TMA producer (SWIZZLE_128B tiles, S-stage mbarrier ring)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns) -> fused op -> global
+// Two TMEM accumulators let the epilogue of tile i overlap the MMAs of tile i+1.
+//
+// Two orientations:
+//   normal  (prefill, temporal; M > 128): UMMA 128 x BN x 16, the 128 TMEM lanes are 128 token rows,
+//           columns are BN output features.
+//   swap-AB (decode side, M <= 128): UMMA 128 x NT x 16 with the 128 lanes = 128 *weight rows* and
+//           NT (64 or 128) columns = the tokens, so a skinny decode batch does not pad the MMA M
+//           dimension to 128 — the decode GEMMs stay weight-streaming (HBM) bound on a small
+//           partition.  SwiGLU in swap mode issues two MMAs per k-step (gate rows
+//           and the matching up rows into two TMEM column ranges), so the epilogue is thread-local.
+// Tiles are assigned statically (tile = blockIdx.x + j * gridDim.x) and every output element is
+// reduced over K in one fixed order: results do not depend on the grid, i.e. on the SM partition.
 #include <cuda.h>
 
 #include "dev_common.cuh"
@@ -101,30 +109,38 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int BN>
+// Tile configuration.
+//   normal: smem A = 128 token rows, smem B = BN weight rows (SwiGLU: BN/2 gate + BN/2 up rows);
+//           accumulator 128 x BN; output tile 128 x (SwiGLU ? BN/2 : BN).
+//   swap:   smem A = 128 weight rows (SwiGLU: two such tiles, gate and up), smem B = BN token rows;
+//           accumulator 128 x BN (SwiGLU: 2 x BN); output tile BN tokens x 128 features.
+template <int BN, int EPI, bool SWAP>
 struct Cfg {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
-  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int A_TILES = (SWAP && EPI == EPI_SWIGLU) ? 2 : 1;
+  static constexpr int A_BYTES = A_TILES * BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int ACC_COLS = (SWAP && EPI == EPI_SWIGLU) ? 2 * BN : BN;
+  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 32 ? 32 : (2 * ACC_COLS <= 64 ? 64 : (2 * ACC_COLS <= 128 ? 128 : (2 * ACC_COLS <= 256 ? 256 : 512)));
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(2 * ACC_COLS <= 512, "TMEM");
 };
 
 struct Params {
-  int M, N, K;       // N = output columns (SwiGLU: width of act)
+  int M, N, K;        // C is M x N; N = output features (SwiGLU: width of act)
   int num_m, num_n, num_tiles;
   bf16* C;
   const bf16* R;
   const bf16* bias;
   int ldc, ldr;
-  int n_up_off;      // SwiGLU: row offset of the up rows in B (= N)
+  int n_up_off;       // SwiGLU: row offset of the up rows in W (= N)
 };
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool SWAP>
 __global__ void __launch_bounds__(192, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p) {
-  using CF = Cfg<BN>;
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, Params p) {
+  using CF = Cfg<BN, EPI, SWAP>;
   constexpr int S = CF::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -140,8 +156,8 @@ __global__ void __launch_bounds__(192, 1)
   const int num_k = p.K / BK;
 
   if (warp == 0 && lane == 0) {
-    prefetch_map(&map_a);
-    prefetch_map(&map_b);
+    prefetch_map(&map_x);
+    prefetch_map(&map_w);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -169,17 +185,26 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         const int mb = t % p.num_m, nb = t / p.num_m;
-        const int m0 = mb * BM;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], CF::STAGE_BYTES);
-          tma_load_2d(&map_a, &full[s], sA + s * CF::A_BYTES, kb * BK, m0);
-          if constexpr (EPI == EPI_SWIGLU) {
-            const int j0 = nb * (BN / 2);
-            tma_load_2d(&map_b, &full[s], sB + s * CF::B_BYTES, kb * BK, j0);
-            tma_load_2d(&map_b, &full[s], sB + s * CF::B_BYTES + (BN / 2) * BK * 2, kb * BK, p.n_up_off + j0);
+          uint8_t* a_dst = sA + s * CF::A_BYTES;
+          uint8_t* b_dst = sB + s * CF::B_BYTES;
+          if constexpr (!SWAP) {
+            tma_load_2d(&map_x, &full[s], a_dst, kb * BK, mb * BM);
+            if constexpr (EPI == EPI_SWIGLU) {
+              const int j0 = nb * (BN / 2);
+              tma_load_2d(&map_w, &full[s], b_dst, kb * BK, j0);
+              tma_load_2d(&map_w, &full[s], b_dst + (BN / 2) * BK * 2, kb * BK, p.n_up_off + j0);
+            } else {
+              tma_load_2d(&map_w, &full[s], b_dst, kb * BK, nb * BN);
+            }
           } else {
-            tma_load_2d(&map_b, &full[s], sB + s * CF::B_BYTES, kb * BK, nb * BN);
+            const int j0 = nb * BM;
+            tma_load_2d(&map_w, &full[s], a_dst, kb * BK, j0);
+            if constexpr (EPI == EPI_SWIGLU)
+              tma_load_2d(&map_w, &full[s], a_dst + BM * BK * 2, kb * BK, p.n_up_off + j0);
+            tma_load_2d(&map_x, &full[s], b_dst, kb * BK, mb * BN);
           }
           if (++s == S) {
             s = 0;
@@ -200,15 +225,19 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t aph = (i >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * CF::ACC_COLS;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + s * CF::A_BYTES);
           const uint32_t b0 = smem_u32(sB + s * CF::B_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
+          for (int k = 0; k < BK / 16; ++k) {
             umma_bf16(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (kb | k) != 0);
+            if constexpr (SWAP && EPI == EPI_SWIGLU)
+              umma_bf16(d_tmem + BN, sw128_desc(a0 + BM * BK * 2 + k * 32), sw128_desc(b0 + k * 32), idesc,
+                        (kb | k) != 0);
+          }
           umma_commit(&empty[s]);
           if (++s == S) {
             s = 0;
@@ -221,65 +250,100 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // ---------------- epilogue warps 2..5: TMEM lane quadrant = warp % 4
     const int quad = warp & 3;
-    const int row_in_tile = quad * 32 + lane;
+    const int lane_row = quad * 32 + lane;
     int i = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++i) {
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
       const int mb = t % p.num_m, nb = t / p.num_m;
-      const int row = mb * BM + row_in_tile;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
-      constexpr int OUT_COLS = EPI == EPI_SWIGLU ? BN / 2 : BN;
-      const int n0 = nb * OUT_COLS;
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * CF::ACC_COLS;
+      if constexpr (!SWAP) {
+        // lane = token row, columns = output features
+        const int row = mb * BM + lane_row;
+        constexpr int OUT_COLS = EPI == EPI_SWIGLU ? BN / 2 : BN;
+        const int n0 = nb * OUT_COLS;
 #pragma unroll 1
-      for (int c = 0; c < OUT_COLS; c += 32) {
-        float v[32];
-        tmem_ld32(tbase + c, v);
-        if constexpr (EPI == EPI_SWIGLU) {
-          float u[32];
-          tmem_ld32(tbase + BN / 2 + c, u);
+        for (int c = 0; c < OUT_COLS; c += 32) {
+          float v[32];
+          tmem_ld32(tbase + c, v);
+          if constexpr (EPI == EPI_SWIGLU) {
+            float u[32];
+            tmem_ld32(tbase + BN / 2 + c, u);
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = silu_f(v[e]) * u[e];
-        }
-        if (row < p.M && n0 + c < p.N) {
-          bf16* dst = p.C + (size_t)row * p.ldc + n0 + c;
-          if (n0 + c + 32 <= p.N) {
-            if constexpr (EPI == EPI_RESIDUAL) {
-              const bf16* rsrc = p.R + (size_t)row * p.ldr + n0 + c;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                float rf[8];
-                load16<bf16>(rsrc + q * 8, rf);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v[q * 8 + e] += rf[e];
-              }
-            } else if constexpr (EPI == EPI_STORE) {
-              if (p.bias) {
+            for (int e = 0; e < 32; ++e) v[e] = silu_f(v[e]) * u[e];
+          }
+          if (row < p.M && n0 + c < p.N) {
+            bf16* dst = p.C + (size_t)row * p.ldc + n0 + c;
+            if (n0 + c + 32 <= p.N) {
+              if constexpr (EPI == EPI_RESIDUAL) {
+                const bf16* rsrc = p.R + (size_t)row * p.ldr + n0 + c;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                  float bf[8];
-                  load16<bf16>(p.bias + n0 + c + q * 8, bf);
+                  float rf[8];
+                  load16<bf16>(rsrc + q * 8, rf);
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) v[q * 8 + e] += bf[e];
+                  for (int e = 0; e < 8; ++e) v[q * 8 + e] += rf[e];
+                }
+              } else if constexpr (EPI == EPI_STORE) {
+                if (p.bias) {
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    float bf[8];
+                    load16<bf16>(p.bias + n0 + c + q * 8, bf);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v[q * 8 + e] += bf[e];
+                  }
                 }
               }
-            }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float o8[8];
+              for (int q = 0; q < 4; ++q) {
+                float o8[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) o8[e] = v[q * 8 + e];
-              store16<bf16>(dst + q * 8, o8);
+                for (int e = 0; e < 8; ++e) o8[e] = v[q * 8 + e];
+                store16<bf16>(dst + q * 8, o8);
+              }
+            } else {
+              for (int e = 0; e < 32 && n0 + c + e < p.N; ++e) {
+                float o = v[e];
+                if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)row * p.ldr + n0 + c + e]);
+                if constexpr (EPI == EPI_STORE)
+                  if (p.bias) o += __bfloat162float(p.bias[n0 + c + e]);
+                dst[e] = __float2bfloat16_rn(o);
+              }
             }
-          } else {
-            for (int e = 0; e < 32 && n0 + c + e < p.N; ++e) {
-              float o = v[e];
-              if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)row * p.ldr + n0 + c + e]);
-              if constexpr (EPI == EPI_STORE)
-                if (p.bias) o += __bfloat162float(p.bias[n0 + c + e]);
-              dst[e] = __float2bfloat16_rn(o);
+          }
+        }
+      } else {
+        // lane = output feature n, columns = tokens m
+        const int n = nb * BM + lane_row;
+        const bool n_ok = n < p.N;
+        float badd = 0.f;
+        if constexpr (EPI == EPI_STORE)
+          if (p.bias && n_ok) badd = __bfloat162float(p.bias[n]);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          const int m0 = mb * BN + c;
+          if (m0 >= p.M) break;  // warp-uniform
+          float v[32];
+          tmem_ld32(tbase + c, v);
+          if constexpr (EPI == EPI_SWIGLU) {
+            float u[32];
+            tmem_ld32(tbase + BN + c, u);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = silu_f(v[e]) * u[e];
+          }
+          if (n_ok) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const int m = m0 + e;
+              if (m < p.M) {
+                float o = v[e];
+                if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)m * p.ldr + n]);
+                if constexpr (EPI == EPI_STORE) o += badd;
+                p.C[(size_t)m * p.ldc + n] = __float2bfloat16_rn(o);
+              }
             }
           }
         }
@@ -328,26 +392,32 @@ static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int l
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool SWAP>
 static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
-  using CF = Cfg<BN>;
+  using CF = Cfg<BN, EPI, SWAP>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
     attr_set = true;
   }
-  CUtensorMap ma, mb;
-  const int b_rows = EPI == EPI_SWIGLU ? 2 * a.N : a.N;
-  const int b_box = EPI == EPI_SWIGLU ? BN / 2 : BN;
-  if (!make_map(&ma, a.A, a.M, a.K, a.lda, BM)) return -1;
-  if (!make_map(&mb, a.B, b_rows, a.K, a.ldb, b_box)) return -1;
+  CUtensorMap mx, mw;
+  const int w_rows = EPI == EPI_SWIGLU ? 2 * a.N : a.N;
   Params p{};
   p.M = a.M;
   p.N = a.N;
   p.K = a.K;
-  const int out_cols = EPI == EPI_SWIGLU ? BN / 2 : BN;
-  p.num_m = (a.M + BM - 1) / BM;
-  p.num_n = (a.N + out_cols - 1) / out_cols;
+  if constexpr (!SWAP) {
+    if (!make_map(&mx, a.A, a.M, a.K, a.lda, BM)) return -1;
+    if (!make_map(&mw, a.B, w_rows, a.K, a.ldb, EPI == EPI_SWIGLU ? BN / 2 : BN)) return -1;
+    const int out_cols = EPI == EPI_SWIGLU ? BN / 2 : BN;
+    p.num_m = (a.M + BM - 1) / BM;
+    p.num_n = (a.N + out_cols - 1) / out_cols;
+  } else {
+    if (!make_map(&mx, a.A, a.M, a.K, a.lda, BN)) return -1;
+    if (!make_map(&mw, a.B, w_rows, a.K, a.ldb, BM)) return -1;
+    p.num_m = (a.M + BN - 1) / BN;
+    p.num_n = (a.N + BM - 1) / BM;
+  }
   p.num_tiles = p.num_m * p.num_n;
   p.C = (bf16*)a.C;
   p.R = (const bf16*)a.R;
@@ -356,8 +426,15 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   p.ldr = a.ldr;
   p.n_up_off = a.N;
   const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
-  gemm_tc_kernel<BN, EPI><<<grid, 192, CF::SMEM, st>>>(ma, mb, p);
+  gemm_tc_kernel<BN, EPI, SWAP><<<grid, 192, CF::SMEM, st>>>(mx, mw, p);
   return 1;
+}
+
+template <int EPI>
+static int launch_epi(const GemmArgs& a, int num_sms, cudaStream_t st) {
+  if (a.M <= 64) return launch<64, EPI, true>(a, num_sms, st);
+  if (a.M <= 128) return launch<128, EPI, true>(a, num_sms, st);
+  return launch<256, EPI, false>(a, num_sms, st);
 }
 
 }  // namespace tc
@@ -372,9 +449,9 @@ bool gemm_tc_supported(const GemmArgs& a) {
 }
 
 int launch_gemm_tc(const GemmArgs& a, int num_sms, cudaStream_t st) {
-  if (a.epi == EPI_SWIGLU) return tc::launch<256, EPI_SWIGLU>(a, num_sms, st);
-  if (a.epi == EPI_RESIDUAL) return tc::launch<256, EPI_RESIDUAL>(a, num_sms, st);
-  return tc::launch<256, EPI_STORE>(a, num_sms, st);
+  if (a.epi == EPI_SWIGLU) return tc::launch_epi<EPI_SWIGLU>(a, num_sms, st);
+  if (a.epi == EPI_RESIDUAL) return tc::launch_epi<EPI_RESIDUAL>(a, num_sms, st);
+  return tc::launch_epi<EPI_STORE>(a, num_sms, st);
 }
 
 }  // namespace duet

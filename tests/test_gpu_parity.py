@@ -186,8 +186,12 @@ def test_page_table_errors_are_caught_before_launch():
 
 
 @pytest.mark.parametrize("M,N,K,epi", [(1, 256, 256, 0), (130, 384, 512, 1), (257, 160, 1024, 2),
-                                       (2048, 6144, 4096, 0), (64, 4096, 14336, 1)])
+                                       (2048, 6144, 4096, 0), (64, 4096, 14336, 1), (64, 14336, 4096, 2),
+                                       (100, 512, 256, 2), (8, 768, 256, 3), (77, 6144, 4096, 3),
+                                       (300, 1000, 512, 3), (128, 200, 128, 1)])
 def test_op_gemm_bf16(M, N, K, epi):
+    """tcgen05 GEMM vs float64 torch: normal tiles (M > 128) and swap-AB tiles (M <= 128), every
+    epilogue (3 = store + bias), ragged M / N."""
     torch.manual_seed(0)
     cfg = configs.get_config("cfg2")
     wl = workload.build(cfg, pre_seqs=[(16, 0)], dec_ctx=[], k=1, with_weights=False)
@@ -196,12 +200,15 @@ def test_op_gemm_bf16(M, N, K, epi):
     Bn = 2 * N if epi == 2 else N
     B = (torch.randn(Bn, K, device="cuda") / K ** 0.5).bfloat16()
     R = torch.randn(M, N, device="cuda").bfloat16()
+    bias = torch.randn(N, device="cuda").bfloat16()
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    ctx.op_gemm(A, B, C, R if epi == 1 else None, None, epi)
+    ctx.op_gemm(A, B, C, R if epi == 1 else None, bias if epi == 3 else None, 0 if epi == 3 else epi)
     torch.cuda.synchronize()
     acc = A.double() @ B.double().T
     if epi == 0:
         ref = acc
+    elif epi == 3:
+        ref = acc + bias.double()
     elif epi == 1:
         ref = R.double() + acc
     else:
