@@ -320,6 +320,8 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       pa.tok_pos = S.pos();
       pa.tok_row = S.tok();
       pa.max_len = ap.max_len_pre;
+      pa.n_pages = kv->n_pages;
+      pa.total_rows = n_rows;
       const int pi = prof_begin(c, st);
       const int r = launch_prefill_attn(dt, pa, st);
       if (r < 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "prefill attention: unsupported head layout");
@@ -347,6 +349,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       da.max_splits = kMaxSplits;
       da.num_sms = num_sms;
       da.max_len = ((ap.max_len_dec + 1023) / 1024) * 1024;  // same bucket in both modes
+      da.n_pages = kv->n_pages;
       const int pi = prof_begin(c, st);
       const int r = launch_decode_attn(dt, da, st);
       if (r < 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "decode attention: unsupported head layout");

@@ -77,6 +77,7 @@ struct DecodeAttnArgs {
   int max_splits;
   int num_sms;
   int max_len;      // upper bound of pos[r] + 1 over the batch (host-known), for split sizing
+  int n_pages;      // pool extent (TMA maps)
 };
 int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st);
 bool decode_tc_supported(const DecodeAttnArgs& a);
@@ -106,10 +107,15 @@ struct PrefillAttnArgs {
   const int* tok_pos;
   const int* tok_row;
   int max_len;  // host-known max(c + q) over the sequences
+  // tensor-core path: pool extent and rows of the q buffer (TMA maps)
+  int n_pages;
+  int total_rows;
 };
 int launch_prefill_attn(DT dt, const PrefillAttnArgs& a, cudaStream_t st);
 bool fa_prefill_supported(const PrefillAttnArgs& a);
 int launch_fa_prefill(const PrefillAttnArgs& a, cudaStream_t st);
+bool fa_tc_supported(const PrefillAttnArgs& a);
+int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- decode window bookkeeping
 // End of one decode step (P:335 look-ahead): y_out[step][r] = y[r]; xin[r] = y[r];

@@ -226,7 +226,7 @@ int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st) {
   dim3 grid(ns, a.hkv, a.n);
   bool ok = true;
   if (dt == DT::BF16 && decode_tc_supported(a)) {
-    launch_decode_tc(a, pps, ns, st);
+    if (launch_decode_tc(a, pps, ns, st) < 0) ok = false;
   } else if (dt == DT::BF16) {
     if (a.dh == 128) dispatch_g<bf16, 128>(a, grid, pps, ns, st, &ok);
     else if (a.dh == 64) dispatch_g<bf16, 64>(a, grid, pps, ns, st, &ok);
@@ -249,7 +249,15 @@ int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st) {
 // chunk row is an independent query at its absolute position, evaluated by the decode kernel.
 int launch_prefill_attn(DT dt, const PrefillAttnArgs& p, cudaStream_t st) {
   if (p.total_q <= 0) return 0;
-  if (dt == DT::BF16 && fa_prefill_supported(p)) return launch_fa_prefill(p, st);
+  if (dt == DT::BF16) {
+    static const char* impl = getenv("DUET_FA");  // "mma": force the mma.sync kernel (A/B comparisons)
+    const bool force_mma = impl && impl[0] == 'm';
+    if (!force_mma && fa_tc_supported(p)) {
+      const int r = launch_fa_tc(p, st);
+      if (r > 0) return r;
+    }
+    if (fa_prefill_supported(p)) return launch_fa_prefill(p, st);
+  }
   DecodeAttnArgs a{};
   a.q = p.q;
   a.q_stride = p.q_stride;

@@ -1,37 +1,61 @@
-// Paged decode attention on tensor cores (bf16, d_h = 128, GQA group G <= 16).
+// Paged decode attention on tensor cores (bf16, d_h = 128, GQA group G <= 8).
 //
-// The G query heads that share a kv head (reading #6) form the rows of a 16 x 128 Q tile (rows
-// >= G are zero), so each 16-token page of K and V is read from HBM exactly once per request and
-// consumed by two mma.sync m16n8k16 chains (S = Q K^T, 16 x 16; O += P V, 16 x 128) instead of
-// warp-shuffle dot products.  One CTA per (split, kv head, request); each of the 4 warps streams
-// its own pages (page w, w+4, ...) through a private 3-stage cp.async ring in shared memory
-// (XOR-swizzled 256-byte rows, conflict-free ldmatrix); slots past the sequence end are zero-filled
-// and masked.  Per-warp online softmax (exp2 domain); the 4 warps and the splits are merged with
-// the log-sum-exp rule.  HBM traffic per request and layer: 2 h_kv (c+1) d_h s bytes.
+// Computed transposed, so that the 16 tokens of a page fill the MMA M dimension and the G query
+// heads sharing a kv head (reading #6) fill N = 8:
+//   S^T (16 keys x 8 heads)  = K_page (16 x 128) . Q^T (128 x 8)          8 x mma.m16n8k16
+//   O^T (128 dims x 8 heads) += V_page^T (128 x 16) . P^T (16 x 8)        8 x mma.m16n8k16
+// P^T goes from the S^T accumulator layout to the B-operand layout with two movmatrix.trans.
+// Each 16-token page of K and V is read from HBM exactly once per request (P:213 counts
+// 2 h_kv (q+c) d_h s bytes).  Pages are fetched with TMA (2-D tensor maps over the pools, one
+// 16-row x 64-column SWIZZLE_128B box per half page) into a private NST-stage ring per warp, so a
+// page costs one elected thread four TMA instructions and an mbarrier; 8 warps per CTA stream
+// pages w, w+8, ...  Slots past the sequence end are masked out of S and zeroed in V.  Online
+// softmax per head (exp2 domain); warps and splits are merged with the log-sum-exp rule.
+// One CTA per (split, kv head, request).
+#include <cuda.h>
+
 #include "dev_common.cuh"
 #include "kernels.h"
 
 namespace duet {
 namespace dtc {
 
-constexpr int DH = 128, PAGE = 16, NST = 3, WARPS = 4;
-constexpr int ROW_BYTES = DH * 2;
-constexpr int PAGE_BYTES = PAGE * ROW_BYTES;  // 4 KiB: one kv head of one page
+constexpr int DH = 128, PAGE = 16, NST = 3, WARPS = 8;
+constexpr int HALF = PAGE * 128;              // one 16-row x 64-col SW128 box = 2 KiB
+constexpr int PAGE_BYTES = 2 * HALF;          // 4 KiB: one kv head of one page
 constexpr int STAGE_BYTES = 2 * PAGE_BYTES;   // K + V
-constexpr int WARP_BYTES = NST * STAGE_BYTES;
-constexpr int SMEM = WARPS * WARP_BYTES;      // 96 KiB
+constexpr int WARP_BYTES = NST * STAGE_BYTES; // 24 KiB
+constexpr int SMEM = WARPS * WARP_BYTES + 1024 + 256;
 
-__device__ __forceinline__ uint32_t swz(int row, int chunk) {
-  return (uint32_t)(row * ROW_BYTES + ((chunk ^ (row & 7)) << 4));
-}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(sz) : "memory");
+// byte offset of 16-B chunk ch (0..15) of row r in a page stored as two SW128 [16][64] halves
+__device__ __forceinline__ uint32_t swz(int r, int ch) {
+  return (uint32_t)((ch >> 3) * HALF + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -42,20 +66,29 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(addr));
 }
-__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t movtrans(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-__global__ void __launch_bounds__(128) decode_tc_kernel(DecodeAttnArgs a, int pps, int n_splits) {
-  extern __shared__ __align__(128) uint8_t smem[];
+__global__ void __launch_bounds__(256) decode_tc_kernel(const __grid_constant__ CUtensorMap map_k,
+                                                         const __grid_constant__ CUtensorMap map_v, DecodeAttnArgs a,
+                                                         int pps, int n_splits) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int split = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.hq / a.hkv;
@@ -64,161 +97,158 @@ __global__ void __launch_bounds__(128) decode_tc_kernel(DecodeAttnArgs a, int pp
   const int pg0 = split * pps;
   const int pg1 = min(n_pages, pg0 + pps);
   const int* tab = a.table + (size_t)a.tok_row[r] * a.max_pages;
-  const bf16* Kg = reinterpret_cast<const bf16*>(a.k_pool);
-  const bf16* Vg = reinterpret_cast<const bf16*>(a.v_pool);
-  const size_t page_stride = (size_t)a.hkv * PAGE * DH;
   uint8_t* wsm = smem + warp * WARP_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + WARPS * WARP_BYTES) + warp * NST;
   const int g = lane >> 2, t4 = lane & 3;
+  if (lane == 0) {
+    for (int i = 0; i < NST; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
 
-  // Q fragments (A operand, rows = heads of the group, zero beyond G)
-  uint32_t qf[8][4];
+  // Q^T as the B operand: b0 = Q[head g][kk*16 + 2t, +1], b1 = Q[g][kk*16 + 8 + 2t, +1]; zero for g >= G
+  uint32_t qb[8][2];
   {
     const bf16* qr = reinterpret_cast<const bf16*>(a.q) + (size_t)r * a.q_stride + (size_t)kvh * G * DH;
-    const bool v0 = g < G, v1 = g + 8 < G;
+    const bool v = g < G;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      const int c0 = kk * 16 + 2 * t4;
-      qf[kk][0] = v0 ? *reinterpret_cast<const uint32_t*>(qr + g * DH + c0) : 0u;
-      qf[kk][1] = v1 ? *reinterpret_cast<const uint32_t*>(qr + (g + 8) * DH + c0) : 0u;
-      qf[kk][2] = v0 ? *reinterpret_cast<const uint32_t*>(qr + g * DH + c0 + 8) : 0u;
-      qf[kk][3] = v1 ? *reinterpret_cast<const uint32_t*>(qr + (g + 8) * DH + c0 + 8) : 0u;
+      qb[kk][0] = v ? *reinterpret_cast<const uint32_t*>(qr + g * DH + kk * 16 + 2 * t4) : 0u;
+      qb[kk][1] = v ? *reinterpret_cast<const uint32_t*>(qr + g * DH + kk * 16 + 8 + 2 * t4) : 0u;
     }
   }
-  auto load_page = [&](int pg, int st) {
-    const size_t base = (size_t)tab[pg] * page_stride + (size_t)kvh * PAGE * DH;
-    const uint32_t sk = smem_u32(wsm + st * STAGE_BYTES), sv = sk + PAGE_BYTES;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int idx = i * 32 + lane;  // 256 chunks of 16 B per tensor
-      const int row = idx >> 4, ch = idx & 15;
-      const bool v = pg * PAGE + row < len;
-      const size_t off = v ? base + (size_t)row * DH + ch * 8 : 0;
-      cp_async16(sk + swz(row, ch), Kg + off, v);
-      cp_async16(sv + swz(row, ch), Vg + off, v);
-    }
-  };
-  const float scale = rsqrtf((float)DH) * 1.4426950408889634f;
-  float o[16][4];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-
   const int first = pg0 + warp;
-  int n_mine = first < pg1 ? (pg1 - first + WARPS - 1) / WARPS : 0;
-#pragma unroll
-  for (int i = 0; i < NST - 1; ++i) {
-    if (i < n_mine) load_page(first + i * WARPS, i);
-    cp_commit();
-  }
-  for (int i = 0; i < n_mine; ++i) {
-    if (i + NST - 1 < n_mine) load_page(first + (i + NST - 1) * WARPS, (i + NST - 1) % NST);
-    cp_commit();
-    cp_wait<NST - 1>();
-    __syncwarp();
+  const int n_mine = first < pg1 ? (pg1 - first + WARPS - 1) / WARPS : 0;
+  auto issue = [&](int i) {  // lane 0: TMA page i of this warp into stage i % NST
     const int st = i % NST;
+    const int prow = (tab[first + i * WARPS] * a.hkv + kvh) * PAGE;
+    uint8_t* dk = wsm + st * STAGE_BYTES;
+    uint8_t* dv = dk + PAGE_BYTES;
+    mbar_expect_tx(&full[st], STAGE_BYTES);
+    tma_load_2d(&map_k, &full[st], dk, 0, prow);
+    tma_load_2d(&map_k, &full[st], dk + HALF, 64, prow);
+    tma_load_2d(&map_v, &full[st], dv, 0, prow);
+    tma_load_2d(&map_v, &full[st], dv + HALF, 64, prow);
+  };
+  if (lane == 0)
+    for (int i = 0; i < NST - 1 && i < n_mine; ++i) issue(i);
+
+  const float scale = rsqrtf((float)DH) * 1.4426950408889634f;
+  float o[8][4];  // O^T: m-tile mt -> dims mt*16 + {g, g+8}, heads {2t, 2t+1}
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};  // heads 2t, 2t+1
+
+  for (int i = 0; i < n_mine; ++i) {
+    // refill the stage consumed in the previous iteration (all lanes are past it: __syncwarp below)
+    if (lane == 0 && i + NST - 1 < n_mine) issue(i + NST - 1);
+    const int st = i % NST;
+    mbar_wait(&full[st], (i / NST) & 1);
     const uint32_t sk = smem_u32(wsm + st * STAGE_BYTES), sv = sk + PAGE_BYTES;
-    const int pg = first + i * WARPS;
-    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int key = (lane & 7) + ((lane >> 4) << 3);
-      const int ch = kk * 2 + ((lane >> 3) & 1);
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(sk + swz(key, ch), b0, b1, b2, b3);
-      mma16816(s[0], qf[kk], b0, b1);
-      mma16816(s[1], qf[kk], b2, b3);
-    }
-    float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const bool v = pg * PAGE + j * 8 + 2 * t4 + e < len;
-        s[j][e] = v ? s[j][e] * scale : -INFINITY;
-        s[j][2 + e] = v ? s[j][2 + e] * scale : -INFINITY;
-        mx0 = fmaxf(mx0, s[j][e]);
-        mx1 = fmaxf(mx1, s[j][2 + e]);
+    const int key0 = (first + i * WARPS) * PAGE;
+    const bool partial = key0 + PAGE > len;
+    if (partial) {  // zero V rows past the sequence end (unwritten slots may hold anything)
+      for (int k = lane; k < PAGE * 16; k += 32) {
+        const int rr = k >> 4, ch = k & 15;
+        if (key0 + rr >= len)
+          *reinterpret_cast<uint4*>(wsm + st * STAGE_BYTES + PAGE_BYTES + swz(rr, ch)) = make_uint4(0, 0, 0, 0);
       }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);  // finite: key 0 of a page is always valid
-    const float c0 = exp2f(m0 - mn0), c1 = exp2f(m1 - mn1);
-    m0 = mn0;
-    m1 = mn1;
-    float p[2][4];
-    float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      p[j][0] = exp2f(s[j][0] - mn0);
-      p[j][1] = exp2f(s[j][1] - mn0);
-      p[j][2] = exp2f(s[j][2] - mn1);
-      p[j][3] = exp2f(s[j][3] - mn1);
-      s0 += p[j][0] + p[j][1];
-      s1 += p[j][2] + p[j][3];
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before TMA re-fills this stage
+      __syncwarp();
     }
-    s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
-    s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
-    l0 = l0 * c0 + s0;
-    l1 = l1 * c1 + s1;
-    const uint32_t pf[4] = {pack_bf16(p[0][0], p[0][1]), pack_bf16(p[0][2], p[0][3]), pack_bf16(p[1][0], p[1][1]),
-                            pack_bf16(p[1][2], p[1][3])};
+    // S^T = K Q^T, two independent accumulation chains (even / odd k-steps)
+    float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+    const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      o[j][0] *= c0;
-      o[j][1] *= c0;
-      o[j][2] *= c1;
-      o[j][3] *= c1;
+    for (int kk = 0; kk < 8; kk += 2) {
+      uint32_t a0, a1, a2, a3, c0, c1, c2, c3;
+      ldsm_x4(sk + swz(key, kk * 2 + (lane >> 4)), a0, a1, a2, a3);
+      ldsm_x4(sk + swz(key, kk * 2 + 2 + (lane >> 4)), c0, c1, c2, c3);
+      mma16816(s, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+      mma16816(s2, c0, c1, c2, c3, qb[kk + 1][0], qb[kk + 1][1]);
     }
+    // s[0], s[1]: key g, heads 2t, 2t+1 ; s[2], s[3]: key g+8
+    const bool v0 = key0 + g < len, v1 = key0 + g + 8 < len;
+    float x[4];
+    x[0] = v0 ? (s[0] + s2[0]) * scale : -INFINITY;
+    x[1] = v0 ? (s[1] + s2[1]) * scale : -INFINITY;
+    x[2] = v1 ? (s[2] + s2[2]) * scale : -INFINITY;
+    x[3] = v1 ? (s[3] + s2[3]) * scale : -INFINITY;
+    float mx[2] = {fmaxf(x[0], x[2]), fmaxf(x[1], x[3])};
 #pragma unroll
-    for (int nj = 0; nj < 8; ++nj) {
-      const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
-      const int ch = nj * 2 + (lane >> 4);
-      uint32_t v0, v1, v2, v3;
-      ldsm_x4_t(sv + swz(key, ch), v0, v1, v2, v3);
-      mma16816(o[2 * nj], pf, v0, v1);
-      mma16816(o[2 * nj + 1], pf, v2, v3);
+    for (int h = 0; h < 2; ++h) {
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 4));
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 8));
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 16));
     }
-    __syncwarp();
+    // key 0 of a page is always valid, so the new maxima are finite
+    const float mn0 = fmaxf(m[0], mx[0]), mn1 = fmaxf(m[1], mx[1]);
+    const float c0 = exp2f(m[0] - mn0), c1 = exp2f(m[1] - mn1);
+    m[0] = mn0;
+    m[1] = mn1;
+    const float p0 = exp2f(x[0] - mn0), p1 = exp2f(x[1] - mn1), p2 = exp2f(x[2] - mn0), p3 = exp2f(x[3] - mn1);
+    float sum0 = p0 + p2, sum1 = p1 + p3;
+    sum0 += __shfl_xor_sync(0xffffffffu, sum0, 4);
+    sum0 += __shfl_xor_sync(0xffffffffu, sum0, 8);
+    sum0 += __shfl_xor_sync(0xffffffffu, sum0, 16);
+    sum1 += __shfl_xor_sync(0xffffffffu, sum1, 4);
+    sum1 += __shfl_xor_sync(0xffffffffu, sum1, 8);
+    sum1 += __shfl_xor_sync(0xffffffffu, sum1, 16);
+    l[0] = l[0] * c0 + sum0;
+    l[1] = l[1] * c1 + sum1;
+    // P^T fragments -> B operand of O^T += V^T P^T
+    const uint32_t pb0 = movtrans(pack_bf16(p0, p1));  // keys 0-7
+    const uint32_t pb1 = movtrans(pack_bf16(p2, p3));  // keys 8-15
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      o[mt][0] *= c0;
+      o[mt][1] *= c1;
+      o[mt][2] *= c0;
+      o[mt][3] *= c1;
+    }
+    const int vkey = (lane & 7) + ((lane >> 4) << 3);
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4_t(sv + swz(vkey, mt * 2 + ((lane >> 3) & 1)), a0, a1, a2, a3);
+      mma16816(o[mt], a0, a1, a2, a3, pb0, pb1);
+    }
+    __syncwarp();  // every lane is done with stage st before lane 0 re-arms it
   }
-  cp_wait<0>();
   __syncthreads();
-  // merge the 4 warps: rows g < G only (row g + 8 is always padding for G <= 8)
-  float* sm_o = reinterpret_cast<float*>(smem);             // [WARPS][16][DH]
-  float* sm_ml = sm_o + WARPS * 16 * DH;                     // [WARPS][16][2]
-  if (t4 == 0) {
-    sm_ml[(warp * 16 + g) * 2] = m0;
-    sm_ml[(warp * 16 + g) * 2 + 1] = l0;
-    sm_ml[(warp * 16 + g + 8) * 2] = m1;
-    sm_ml[(warp * 16 + g + 8) * 2 + 1] = l1;
+  // merge the 4 warps (heads h < G); the rings are no longer needed
+  float* sm_o = reinterpret_cast<float*>(smem);  // [WARPS][8 heads][DH]
+  float* sm_ml = sm_o + WARPS * 8 * DH;          // [WARPS][8][2]
+  if (g == 0) {
+    sm_ml[(warp * 8 + 2 * t4) * 2] = m[0];
+    sm_ml[(warp * 8 + 2 * t4) * 2 + 1] = l[0];
+    sm_ml[(warp * 8 + 2 * t4 + 1) * 2] = m[1];
+    sm_ml[(warp * 8 + 2 * t4 + 1) * 2 + 1] = l[1];
   }
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int col = j * 8 + 2 * t4;
-    sm_o[(warp * 16 + g) * DH + col] = o[j][0];
-    sm_o[(warp * 16 + g) * DH + col + 1] = o[j][1];
-    sm_o[(warp * 16 + g + 8) * DH + col] = o[j][2];
-    sm_o[(warp * 16 + g + 8) * DH + col + 1] = o[j][3];
+  for (int mt = 0; mt < 8; ++mt) {
+    const int d0 = mt * 16 + g;
+    sm_o[(warp * 8 + 2 * t4) * DH + d0] = o[mt][0];
+    sm_o[(warp * 8 + 2 * t4 + 1) * DH + d0] = o[mt][1];
+    sm_o[(warp * 8 + 2 * t4) * DH + d0 + 8] = o[mt][2];
+    sm_o[(warp * 8 + 2 * t4 + 1) * DH + d0 + 8] = o[mt][3];
   }
   __syncthreads();
   for (int t = threadIdx.x; t < G * DH; t += blockDim.x) {
-    const int gg = t / DH, dim = t % DH;
+    const int h = t / DH, dim = t % DH;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) M = fmaxf(M, sm_ml[(w * 16 + gg) * 2]);
+    for (int w = 0; w < WARPS; ++w) M = fmaxf(M, sm_ml[(w * 8 + h) * 2]);
     float L = 0.f, O = 0.f;
     if (M != -INFINITY) {
 #pragma unroll
       for (int w = 0; w < WARPS; ++w) {
-        const float c = exp2f(sm_ml[(w * 16 + gg) * 2] - M);
-        L += sm_ml[(w * 16 + gg) * 2 + 1] * c;
-        O += sm_o[(w * 16 + gg) * DH + dim] * c;
+        const float c = exp2f(sm_ml[(w * 8 + h) * 2] - M);
+        L += sm_ml[(w * 8 + h) * 2 + 1] * c;
+        O += sm_o[(w * 8 + h) * DH + dim] * c;
       }
     }
-    const int head = kvh * G + gg;
+    const int head = kvh * G + h;
     if (n_splits == 1) {
       bf16* out = reinterpret_cast<bf16*>(a.o) + (size_t)r * a.hq * DH + (size_t)head * DH;
       out[dim] = __float2bfloat16_rn(O / L);
@@ -233,11 +263,39 @@ __global__ void __launch_bounds__(128) decode_tc_kernel(DecodeAttnArgs a, int pp
   }
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  }
+  return fn;
+}
+// pool viewed as [n_pages * h_kv * 16 rows][128 dims]; box = 16 rows x 64 dims, SWIZZLE_128B
+static bool pool_map(CUtensorMap* m, const void* pool, uint64_t rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)DH, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)DH * 2};
+  cuuint32_t box[2] = {64, PAGE};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace dtc
 
 bool decode_tc_supported(const DecodeAttnArgs& a) {
   const int G = a.hq / a.hkv;
-  return a.dh == dtc::DH && a.page_size == dtc::PAGE && G >= 1 && G <= 8;
+  return a.dh == dtc::DH && a.page_size == dtc::PAGE && G >= 1 && G <= 8 && a.n_pages > 0 &&
+         dtc::encode_fn() != nullptr;
 }
 
 int launch_decode_tc(const DecodeAttnArgs& a, int pps, int n_splits, cudaStream_t st) {
@@ -246,8 +304,11 @@ int launch_decode_tc(const DecodeAttnArgs& a, int pps, int n_splits, cudaStream_
     cudaFuncSetAttribute(dtc::decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dtc::SMEM);
     attr = true;
   }
+  CUtensorMap mk, mv;
+  const uint64_t rows = (uint64_t)a.n_pages * a.hkv * dtc::PAGE;
+  if (!dtc::pool_map(&mk, a.k_pool, rows) || !dtc::pool_map(&mv, a.v_pool, rows)) return -1;
   dim3 grid(n_splits, a.hkv, a.n);
-  dtc::decode_tc_kernel<<<grid, 128, dtc::SMEM, st>>>(a, pps, n_splits);
+  dtc::decode_tc_kernel<<<grid, 32 * dtc::WARPS, dtc::SMEM, st>>>(mk, mv, a, pps, n_splits);
   return 1;
 }
 

@@ -1,0 +1,410 @@
+// Causal prefill attention over the paged KV cache on 5th-generation tensor cores (tcgen05/TMEM/TMA).
+//
+// Chunked prefill (§4.1; readings #2, #6, #7): a chunk of q tokens at positions
+// c..c+q-1 attends to its c-token prefix and to itself causally.  One CTA = 128 query rows of one
+// query head; 128-key tiles (8 pages of 16 tokens, fetched page by page with TMA straight from the
+// paged pool) double-buffered in shared memory.
+//   warp 0      TMA producer: Q once (2 x 64-column boxes), K and V tiles (16-row boxes per page)
+//   warp 1      TMEM allocator + tcgen05.mma issuer:  S_j = Q K_j^T  (UMMA 128x128x16, K-major operands)
+//               into one of two TMEM S buffers, then O += P_{j-1} V_{j-1} (A = P from smem, B = V
+//               MN-major), so the MMAs of S_{j+1} overlap the softmax of tile j
+//   warps 2..5  softmax, one thread per query row (= TMEM lane): row max / exp2 / row sum entirely in
+//               registers (no shuffles), P written to smem in the UMMA SW128 layout; the running max
+//               is re-based (O rescaled in TMEM) only when it grows by more than 2^8, so P <= 256
+// Keys past the causal end are masked; the unwritten slots of the sequence's last page are zeroed in
+// the V tile before the P.V MMA (unwritten page slots may hold anything).
+#include <cuda.h>
+
+#include "dev_common.cuh"
+#include "kernels.h"
+
+namespace duet {
+namespace fatc {
+
+constexpr int BQ = 128, BKV = 128, DH = 128, PAGE = 16;
+constexpr int SUB = 128 * 64 * 2;  // [128 rows][64 cols] bf16 SW128 sub-tile = 16 KiB
+constexpr int TILE = 2 * SUB;      // [128][128] = 32 KiB
+constexpr int OFF_Q = 0, OFF_K = TILE, OFF_V = 3 * TILE, OFF_P = 5 * TILE, OFF_BAR = 6 * TILE;
+constexpr int SMEM = 6 * TILE + 256 + 1024;
+constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// K-major SW128 descriptor (rows of 128 B, 8-row atoms of 1 KiB): LBO unused (1), SBO = 1 KiB
+__device__ __forceinline__ uint64_t desc_k(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) |
+         ((uint64_t)2 << 61);
+}
+// MN-major SW128 descriptor: 64-element (128 B) MN blocks LBO = 16 KiB apart, 8-row K groups SBO = 1 KiB
+__device__ __forceinline__ uint64_t desc_mn(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(SUB >> 4) << 16) | ((uint64_t)64 << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// kind::f16, D f32, A = B = bf16, M = 128, N = 128; b_mn selects an MN-major B operand (bit 16)
+__host__ __device__ constexpr uint32_t idesc(bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(128 >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+struct Params {
+  const int* row0;
+  const int* qlen;
+  const int* cpre;
+  const int* seq_row;
+  const int* table;
+  int max_pages, hq, hkv, n_qtiles;
+  bf16* o;
+};
+
+__global__ void __launch_bounds__(192, 1)
+    fa_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                 const __grid_constant__ CUtensorMap map_v, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bar = (uint64_t*)(smem + OFF_BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;    // [2]
+  uint64_t* s_free = bar + 7;    // [2]
+  uint64_t* p_full = bar + 9;
+  uint64_t* pv_done = bar + 10;
+  uint32_t* tmem_slot = (uint32_t*)(bar + 12);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = p.n_qtiles - 1 - blockIdx.x;  // heavy (late) tiles first
+  const int head = blockIdx.y, s_id = blockIdx.z;
+  const int qlen = p.qlen[s_id];
+  if (qt * BQ >= qlen) return;
+  const int G = p.hq / p.hkv, kvh = head / G;
+  const int row0 = p.row0[s_id], cpre = p.cpre[s_id];
+  const int* tab = p.table + (size_t)p.seq_row[s_id] * p.max_pages;
+  const int q0 = qt * BQ;
+  const int q_last = min(q0 + BQ, qlen) - 1;
+  const int kv_end = cpre + q_last + 1;
+  const int n_kt = (kv_end + BKV - 1) / BKV;
+  const int n_pages_total = (kv_end + PAGE - 1) / PAGE;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t T_S[2] = {tmem, tmem + 128};
+  const uint32_t T_O = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      mbar_expect_tx(q_full, TILE);
+      tma_load_2d(&map_q, q_full, smem + OFF_Q, head * DH, row0 + q0);
+      tma_load_2d(&map_q, q_full, smem + OFF_Q + SUB, head * DH + 64, row0 + q0);
+      for (int j = 0; j < n_kt; ++j) {
+        const int s = j & 1;
+        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+        const int pg0 = j * (BKV / PAGE);
+        const int n_pg = min(BKV / PAGE, n_pages_total - pg0);
+        mbar_expect_tx(&kv_full[s], n_pg * 4 * (PAGE * 128));
+        uint8_t* kd = smem + OFF_K + s * TILE;
+        uint8_t* vd = smem + OFF_V + s * TILE;
+        for (int pp = 0; pp < n_pg; ++pp) {
+          const int prow = (tab[pg0 + pp] * p.hkv + kvh) * PAGE;
+          const int off = pp * PAGE * 128;
+          tma_load_2d(&map_k, &kv_full[s], kd + off, 0, prow);
+          tma_load_2d(&map_k, &kv_full[s], kd + SUB + off, 64, prow);
+          tma_load_2d(&map_v, &kv_full[s], vd + off, 0, prow);
+          tma_load_2d(&map_v, &kv_full[s], vd + SUB + off, 64, prow);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (lane 0 issues; the warp zeroes V tails)
+    constexpr uint32_t ID_S = idesc(false), ID_PV = idesc(true);
+    const uint32_t sq = smem_u32(smem + OFF_Q);
+    mbar_wait(q_full, 0);
+    for (int j = 0; j <= n_kt; ++j) {
+      if (j < n_kt) {
+        const int s = j & 1;
+        if (j >= 2) mbar_wait(&s_free[s], ((j - 2) >> 1) & 1);
+        mbar_wait(&kv_full[s], (j >> 1) & 1);
+        tc_after();
+        if (lane == 0) {
+          const uint32_t sk = smem_u32(smem + OFF_K + s * TILE);
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
+            umma(T_S[s], desc_k(sq + off), desc_k(sk + off), ID_S, kk > 0);
+          }
+          umma_commit(&s_full[s]);
+        }
+        __syncwarp();
+      }
+      if (j >= 1) {
+        const int jp = j - 1, sp = jp & 1;
+        const int pg0 = jp * (BKV / PAGE);
+        const int n_pg = min(BKV / PAGE, n_pages_total - pg0);
+        uint8_t* vt = smem + OFF_V + sp * TILE;
+        // zero the unwritten slots of the sequence's last page (keys >= kv_end) in this V tile
+        if (jp == n_kt - 1 && (kv_end % PAGE) != 0) {
+          const int r0 = (n_pg - 1) * PAGE + (kv_end % PAGE), r1 = n_pg * PAGE;
+          for (int i = lane; i < (r1 - r0) * 16; i += 32) {
+            const int rr = r0 + i / 16, ch = i % 16;
+            *reinterpret_cast<uint4*>(vt + (ch >> 3) * SUB + rr * 128 + ((ch & 7) << 4)) = make_uint4(0, 0, 0, 0);
+          }
+          fence_async_smem();
+        }
+        __syncwarp();
+        mbar_wait(p_full, jp & 1);
+        tc_after();
+        if (lane == 0) {
+          const uint32_t spp = smem_u32(smem + OFF_P), sv = smem_u32(vt);
+          for (int kk = 0; kk < n_pg; ++kk) {  // 16 keys (one page) per UMMA k-step
+            const uint32_t aoff = (kk >> 2) * SUB + (kk & 3) * 32;
+            umma(T_O, desc_k(spp + aoff), desc_mn(sv + kk * PAGE * 128), ID_PV, (jp > 0 || kk > 0));
+          }
+          umma_commit(&kv_empty[sp]);
+          umma_commit(pv_done);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------ softmax warps: one thread per query row
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;                              // row in tile = TMEM lane
+    const int pos = min(cpre + q0 + r, kv_end - 1);              // clamp rows past the chunk
+    const float sc = rsqrtf((float)DH) * 1.4426950408889634f;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    uint8_t* prow = smem + OFF_P + r * 128;
+    const uint32_t sw = (uint32_t)(r & 7);
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kt; ++j) {
+      const int s = j & 1;
+      mbar_wait(&s_full[s], (j >> 1) & 1);
+      tc_after();
+      const int kbase = j * BKV;
+      // pass 1: row max over visible keys
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < BKV; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(T_S[s] + lane_base + c, v);
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (kbase + c + e <= pos) mx = fmaxf(mx, __uint_as_float(v[e]) * sc);
+      }
+      const float m_new = fmaxf(m_used, mx);
+      const bool rescale = m_new > m_used + RESCALE_THRESHOLD;
+      // P buffer and O are free once PV(j-1) has completed
+      if (j >= 1) {
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_after();
+      }
+      if (rescale) {
+        if (j >= 1) {
+          const float f = exp2f(m_used - m_new);
+          l *= f;
+#pragma unroll 1
+          for (int c = 0; c < DH; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(T_O + lane_base + c, v);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * f);
+            tmem_st32(T_O + lane_base + c, v);
+          }
+        }
+        m_used = m_new;
+      }
+      // pass 2: P = exp2(s - m_used) (masked -> 0), row sum, P row -> smem (SW128, K-major)
+#pragma unroll
+      for (int c = 0; c < BKV; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(T_S[s] + lane_base + c, v);
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float p0 = (kbase + c + e <= pos) ? exp2f(__uint_as_float(v[e]) * sc - m_used) : 0.f;
+          const float p1 = (kbase + c + e + 1 <= pos) ? exp2f(__uint_as_float(v[e + 1]) * sc - m_used) : 0.f;
+          l += p0 + p1;
+          __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+          pk[e / 2] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        // keys c..c+31 = 4 chunks of 8 keys in sub-tile c / 64
+        uint8_t* sub = prow + (c >> 6) * SUB;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint32_t chunk = (uint32_t)(((c & 63) >> 3) + q4);
+          *reinterpret_cast<uint4*>(sub + ((chunk ^ sw) << 4)) =
+              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+        }
+      }
+      tc_before();
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&s_free[s]);
+        mbar_arrive(p_full);
+      }
+    }
+    // epilogue: O / l -> bf16 -> global
+    mbar_wait(pv_done, (n_kt - 1) & 1);
+    tc_after();
+    const bool row_ok = q0 + r < qlen;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    bf16* dst = p.o + (size_t)(row0 + q0 + r) * p.hq * DH + (size_t)head * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH; c += 32) {
+      uint32_t v[32];
+      tmem_ld32(T_O + lane_base + c, v);
+      if (row_ok) {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          float o8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o8[e] = __uint_as_float(v[q4 * 8 + e]) * inv;
+          store16<bf16>(dst + c + q4 * 8, o8);
+        }
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  }
+  return fn;
+}
+static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems,
+                     uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace fatc
+
+bool fa_tc_supported(const PrefillAttnArgs& a) {
+  return a.dh == fatc::DH && a.page_size == fatc::PAGE && a.n_pages > 0 && a.q_stride % 8 == 0 &&
+         fatc::encode_fn() != nullptr && a.total_rows > 0;
+}
+
+int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fatc::fa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::SMEM);
+    attr = true;
+  }
+  CUtensorMap mq, mk, mv;
+  const uint64_t pool_rows = (uint64_t)a.n_pages * a.hkv * fatc::PAGE;
+  if (!fatc::make_map(&mq, a.q, (uint64_t)a.total_rows, (uint64_t)a.q_stride, (uint64_t)a.q_stride, 128)) return -1;
+  if (!fatc::make_map(&mk, a.k_pool, pool_rows, fatc::DH, fatc::DH, fatc::PAGE)) return -1;
+  if (!fatc::make_map(&mv, a.v_pool, pool_rows, fatc::DH, fatc::DH, fatc::PAGE)) return -1;
+  fatc::Params p{a.row0, a.qlen, a.cpre, a.seq_row, a.table, a.max_pages, a.hq, a.hkv, 0, (bf16*)a.o};
+  p.n_qtiles = (a.max_q + fatc::BQ - 1) / fatc::BQ;
+  dim3 grid(p.n_qtiles, a.hq, a.n_seqs);
+  fatc::fa_tc_kernel<<<grid, 192, fatc::SMEM, st>>>(mq, mk, mv, p);
+  return 1;
+}
+
+}  // namespace duet

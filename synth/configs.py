@@ -74,6 +74,13 @@ CONFIGS = {
                                                decode=tuple(2048 + (6144 * r) // 255 for r in range(256)), k=1,
                                                tbt_slo_s=50e-3), dtype="bf16", seed=4791 + 3,
                    note="Llama-3-8B 32 layers: 8k prompt into 256 decodes at ctx 2k-8k, TBT SLO 50 ms"),
+    # cfg3 with the context ramp narrowed to 2k-6k so that 32 layers of KV (about 129 GiB) plus weights and
+    # workspace fit one 180 GB B200 (SURVEY.md §8(d) fallback); used when the full ramp does not fit
+    "cfg3-fit": Config("cfg3-fit", LLAMA3_8B, BatchCfg(prefill=((8192, 0),),
+                                                       decode=tuple(2048 + (4096 * r) // 255 for r in range(256)),
+                                                       k=1, tbt_slo_s=50e-3), dtype="bf16", seed=4791 + 3,
+                       note="Llama-3-8B 32 layers: 8k prompt into 256 decodes at ctx 2k-6k (fits 180 GB), "
+                            "TBT SLO 50 ms"),
 }
 
 
