@@ -14,18 +14,20 @@
 // One CTA per (split, kv head, request).
 #include <cuda.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "dev_common.cuh"
 #include "kernels.h"
 
 namespace duet {
 namespace dtc {
 
-constexpr int DH = 128, PAGE = 16, NST = 3, WARPS = 8;
+constexpr int DH = 128, PAGE = 16;
 constexpr int HALF = PAGE * 128;              // one 16-row x 64-col SW128 box = 2 KiB
 constexpr int PAGE_BYTES = 2 * HALF;          // 4 KiB: one kv head of one page
 constexpr int STAGE_BYTES = 2 * PAGE_BYTES;   // K + V
-constexpr int WARP_BYTES = NST * STAGE_BYTES; // 24 KiB
-constexpr int SMEM = WARPS * WARP_BYTES + 1024 + 256;
+__host__ __device__ constexpr int smem_bytes(int warps, int nst) { return warps * nst * STAGE_BYTES + 1024 + 512; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 // byte offset of 16-B chunk ch (0..15) of row r in a page stored as two SW128 [16][64] halves
@@ -84,9 +86,13 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-__global__ void __launch_bounds__(256) decode_tc_kernel(const __grid_constant__ CUtensorMap map_k,
-                                                         const __grid_constant__ CUtensorMap map_v, DecodeAttnArgs a,
-                                                         int pps, int n_splits) {
+// WARPS consumer warps per CTA, NST-stage ring per warp; TMA = pages fetched by TMA boxes (lane 0),
+// else by cp.async from all 32 lanes (cheaper to issue on small SM partitions).
+template <int WARPS, int NST, bool TMA>
+__global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_constant__ CUtensorMap map_k,
+                                                                const __grid_constant__ CUtensorMap map_v,
+                                                                DecodeAttnArgs a, int pps, int n_splits) {
+  constexpr int WARP_BYTES = NST * STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int split = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(256) decode_tc_kernel(const __grid_constant__ 
   uint8_t* wsm = smem + warp * WARP_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + WARPS * WARP_BYTES) + warp * NST;
   const int g = lane >> 2, t4 = lane & 3;
-  if (lane == 0) {
+  if (TMA && lane == 0) {
     for (int i = 0; i < NST; ++i) mbar_init(&full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -119,19 +125,49 @@ __global__ void __launch_bounds__(256) decode_tc_kernel(const __grid_constant__ 
   }
   const int first = pg0 + warp;
   const int n_mine = first < pg1 ? (pg1 - first + WARPS - 1) / WARPS : 0;
-  auto issue = [&](int i) {  // lane 0: TMA page i of this warp into stage i % NST
+  uint32_t soff[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) soff[k] = swz(2 * k + (lane >> 4), lane & 15);
+  auto issue = [&](int i) {  // page i of this warp into stage i % NST
     const int st = i % NST;
-    const int prow = (tab[first + i * WARPS] * a.hkv + kvh) * PAGE;
     uint8_t* dk = wsm + st * STAGE_BYTES;
     uint8_t* dv = dk + PAGE_BYTES;
-    mbar_expect_tx(&full[st], STAGE_BYTES);
-    tma_load_2d(&map_k, &full[st], dk, 0, prow);
-    tma_load_2d(&map_k, &full[st], dk + HALF, 64, prow);
-    tma_load_2d(&map_v, &full[st], dv, 0, prow);
-    tma_load_2d(&map_v, &full[st], dv + HALF, 64, prow);
+    if constexpr (TMA) {  // lane 0 only
+      const int prow = (tab[first + i * WARPS] * a.hkv + kvh) * PAGE;
+      mbar_expect_tx(&full[st], STAGE_BYTES);
+      tma_load_2d(&map_k, &full[st], dk, 0, prow);
+      tma_load_2d(&map_k, &full[st], dk + HALF, 64, prow);
+      tma_load_2d(&map_v, &full[st], dv, 0, prow);
+      tma_load_2d(&map_v, &full[st], dv + HALF, 64, prow);
+    } else {  // all lanes: 256 x 16 B per tensor; slots past the end are zero-filled
+      // chunk k*32 + lane of the 4 KiB page block is row 2k + lane/16, 16-B column lane%16: its global
+      // offset is (k*32 + lane) * 8 elements and its swizzled smem offset soff[k] (precomputed)
+      const int pg = first + i * WARPS;
+      const size_t base = ((size_t)tab[pg] * a.hkv + kvh) * PAGE * DH + lane * 8;
+      const bf16* ks = reinterpret_cast<const bf16*>(a.k_pool) + base;
+      const bf16* vs = reinterpret_cast<const bf16*>(a.v_pool) + base;
+      const uint32_t sk = smem_u32(dk), sv = smem_u32(dv);
+      const int rows_valid = len - pg * PAGE;  // >= 16 except on the last page
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int sz = (2 * k + (lane >> 4)) < rows_valid ? 16 : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sk + soff[k]), "l"(ks + k * 256),
+                     "r"(sz) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sv + soff[k]), "l"(vs + k * 256),
+                     "r"(sz) : "memory");
+      }
+    }
   };
-  if (lane == 0)
-    for (int i = 0; i < NST - 1 && i < n_mine; ++i) issue(i);
+  if constexpr (TMA) {
+    if (lane == 0)
+      for (int i = 0; i < NST - 1 && i < n_mine; ++i) issue(i);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NST - 1; ++i) {
+      if (i < n_mine) issue(i);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  }
 
   const float scale = rsqrtf((float)DH) * 1.4426950408889634f;
   float o[8][4];  // O^T: m-tile mt -> dims mt*16 + {g, g+8}, heads {2t, 2t+1}
@@ -141,12 +177,19 @@ __global__ void __launch_bounds__(256) decode_tc_kernel(const __grid_constant__ 
 
   for (int i = 0; i < n_mine; ++i) {
     // refill the stage consumed in the previous iteration (all lanes are past it: __syncwarp below)
-    if (lane == 0 && i + NST - 1 < n_mine) issue(i + NST - 1);
     const int st = i % NST;
-    mbar_wait(&full[st], (i / NST) & 1);
+    if constexpr (TMA) {
+      if (lane == 0 && i + NST - 1 < n_mine) issue(i + NST - 1);
+      mbar_wait(&full[st], (i / NST) & 1);
+    } else {
+      if (i + NST - 1 < n_mine) issue(i + NST - 1);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group %0;" ::"n"(NST - 1) : "memory");
+      __syncwarp();
+    }
     const uint32_t sk = smem_u32(wsm + st * STAGE_BYTES), sv = sk + PAGE_BYTES;
     const int key0 = (first + i * WARPS) * PAGE;
-    const bool partial = key0 + PAGE > len;
+    const bool partial = TMA && key0 + PAGE > len;
     if (partial) {  // zero V rows past the sequence end (unwritten slots may hold anything)
       for (int k = lane; k < PAGE * 16; k += 32) {
         const int rr = k >> 4, ch = k & 15;
@@ -298,17 +341,31 @@ bool decode_tc_supported(const DecodeAttnArgs& a) {
          dtc::encode_fn() != nullptr;
 }
 
-int launch_decode_tc(const DecodeAttnArgs& a, int pps, int n_splits, cudaStream_t st) {
+template <int W, int N, bool T>
+static void launch_variant(const CUtensorMap& mk, const CUtensorMap& mv, const DecodeAttnArgs& a, int pps,
+                           int n_splits, cudaStream_t st) {
   static bool attr = false;
+  constexpr int smem = dtc::smem_bytes(W, N);
   if (!attr) {
-    cudaFuncSetAttribute(dtc::decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dtc::SMEM);
+    cudaFuncSetAttribute(dtc::decode_tc_kernel<W, N, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
+  dim3 grid(n_splits, a.hkv, a.n);
+  dtc::decode_tc_kernel<W, N, T><<<grid, 32 * W, smem, st>>>(mk, mv, a, pps, n_splits);
+}
+
+int launch_decode_tc(const DecodeAttnArgs& a, int pps, int n_splits, cudaStream_t st) {
   CUtensorMap mk, mv;
   const uint64_t rows = (uint64_t)a.n_pages * a.hkv * dtc::PAGE;
   if (!dtc::pool_map(&mk, a.k_pool, rows) || !dtc::pool_map(&mv, a.v_pool, rows)) return -1;
-  dim3 grid(n_splits, a.hkv, a.n);
-  dtc::decode_tc_kernel<<<grid, 32 * dtc::WARPS, dtc::SMEM, st>>>(mk, mv, a, pps, n_splits);
+  // variant (A/B measurements): DUET_DECODE = tma8x3 | cp4x6 | cp8x3 | cp4x3x2 (2 CTAs/SM)
+  static const char* v = getenv("DUET_DECODE");
+  const char* sel = v ? v : "cp4x3x2";
+  if (!strcmp(sel, "tma8x3")) launch_variant<8, 3, true>(mk, mv, a, pps, n_splits, st);
+  else if (!strcmp(sel, "cp8x3")) launch_variant<8, 3, false>(mk, mv, a, pps, n_splits, st);
+  else if (!strcmp(sel, "cp4x6")) launch_variant<4, 6, false>(mk, mv, a, pps, n_splits, st);
+  else if (!strcmp(sel, "cp2x4x3")) launch_variant<2, 4, false>(mk, mv, a, pps, n_splits, st);
+  else launch_variant<4, 3, false>(mk, mv, a, pps, n_splits, st);  // 96 KiB -> 2 CTAs per SM
   return 1;
 }
 

@@ -119,11 +119,11 @@ struct Params {
   const int* table;
   int max_pages, hq, hkv, n_qtiles;
   bf16* o;
+  const bf16* k_pool;
+  const bf16* v_pool;
 };
 
-__global__ void __launch_bounds__(192, 1)
-    fa_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                 const __grid_constant__ CUtensorMap map_v, Params p) {
+__global__ void __launch_bounds__(320, 1) fa_tc_kernel(const __grid_constant__ CUtensorMap map_q, Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bar = (uint64_t*)(smem + OFF_BAR);
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_full[i], 4);  // one arrive per loader warp
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 4);
@@ -175,27 +175,52 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ------------------------------------------------ TMA producer
+      // ------------------------------------------------ Q tile (TMA, two 64-column boxes)
       mbar_expect_tx(q_full, TILE);
       tma_load_2d(&map_q, q_full, smem + OFF_Q, head * DH, row0 + q0);
       tma_load_2d(&map_q, q_full, smem + OFF_Q + SUB, head * DH + 64, row0 + q0);
-      for (int j = 0; j < n_kt; ++j) {
-        const int s = j & 1;
-        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        const int pg0 = j * (BKV / PAGE);
-        const int n_pg = min(BKV / PAGE, n_pages_total - pg0);
-        mbar_expect_tx(&kv_full[s], n_pg * 4 * (PAGE * 128));
-        uint8_t* kd = smem + OFF_K + s * TILE;
-        uint8_t* vd = smem + OFF_V + s * TILE;
-        for (int pp = 0; pp < n_pg; ++pp) {
-          const int prow = (tab[pg0 + pp] * p.hkv + kvh) * PAGE;
-          const int off = pp * PAGE * 128;
-          tma_load_2d(&map_k, &kv_full[s], kd + off, 0, prow);
-          tma_load_2d(&map_k, &kv_full[s], kd + SUB + off, 64, prow);
-          tma_load_2d(&map_v, &kv_full[s], vd + off, 0, prow);
-          tma_load_2d(&map_v, &kv_full[s], vd + SUB + off, 64, prow);
-        }
+    }
+  } else if (warp >= 6) {
+    // ------------------------------------------------ K/V loaders: 4 warps of cp.async (16 B per lane)
+    // A 128-key tile is 8 scattered 4 KiB page blocks per tensor; issuing them as TMA boxes costs one
+    // serialized instruction per 2 KiB box, so the gather is spread over 128 threads instead.  Keys past
+    // the causal end are zero-filled (cp.async src-size 0): unwritten page slots may hold anything.
+    const int lt = threadIdx.x - 6 * 32;  // 0..127
+    const bf16* Kg = p.k_pool;
+    const bf16* Vg = p.v_pool;
+    const size_t page_stride = (size_t)p.hkv * PAGE * DH;
+    auto issue = [&](int j) {
+      const int s = j & 1;
+      const uint32_t kd = smem_u32(smem + OFF_K + s * TILE), vd = smem_u32(smem + OFF_V + s * TILE);
+#pragma unroll 4
+      for (int i = 0; i < (BKV * 16) / 128; ++i) {  // 2048 16-B chunks per tensor
+        const int c = lt + i * 128;
+        const int rr = c >> 4, ch = c & 15;
+        const int key = j * BKV + rr;
+        const bool v = key < kv_end;
+        const size_t off = v ? (size_t)tab[key / PAGE] * page_stride + ((size_t)kvh * PAGE + (key % PAGE)) * DH + ch * 8
+                             : 0;
+        const uint32_t so = (uint32_t)((ch >> 3) * SUB + rr * 128 + (((ch & 7) ^ (rr & 7)) << 4));
+        const int sz = v ? 16 : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(kd + so), "l"(Kg + off), "r"(sz)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(vd + so), "l"(Vg + off), "r"(sz)
+                     : "memory");
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto publish = [&](int j) {  // tile j's copies (this thread's) have landed -> visible to the async proxy
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&kv_full[j & 1]);
+    };
+    // tile j is published as soon as it lands: the MMA issuer needs K_{j} before it can retire
+    // P_{j-1} V_{j-1}, which is what frees the buffer tile j+1 goes to (no publish may wait on a free)
+    for (int j = 0; j < n_kt; ++j) {
+      mbar_wait(&kv_empty[j & 1], ((j >> 1) & 1) ^ 1);
+      issue(j);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      publish(j);
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (lane 0 issues; the warp zeroes V tails)
@@ -223,17 +248,7 @@ __global__ void __launch_bounds__(192, 1)
         const int jp = j - 1, sp = jp & 1;
         const int pg0 = jp * (BKV / PAGE);
         const int n_pg = min(BKV / PAGE, n_pages_total - pg0);
-        uint8_t* vt = smem + OFF_V + sp * TILE;
-        // zero the unwritten slots of the sequence's last page (keys >= kv_end) in this V tile
-        if (jp == n_kt - 1 && (kv_end % PAGE) != 0) {
-          const int r0 = (n_pg - 1) * PAGE + (kv_end % PAGE), r1 = n_pg * PAGE;
-          for (int i = lane; i < (r1 - r0) * 16; i += 32) {
-            const int rr = r0 + i / 16, ch = i % 16;
-            *reinterpret_cast<uint4*>(vt + (ch >> 3) * SUB + rr * 128 + ((ch & 7) << 4)) = make_uint4(0, 0, 0, 0);
-          }
-          fence_async_smem();
-        }
-        __syncwarp();
+        uint8_t* vt = smem + OFF_V + sp * TILE;  // keys >= kv_end were zero-filled by the loaders
         mbar_wait(p_full, jp & 1);
         tc_after();
         if (lane == 0) {
@@ -395,15 +410,14 @@ int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(fatc::fa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::SMEM);
     attr = true;
   }
-  CUtensorMap mq, mk, mv;
-  const uint64_t pool_rows = (uint64_t)a.n_pages * a.hkv * fatc::PAGE;
+  CUtensorMap mq;
   if (!fatc::make_map(&mq, a.q, (uint64_t)a.total_rows, (uint64_t)a.q_stride, (uint64_t)a.q_stride, 128)) return -1;
-  if (!fatc::make_map(&mk, a.k_pool, pool_rows, fatc::DH, fatc::DH, fatc::PAGE)) return -1;
-  if (!fatc::make_map(&mv, a.v_pool, pool_rows, fatc::DH, fatc::DH, fatc::PAGE)) return -1;
-  fatc::Params p{a.row0, a.qlen, a.cpre, a.seq_row, a.table, a.max_pages, a.hq, a.hkv, 0, (bf16*)a.o};
+  fatc::Params p{a.row0,  a.qlen, a.cpre,       a.seq_row,           a.table, a.max_pages,
+                 a.hq,    a.hkv,  0,            (bf16*)a.o,          (const bf16*)a.k_pool,
+                 (const bf16*)a.v_pool};
   p.n_qtiles = (a.max_q + fatc::BQ - 1) / fatc::BQ;
   dim3 grid(p.n_qtiles, a.hq, a.n_seqs);
-  fatc::fa_tc_kernel<<<grid, 192, fatc::SMEM, st>>>(mq, mk, mv, p);
+  fatc::fa_tc_kernel<<<grid, 320, fatc::SMEM, st>>>(mq, p);
   return 1;
 }
 

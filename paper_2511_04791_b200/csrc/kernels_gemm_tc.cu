@@ -59,6 +59,14 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -117,10 +125,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 template <int BN, int EPI, bool SWAP>
 struct Cfg {
   static constexpr int A_TILES = (SWAP && EPI == EPI_SWIGLU) ? 2 : 1;
+  // swap mode: cp.async producers (CP) or one TMA producer with two CTAs per SM (two TMA issuers and
+  // two MMA/epilogue pipelines per SM: a TMA instruction costs its issuing thread ~0.25 us on B200,
+  // profiles/r01_probe_tma_bw.txt, so one issuer per SM cannot stream a small partition's HBM share)
+  static constexpr bool CP = false;
+  static constexpr int NPROD = (SWAP && CP) ? 4 : 1;         // producer warps
+  static constexpr int THREADS = 192 + (NPROD - 1) * 32;
+  static constexpr int CTAS = (SWAP && !CP) ? 2 : 1;         // CTAs per SM
   static constexpr int A_BYTES = A_TILES * BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int SMEM_BUDGET = CTAS == 2 ? 104 * 1024 : 200 * 1024;
+  static constexpr int STAGES = SMEM_BUDGET / STAGE_BYTES > 8 ? 8 : SMEM_BUDGET / STAGE_BYTES;
   static constexpr int ACC_COLS = (SWAP && EPI == EPI_SWIGLU) ? 2 * BN : BN;
   static constexpr int TMEM_COLS = 2 * ACC_COLS <= 32 ? 32 : (2 * ACC_COLS <= 64 ? 64 : (2 * ACC_COLS <= 128 ? 128 : (2 * ACC_COLS <= 256 ? 256 : 512)));
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
@@ -135,10 +151,13 @@ struct Params {
   const bf16* bias;
   int ldc, ldr;
   int n_up_off;       // SwiGLU: row offset of the up rows in W (= N)
+  const bf16* X;      // swap mode (cp.async producers): activations [M][ldx], weights [rows][ldw]
+  const bf16* W;
+  int ldx, ldw;
 };
 
 template <int BN, int EPI, bool SWAP>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP>::CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, Params p) {
   using CF = Cfg<BN, EPI, SWAP>;
   constexpr int S = CF::STAGES;
@@ -159,7 +178,7 @@ __global__ void __launch_bounds__(192, 1)
     prefetch_map(&map_x);
     prefetch_map(&map_w);
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], CF::NPROD);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -178,9 +197,72 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (SWAP && CF::CP && (warp == 0 || warp >= 6)) {
+    // ---------------- swap mode: 4 producer warps (128 threads) stream the weight tile and the token
+    // tile with cp.async (16 B per lane) into the SW128 K-major layout.  On a small SM partition a TMA
+    // unit sustains only ~60 GB/s per SM from HBM (profiles/r01_probe_tma_bw.txt) while cp.async from
+    // 128 threads reaches ~130 GB/s; the decode-side GEMMs are weight-streaming, so this is their bound.
+    // A stage is published (fence.proxy.async + mbarrier arrive) LAG stages after it was issued, with
+    // LAG <= STAGES - 2 so that a publication never waits on the slot it frees.
+    constexpr int LAG = S - 2;
+    const int pt = (warp == 0 ? 0 : warp - 5) * 32 + lane;  // 0..127
+    const bf16* X = p.X;
+    const bf16* Wt = p.W;
+    int s = 0, ps = 0, inflight = 0;
+    uint32_t ph = 0;
+    auto publish = [&]() {
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[ps]);
+      if (++ps == S) ps = 0;
+    };
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      const int mb = t % p.num_m, nb = t / p.num_m;
+      for (int kb = 0; kb < num_k; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        const uint32_t a_dst = smem_u32(sA + s * CF::A_BYTES), b_dst = smem_u32(sB + s * CF::B_BYTES);
+        // weight rows (gate rows, then up rows for SwiGLU): 128 rows x 8 chunks per tile
+#pragma unroll
+        for (int tt = 0; tt < CF::A_TILES; ++tt) {
+          const int roff = tt ? p.n_up_off : 0;
+#pragma unroll
+          for (int i = 0; i < (BM * 8) / 128; ++i) {
+            const int c = pt + i * 128, row = c >> 3, c16 = c & 7;
+            const int n = nb * BM + row;
+            const bool v = n < p.N;
+            const bf16* src = Wt + (v ? (size_t)(roff + n) * p.ldw + (size_t)kb * BK + c16 * 8 : 0);
+            cp_async16(a_dst + tt * BM * BK * 2 + row * 128 + ((c16 ^ (row & 7)) << 4), src, v);
+          }
+        }
+        // token rows: BN rows x 8 chunks
+#pragma unroll
+        for (int i = 0; i < (BN * 8 + 127) / 128; ++i) {
+          const int c = pt + i * 128;
+          if (c < BN * 8) {
+            const int row = c >> 3, c16 = c & 7;
+            const int m = mb * BN + row;
+            const bool v = m < p.M;
+            const bf16* src = X + (v ? (size_t)m * p.ldx + (size_t)kb * BK + c16 * 8 : 0);
+            cp_async16(b_dst + row * 128 + ((c16 ^ (row & 7)) << 4), src, v);
+          }
+        }
+        cp_commit();
+        if (++inflight > LAG) {
+          cp_wait<LAG>();
+          publish();
+          --inflight;
+        }
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    cp_wait<0>();
+    while (inflight-- > 0) publish();
+  } else if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
+      // ---------------- TMA producer (normal tiles)
       int s = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -190,7 +272,13 @@ __global__ void __launch_bounds__(192, 1)
           mbar_expect_tx(&full[s], CF::STAGE_BYTES);
           uint8_t* a_dst = sA + s * CF::A_BYTES;
           uint8_t* b_dst = sB + s * CF::B_BYTES;
-          if constexpr (!SWAP) {
+          if constexpr (SWAP) {
+            const int j0 = nb * BM;
+            tma_load_2d(&map_w, &full[s], a_dst, kb * BK, j0);
+            if constexpr (EPI == EPI_SWIGLU)
+              tma_load_2d(&map_w, &full[s], a_dst + BM * BK * 2, kb * BK, p.n_up_off + j0);
+            tma_load_2d(&map_x, &full[s], b_dst, kb * BK, mb * BN);
+          } else {
             tma_load_2d(&map_x, &full[s], a_dst, kb * BK, mb * BM);
             if constexpr (EPI == EPI_SWIGLU) {
               const int j0 = nb * (BN / 2);
@@ -199,12 +287,6 @@ __global__ void __launch_bounds__(192, 1)
             } else {
               tma_load_2d(&map_w, &full[s], b_dst, kb * BK, nb * BN);
             }
-          } else {
-            const int j0 = nb * BM;
-            tma_load_2d(&map_w, &full[s], a_dst, kb * BK, j0);
-            if constexpr (EPI == EPI_SWIGLU)
-              tma_load_2d(&map_w, &full[s], a_dst + BM * BK * 2, kb * BK, p.n_up_off + j0);
-            tma_load_2d(&map_x, &full[s], b_dst, kb * BK, mb * BN);
           }
           if (++s == S) {
             s = 0;
@@ -414,7 +496,7 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
     p.num_n = (a.N + out_cols - 1) / out_cols;
   } else {
     if (!make_map(&mx, a.A, a.M, a.K, a.lda, BN)) return -1;
-    if (!make_map(&mw, a.B, w_rows, a.K, a.ldb, BM)) return -1;
+    if (!make_map(&mw, a.B, w_rows, a.K, a.ldb, BM / CF::NPROD)) return -1;
     p.num_m = (a.M + BN - 1) / BN;
     p.num_n = (a.N + BM - 1) / BM;
   }
@@ -425,8 +507,12 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   p.ldc = a.ldc;
   p.ldr = a.ldr;
   p.n_up_off = a.N;
-  const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
-  gemm_tc_kernel<BN, EPI, SWAP><<<grid, 192, CF::SMEM, st>>>(mx, mw, p);
+  p.X = (const bf16*)a.A;
+  p.W = (const bf16*)a.B;
+  p.ldx = a.lda;
+  p.ldw = a.ldb;
+  const int grid = p.num_tiles < CF::CTAS * num_sms ? p.num_tiles : CF::CTAS * num_sms;
+  gemm_tc_kernel<BN, EPI, SWAP><<<grid, CF::THREADS, CF::SMEM, st>>>(mx, mw, p);
   return 1;
 }
 

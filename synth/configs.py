@@ -65,7 +65,8 @@ CONFIGS = {
     "cfg1-gqa": Config("cfg1-gqa", TINY_GQA, BatchCfg(prefill=((128, 64),), decode=(256,) * 8, k=4), dtype="fp32",
                        seed=4791 + 1),
     "cfg2-mini": Config("cfg2-mini", LLAMA3_8B_LAYER,
-                        BatchCfg(prefill=((200, 37), (77, 0)), decode=(300, 17, 1029), k=3), dtype="bf16",
+                        BatchCfg(prefill=((200, 37), (77, 0), (520, 300)), decode=(300, 17, 1029), k=3),
+                        dtype="bf16",
                         seed=4791 + 2, note="Llama-3-8B layer shapes, ragged small batch (parity only)"),
     "cfg2": Config("cfg2", LLAMA3_8B_LAYER, BatchCfg(prefill=((2048, 0),), decode=(4096,) * 64, k=1,
                                                      tbt_slo_s=50e-3 / 32), dtype="bf16", seed=4791 + 2,

@@ -25,13 +25,18 @@ __global__ void __launch_bounds__(512) ldg_kernel(const uint4* __restrict__ buf,
   if (acc == 0x12345) sink[0] = acc;
 }
 
-// one CTA per SM; thread 0 issues boxes into NST stages; all boxes are "consumed" immediately
+// one CTA per SM; lane 0 of each of the blockDim/32 warps issues boxes into its own NST stages;
+// all boxes are "consumed" immediately
 template <int NST>
 __global__ void tma_kernel(const __grid_constant__ CUtensorMap map, int box_bytes, int boxes_per_stage, int rows_total,
-                           int box_rows, int cols_boxes, int total_units) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * box_bytes * boxes_per_stage);
-  if (threadIdx.x == 0) {
+                           int box_rows, int cols_boxes, int total_units_all) {
+  extern __shared__ __align__(1024) uint8_t smem_all[];
+  const int nw = blockDim.x / 32, w = threadIdx.x / 32;
+  const int ring = NST * box_bytes * boxes_per_stage;
+  uint8_t* smem = smem_all + w * ring;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_all + nw * ring) + w * NST;
+  const int total_units = total_units_all / nw;   // this warp's share: units u*nw + w
+  if ((threadIdx.x & 31) == 0) {
     for (int i = 0; i < NST; ++i)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[i])));
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -44,7 +49,8 @@ __global__ void tma_kernel(const __grid_constant__ CUtensorMap map, int box_byte
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[st])),
                    "r"(box_bytes * boxes_per_stage));
       for (int b = 0; b < boxes_per_stage; ++b) {
-        const int u = blockIdx.x + (s * boxes_per_stage + b) * gridDim.x;
+        // consecutive boxes of a stage are consecutive units (neighbouring column boxes of the same rows)
+        const int u = (((s * gridDim.x + blockIdx.x) * nw + w) * boxes_per_stage + b) % total_units_all;
         const int rb = u / cols_boxes, cb = u % cols_boxes;
         const int c0 = cb * 64, c1 = (rb * box_rows) % rows_total;
         asm volatile(
@@ -66,6 +72,24 @@ __global__ void tma_kernel(const __grid_constant__ CUtensorMap map, int box_byte
   __syncthreads();
 }
 
+// cp.async (LDGSTS 16 B) streaming: each CTA copies stages of `stage_bytes` contiguous bytes, NST groups in flight
+template <int NST>
+__global__ void cpasync_kernel(const uint8_t* __restrict__ buf, size_t bytes, int stage_bytes) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const size_t n_stages = bytes / stage_bytes;
+  int slot = 0;
+  for (size_t s = blockIdx.x; s < n_stages; s += gridDim.x) {
+    const uint8_t* src = buf + s * stage_bytes;
+    uint8_t* dst = smem + slot * stage_bytes;
+    for (int i = threadIdx.x * 16; i < stage_bytes; i += blockDim.x * 16)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst + i)), "l"(src + i) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(NST - 1) : "memory");
+    slot = (slot + 1) % NST;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 int main() {
   RK(cudaSetDevice(0));
   RK(cudaFree(0));
@@ -77,9 +101,12 @@ int main() {
   cudaEvent_t e0, e1; RK(cudaEventCreate(&e0)); RK(cudaEventCreate(&e1));
   // tensor maps over buf viewed as [rows][cols] bf16
   struct Shape { const char* name; uint64_t cols; uint32_t box_rows; int boxes_per_stage; };
-  Shape shapes[] = {{"gemm-128x128B-pitch8K", 4096, 128, 1}, {"page-16x128B-pitch256", 128, 16, 4},
-                    {"page-16x128B-pitch256 x8/stage", 128, 16, 8}};
-  for (int S : {8, 16, 32, 64, 148}) {
+  Shape shapes[] = {{"gemm-128x128B-pitch8K", 4096, 128, 1},
+                    {"gemm-128x(4x128B)-pitch8K", 4096, 128, 4},
+                    {"gemm-32x(4x128B)-pitch8K", 4096, 32, 4},
+                    {"contig-128x128B-pitch128", 64, 128, 1},
+                    {"page-16x128B-pitch256", 128, 16, 4}};
+  for (int S : {16, 148}) {
     cudaStream_t st = nullptr;
     CUgreenCtx g1 = nullptr, g2 = nullptr;
     if (S < 148) {
@@ -101,7 +128,22 @@ int main() {
       float ms; RK(cudaEventElapsedTime(&ms, e0, e1)); if (ms < best) best = ms;
     }
     printf("S=%3d  LDG stream                        %7.0f GB/s  (%5.1f GB/s/SM)\n", S, bytes / best / 1e6, bytes / best / 1e6 / S);
+    for (int threads : {256, 512}) {
+      const int stage = 8192, nst = 8;
+      RK(cudaFuncSetAttribute(cpasync_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, stage * nst));
+      best = 1e9;
+      for (int rep = 0; rep < 5; ++rep) {
+        RK(cudaEventRecord(e0, st));
+        cpasync_kernel<8><<<S * 2, threads, stage * nst, st>>>((const uint8_t*)buf, bytes, stage);
+        RK(cudaGetLastError());
+        RK(cudaEventRecord(e1, st)); RK(cudaEventSynchronize(e1));
+        float ms; RK(cudaEventElapsedTime(&ms, e0, e1)); if (ms < best) best = ms;
+      }
+      printf("S=%3d  cp.async 8 KB stages x8, 2 CTA/SM x %d thr %7.0f GB/s  (%5.1f GB/s/SM)\n", S, threads,
+             bytes / best / 1e6, bytes / best / 1e6 / S);
+    }
     for (auto& sh : shapes) {
+      for (int nw : {1, 2, 4})
       for (int nst : {4, 8}) {
         CUtensorMap map;
         const uint64_t rows = bytes / 2 / sh.cols;
@@ -116,21 +158,23 @@ int main() {
         const int cols_boxes = (int)(sh.cols / 64);
         const int rows_total = (int)rows;
         const int total_units = (int)(bytes / box_bytes);
-        const int smem = nst * box_bytes * sh.boxes_per_stage + 1024;
+        const int smem = nw * nst * box_bytes * sh.boxes_per_stage + 1024;
         if (smem > 220 * 1024) continue;
         void (*k)(CUtensorMap, int, int, int, int, int, int) = nst == 4 ? tma_kernel<4> : tma_kernel<8>;
         RK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         best = 1e9;
         for (int rep = 0; rep < 5; ++rep) {
           RK(cudaEventRecord(e0, st));
-          k<<<S, 32, smem, st>>>(map, box_bytes, sh.boxes_per_stage, rows_total, sh.box_rows, cols_boxes, total_units);
+          k<<<S, 32 * nw, smem, st>>>(map, box_bytes, sh.boxes_per_stage, rows_total, sh.box_rows, cols_boxes,
+                                      total_units);
           RK(cudaGetLastError());
           RK(cudaEventRecord(e1, st)); RK(cudaEventSynchronize(e1));
           float ms; RK(cudaEventElapsedTime(&ms, e0, e1)); if (ms < best) best = ms;
         }
-        const double moved = (double)(total_units / S / sh.boxes_per_stage) * sh.boxes_per_stage * S * box_bytes;
-        printf("S=%3d  TMA %-32s nst=%d in-flight %3d KB  %7.0f GB/s  (%5.1f GB/s/SM)\n", S, sh.name, nst,
-               nst * box_bytes * sh.boxes_per_stage / 1024, moved / best / 1e6, moved / best / 1e6 / S);
+        const double moved = (double)(total_units / nw / S / sh.boxes_per_stage) * sh.boxes_per_stage * S * nw *
+                             box_bytes;
+        printf("S=%3d  TMA %-32s warps=%d nst=%d in-flight %3d KB  %7.0f GB/s  (%5.1f GB/s/SM)\n", S, sh.name, nw,
+               nst, nw * nst * box_bytes * sh.boxes_per_stage / 1024, moved / best / 1e6, moved / best / 1e6 / S);
       }
     }
     if (g1) { CK(cuStreamDestroy((CUstream)st)); CK(cuGreenCtxDestroy(g1)); } else RK(cudaStreamDestroy(st));
