@@ -33,6 +33,15 @@ METRIC = "tokens/s per mixed iteration at TBT SLO vs SM split; % HBM/TC roofline
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+_T0 = time.time()
+
+
+def log(msg: str):
+    """Progress on stderr (the JSON line is the only stdout output)."""
+    sys.stderr.write(f"[bench {time.time() - _T0:7.1f}s] {msg}\n")
+    sys.stderr.flush()
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -141,14 +150,19 @@ class OracleSample:
         from tests.oracle_run import make_kv
         from oracle import layer as OL
         cfg = configs.get_config(cfg_name)
-        wl = workload.build(cfg, pre_seqs=[(n_pre, 0)], dec_ctx=list(cfg.batch.decode)[:n_dec], k=1)
+        # one layer of the configuration; deeper models are extrapolated per layer
+        self.layers_total = cfg.model.n_layers
+        wl = workload.build(cfg, pre_seqs=[(n_pre, 0)], dec_ctx=list(cfg.batch.decode)[:n_dec], k=1, n_layers=1)
         wl.weights = [{k_: (None if v is None else np.asarray(v, dtype=np.float64)) for k_, v in w.items()}
                       for w in wl.weights]
         self.wl, self.kv, self.OL = wl, make_kv(wl), OL
         self.mdl = OL.Model.from_cfg(wl.cfg.model)
-        self.tokens = n_pre + n_dec
-        self.desc = (f"oracle (numpy float64) on {cfg_name}: prompt rows 0..{n_pre - 1} of the 2048-token chunk "
-                     f"(exact by causality) + {n_dec} of the 64 decodes at ctx 4096, one layer")
+        # tokens per second of the whole model = tokens / (time of one layer x layers)
+        self.tokens = (n_pre + n_dec) / self.layers_total
+        n_full = sum(q for q, _ in cfg.batch.prefill)
+        self.desc = (f"oracle (numpy float64) on {cfg_name}: prompt rows 0..{n_pre - 1} of the {n_full}-token "
+                     f"chunk (exact by causality) + {n_dec} of the {len(cfg.batch.decode)} decodes, one layer"
+                     + (f", extrapolated x{self.layers_total} layers" if self.layers_total > 1 else ""))
 
     def run(self):
         wl = self.wl
@@ -233,15 +247,23 @@ def main():
     from synth import configs, workload
     from synth.gpu import inputs_gpu, kv_pools_gpu, layer_weights_gpu
 
+    if args.config == "cfg3":   # full 2k-8k ramp needs ~187 GB with weights; fall back when it does not fit
+        free, _ = torch.cuda.mem_get_info()
+        if free < 190e9:
+            args.config = "cfg3-fit"
     cfg = configs.get_config(args.config)
     dev = torch.device("cuda", torch.cuda.current_device())
     tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
     m = cfg.model
-    k_max = 32
-    wl = workload.build(cfg, k=8, with_weights=False)     # pages for up to 8 look-ahead steps
+    k_max = 8                                            # look-ahead window cap (reading #17)
+    nqkv = (m.n_q_heads + 2 * m.n_kv_heads) * m.head_dim
+    step_bytes = m.n_layers * 2 * (nqkv * m.d_model + m.d_model * m.n_q_heads * m.head_dim + 3 * m.ffn_dim * m.d_model
+                                   + sum(2 * m.n_kv_heads * m.head_dim * (c + 1) for c in cfg.batch.decode))
+    wl = workload.build(cfg, k=k_max, with_weights=False)  # pages for up to k_max look-ahead steps
+    log(f"config {args.config}: generating weights")
     W = [layer_weights_gpu(m, l, cfg.seed, dev, tdt) for l in range(m.n_layers)]
-    Kp, Vp = kv_pools_gpu(wl, dev, tdt)
     x_pre, x_dec = inputs_gpu(wl, dev, tdt)
+    torch.cuda.empty_cache()  # hand the generator's temporaries back: libduet allocates with cudaMalloc
     n_p, n_d = x_pre.shape[0], x_dec.shape[0]
     y_pre = torch.empty_like(x_pre)
     y_dec = torch.empty((8,) + tuple(x_dec.shape), dtype=tdt, device=dev)
@@ -263,6 +285,10 @@ def main():
         fl, bw = ctx.calibrate(total)
     t_cal = time.perf_counter() - t0
     hw = D.HwProfile(total, parts, fl, bw)
+    log(f"calibrated in {t_cal:.1f}s; generating the KV history")
+    Kp, Vp = kv_pools_gpu(wl, dev, tdt)   # after calibration: the pools take most of HBM at cfg3
+    log("KV ready; warm-up")
+    torch.cuda.empty_cache()
     tau = args.tau if args.tau is not None else cfg.batch.tbt_slo_s
     batch = [(q, c, 0 if c == 0 else 1, 1) for q, c in wl.pre_seqs] + [(1, c, 2, 1) for c in wl.dec_ctx]
     opts = D.DUET_OPT_FORCE_SPATIAL if args.mode == "spatial" else 0
@@ -289,10 +315,15 @@ def main():
         return s, k
 
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
+    s0 = decide()
+    log(f"split: mode={s0.mode} s_p={s0.s_p} s_d={s0.s_d} k={s0.k} flags={s0.flags} t_mixed={s0.t_mixed * 1e3:.2f} ms "
+        f"t_p={s0.t_p * 1e3:.2f} ms t_d={s0.t_d * 1e3:.2f} ms")
+    for i in range(args.warmup):
         one_step()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        log(f"warm-up step {i} done ({ctx.last_step_times()['t_window'] * 1e3:.2f} ms)")
 
+    log("timed region")
     # ------------------------------------------------ timed region
     barrier(ws)
     torch.cuda.synchronize()
@@ -329,6 +360,7 @@ def main():
         t_pred = split.t_mixed
     pred_err = abs(t_pred - side["t_window"]) / side["t_window"]
 
+    log(f"timed: {ms_per_step:.3f} ms/step; comparisons")
     # ------------------------------------------------ aggregated vs partitioned (same kernels, same batch)
     comp = {}
     if not args.profile_only:
@@ -376,6 +408,7 @@ def main():
                 rows.append({"s_d": sd, "tok_s": r[0], "window_ms": r[1] * 1e3, "tbt_ms": r[2] * 1e3})
             comp["sweep_k1"] = rows
 
+    log("e2e")
     # ------------------------------------------------ e2e through the C ABI with host buffers
     e2e = None
     if not args.profile_only:
@@ -431,6 +464,7 @@ def main():
                 "kernel": dom}
     share = {kname: v["seconds"] for kname, v in kstats.items()}
 
+    log("cpu baseline")
     # ------------------------------------------------ CPU baseline (oracle), rank 0, N=1 only
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile_only:
@@ -445,7 +479,7 @@ def main():
             "config": {"workload": f"{args.config}: {cfg.note}", "mode": ["temporal", "spatial"][split.mode],
                        "s_p": split.s_p, "s_d": split.s_d, "k": split.k, "flags": split.flags,
                        "tau_ms": tau * 1e3, "prefill_tokens": n_p, "decode_reqs": n_d,
-                       "l2": "inputs > L2 (1.5 GB of weights + KV read per step), no flush",
+                       "l2": f"inputs > L2 ({step_bytes / 1e9:.1f} GB of weights + KV read per step), no flush",
                        "parallelism": f"dp{ws} (independent replicas)", "calibration_s": round(t_cal, 2)},
             "predictor": {"t_pred_ms": t_pred * 1e3, "t_meas_ms": side["t_window"] * 1e3, "err": pred_err,
                           "t_meas_decode_ms": side["t_decode"] * 1e3, "t_meas_prefill_ms": side["t_prefill"] * 1e3},

@@ -275,11 +275,18 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
   auto gemm_by = [&](double N, double K, double Nout, bool resid) {
     return (n * K + N * K + n * Nout + (resid ? n * Nout : 0.0)) * e;
   };
-#define TIMED(cls, fl, by, call)            \
-  do {                                      \
-    const int pi_ = prof_begin(c, st);      \
-    nk += (call);                           \
-    prof_end(c, st, pi_, cls, fl, by);      \
+  // DUET_DEBUG_SYNC=1: synchronize after every launch and report it (hang / fault triage only)
+  static const bool dbg_sync = getenv("DUET_DEBUG_SYNC") != nullptr;
+#define TIMED(cls, fl, by, call)                                                                  \
+  do {                                                                                            \
+    const int pi_ = prof_begin(c, st);                                                            \
+    nk += (call);                                                                                 \
+    prof_end(c, st, pi_, cls, fl, by);                                                            \
+    if (dbg_sync && !c->capturing) {                                                              \
+      fprintf(stderr, "[duet] layer %d: %s ...", l, #call);                                       \
+      cudaError_t e_ = cudaStreamSynchronize(st);                                                 \
+      fprintf(stderr, " %s\n", cudaGetErrorString(e_));                                           \
+    }                                                                                             \
   } while (0)
   for (int l = 0; l < sp.n_layers; ++l) {
     const void* X = l == 0 ? x_in : ((l & 1) ? S.xa : S.xb);
@@ -326,6 +333,10 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       const int r = launch_prefill_attn(dt, pa, st);
       if (r < 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "prefill attention: unsupported head layout");
       prof_end(c, st, pi, DUET_KCLASS_PREFILL_ATTN, ap.attn_flops_pre, ap.attn_bytes_pre);
+      if (dbg_sync && !c->capturing) {
+        fprintf(stderr, "[duet] layer %d: prefill attention ...", l);
+        fprintf(stderr, " %s\n", cudaGetErrorString(cudaStreamSynchronize(st)));
+      }
       nk += r;
     }
     if (ap.n_dec > 0) {
@@ -909,7 +920,10 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
   if (!c || !flops || !bw) DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL argument");
   if (len < c->total_sms + 1) DUET_FAIL(DUET_ERR_CAPACITY, "tables need %d entries", c->total_sms + 1);
   for (auto& p : c->parts) DUET_TRY(ensure_partition(c, p));
-  const size_t n_bytes = (size_t)2 << 30;
+  size_t free_b = 0, total_b = 0;
+  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  size_t n_bytes = (size_t)2 << 30;  // >> L2 (126 MB)
+  while (n_bytes > ((size_t)512 << 20) && n_bytes + ((size_t)1 << 30) > free_b) n_bytes >>= 1;
   void* buf = nullptr;
   unsigned long long* sink = nullptr;
   CUDA_TRY(cudaMalloc(&buf, n_bytes));

@@ -128,6 +128,8 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
   uint32_t soff[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) soff[k] = swz(2 * k + (lane >> 4), lane & 15);
+  uint64_t l2_first;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(l2_first));
   auto issue = [&](int i) {  // page i of this warp into stage i % NST
     const int st = i % NST;
     uint8_t* dk = wsm + st * STAGE_BYTES;
@@ -148,13 +150,15 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
       const bf16* vs = reinterpret_cast<const bf16*>(a.v_pool) + base;
       const uint32_t sk = smem_u32(dk), sv = smem_u32(dv);
       const int rows_valid = len - pg * PAGE;  // >= 16 except on the last page
+      // KV is read once per step: evict-first in L2, so the stream does not push out the working set
+      // of a concurrently running prefill partition (GEMM operands, the chunk's own K/V)
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int sz = (2 * k + (lane >> 4)) < rows_valid ? 16 : 0;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sk + soff[k]), "l"(ks + k * 256),
-                     "r"(sz) : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sv + soff[k]), "l"(vs + k * 256),
-                     "r"(sz) : "memory");
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(sk + soff[k]),
+                     "l"(ks + k * 256), "r"(sz), "l"(l2_first) : "memory");
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(sv + soff[k]),
+                     "l"(vs + k * 256), "r"(sz), "l"(l2_first) : "memory");
       }
     }
   };

@@ -103,9 +103,56 @@ __global__ void rope_kv_kernel(RopeKvArgs a) {
   }
 }
 
+// bf16, vectorized: one work item = 8 consecutive rotation pairs of one q/k head (two 16-B loads, a
+// 64-B cos/sin load, two 16-B stores) or 8 elements of one v head (one 16-B copy).
+__global__ void __launch_bounds__(256) rope_kv_vec_kernel(RopeKvArgs a) {
+  const int row = blockIdx.x;
+  const int half = a.dh / 2, hv = half / 8, vv = a.dh / 8;
+  bf16* qkv = reinterpret_cast<bf16*>(a.qkv) + (size_t)row * (a.hq + 2 * a.hkv) * a.dh;
+  const int p = a.pos[row];
+  const int page = a.table[(size_t)a.tok_row[row] * a.max_pages + p / a.page_size];
+  const int slot = p % a.page_size;
+  const float2* rp = a.rope + (size_t)p * half;
+  bf16* kp = reinterpret_cast<bf16*>(a.k_pool);
+  bf16* vp = reinterpret_cast<bf16*>(a.v_pool);
+  const int n_rot = (a.hq + a.hkv) * hv;
+  const int n_all = n_rot + a.hkv * vv;
+  for (int t = threadIdx.x; t < n_all; t += blockDim.x) {
+    if (t < n_rot) {
+      const int head = t / hv, i0 = (t % hv) * 8;
+      bf16* x0p = qkv + head * a.dh + i0;
+      float x0[8], x1[8];
+      load16<bf16>(x0p, x0);
+      load16<bf16>(x0p + half, x1);
+      float y0[8], y1[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float2 cs = rp[i0 + e];
+        y0[e] = x0[e] * cs.x - x1[e] * cs.y;
+        y1[e] = x1[e] * cs.x + x0[e] * cs.y;
+      }
+      if (head < a.hq) {
+        store16<bf16>(x0p, y0);
+        store16<bf16>(x0p + half, y1);
+      } else {
+        bf16* dst = kp + (((size_t)page * a.hkv + (head - a.hq)) * a.page_size + slot) * a.dh + i0;
+        store16<bf16>(dst, y0);
+        store16<bf16>(dst + half, y1);
+      }
+    } else {
+      const int u = t - n_rot;
+      const int vh = u / vv, e0 = (u % vv) * 8;
+      const uint4 val = *reinterpret_cast<const uint4*>(qkv + (a.hq + a.hkv + vh) * a.dh + e0);
+      *reinterpret_cast<uint4*>(vp + (((size_t)page * a.hkv + vh) * a.page_size + slot) * a.dh + e0) = val;
+    }
+  }
+}
+
 int launch_rope_kv(DT dt, const RopeKvArgs& a, cudaStream_t st) {
   if (a.n <= 0) return 0;
-  if (dt == DT::BF16)
+  if (dt == DT::BF16 && !a.bias && a.dh % 16 == 0)
+    rope_kv_vec_kernel<<<a.n, 256, 0, st>>>(a);
+  else if (dt == DT::BF16)
     rope_kv_kernel<bf16><<<a.n, 256, 0, st>>>(a);
   else
     rope_kv_kernel<float><<<a.n, 256, 0, st>>>(a);

@@ -1,18 +1,19 @@
-// Causal prefill attention over the paged KV cache on 5th-generation tensor cores (tcgen05/TMEM/TMA).
+// Causal prefill attention over the paged KV cache on 5th-generation tensor cores (tcgen05 / TMEM).
 //
 // Chunked prefill (§4.1; readings #2, #6, #7): a chunk of q tokens at positions
 // c..c+q-1 attends to its c-token prefix and to itself causally.  One CTA = 128 query rows of one
-// query head; 128-key tiles (8 pages of 16 tokens, fetched page by page with TMA straight from the
-// paged pool) double-buffered in shared memory.
-//   warp 0      TMA producer: Q once (2 x 64-column boxes), K and V tiles (16-row boxes per page)
-//   warp 1      TMEM allocator + tcgen05.mma issuer:  S_j = Q K_j^T  (UMMA 128x128x16, K-major operands)
-//               into one of two TMEM S buffers, then O += P_{j-1} V_{j-1} (A = P from smem, B = V
-//               MN-major), so the MMAs of S_{j+1} overlap the softmax of tile j
-//   warps 2..5  softmax, one thread per query row (= TMEM lane): row max / exp2 / row sum entirely in
-//               registers (no shuffles), P written to smem in the UMMA SW128 layout; the running max
-//               is re-based (O rescaled in TMEM) only when it grows by more than 2^8, so P <= 256
-// Keys past the causal end are masked; the unwritten slots of the sequence's last page are zeroed in
-// the V tile before the P.V MMA (unwritten page slots may hold anything).
+// query head; the keys stream in 64-key tiles (4 pages of 16 tokens).
+//   warp 0      Q tile by TMA (two 64-column SWIZZLE_128B boxes)
+//   warp 1      TMEM allocator + tcgen05.mma issuer: S_j = Q K_j^T (UMMA 128x64x16, both operands
+//               K-major) into one of two TMEM S buffers, then O += P_{j-1} V_{j-1} (A = P from smem,
+//               B = V MN-major) — the MMAs of S_{j+1} overlap the softmax of tile j
+//   warps 2..5  softmax, one thread per query row (= TMEM lane): max / exp2 / sum in registers, P
+//               written to one of two smem buffers in the UMMA SW128 layout; the running max is re-based
+//               (O rescaled in TMEM) only when it grows by more than 2^8, so P <= 256
+//   warps 6..9  K/V loaders: cp.async gathers of the scattered 4 KiB page blocks into a 4-stage ring
+//               (a TMA box costs its issuing thread ~0.25 us on B200 — profiles/r01_probe_tma_bw.txt —
+//               and a page needs four), published LAG = 2 tiles behind the issue front
+// Keys past the causal end of the tile are zero-filled (cp.async src-size 0) and masked.
 #include <cuda.h>
 
 #include "dev_common.cuh"
@@ -21,11 +22,19 @@
 namespace duet {
 namespace fatc {
 
-constexpr int BQ = 128, BKV = 128, DH = 128, PAGE = 16;
-constexpr int SUB = 128 * 64 * 2;  // [128 rows][64 cols] bf16 SW128 sub-tile = 16 KiB
-constexpr int TILE = 2 * SUB;      // [128][128] = 32 KiB
-constexpr int OFF_Q = 0, OFF_K = TILE, OFF_V = 3 * TILE, OFF_P = 5 * TILE, OFF_BAR = 6 * TILE;
-constexpr int SMEM = 6 * TILE + 256 + 1024;
+constexpr int BQ = 128, BKV = 64, DH = 128, PAGE = 16, KV_STAGES = 4, LAG = 2;
+constexpr int Q_SUB = BQ * 128;            // [128 rows][64 cols] SW128 sub-tile = 16 KiB
+constexpr int KV_SUB = BKV * 128;          // [64 rows][64 cols] = 8 KiB
+constexpr int Q_BYTES = 2 * Q_SUB;         // 32 KiB
+constexpr int KV_BYTES = 2 * KV_SUB;       // 16 KiB per tensor per stage
+constexpr int P_BYTES = BQ * BKV * 2;      // [128 rows][64 keys] = one SW128 sub-tile, 16 KiB
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = OFF_Q + Q_BYTES;
+constexpr int OFF_V = OFF_K + KV_STAGES * KV_BYTES;
+constexpr int OFF_P = OFF_V + KV_STAGES * KV_BYTES;
+constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+constexpr int TMEM_COLS = 256;             // S0 (64) | S1 (64) | O (128)
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -61,14 +70,14 @@ __device__ __forceinline__ uint64_t desc_k(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) |
          ((uint64_t)2 << 61);
 }
-// MN-major SW128 descriptor: 64-element (128 B) MN blocks LBO = 16 KiB apart, 8-row K groups SBO = 1 KiB
+// MN-major SW128 descriptor: 64-element MN blocks LBO = KV_SUB apart, 8-row K groups SBO = 1 KiB
 __device__ __forceinline__ uint64_t desc_mn(uint32_t saddr) {
-  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(SUB >> 4) << 16) | ((uint64_t)64 << 32) |
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(KV_SUB >> 4) << 16) | ((uint64_t)64 << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-// kind::f16, D f32, A = B = bf16, M = 128, N = 128; b_mn selects an MN-major B operand (bit 16)
-__host__ __device__ constexpr uint32_t idesc(bool b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(128 >> 3) << 17) |
+// kind::f16, D f32, A = B = bf16, M = 128, N; b_mn selects an MN-major B operand (bit 16)
+__host__ __device__ constexpr uint32_t idesc(int n, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(n >> 3) << 17) |
          ((uint32_t)(128 >> 4) << 24);
 }
 __device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
@@ -87,6 +96,12 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// 2^x on the SFU without the denormal range fix-up exp2f adds (arguments are <= 8 here; underflow -> 0)
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -127,14 +142,14 @@ __global__ void __launch_bounds__(320, 1) fa_tc_kernel(const __grid_constant__ C
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bar = (uint64_t*)(smem + OFF_BAR);
-  uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;    // [2]
-  uint64_t* s_free = bar + 7;    // [2]
-  uint64_t* p_full = bar + 9;
-  uint64_t* pv_done = bar + 10;
-  uint32_t* tmem_slot = (uint32_t*)(bar + 12);
+  uint64_t* q_full = bar;                   // 1
+  uint64_t* kv_full = bar + 1;              // [KV_STAGES]
+  uint64_t* kv_empty = kv_full + KV_STAGES; // [KV_STAGES]
+  uint64_t* s_full = kv_empty + KV_STAGES;  // [2]
+  uint64_t* s_free = s_full + 2;            // [2]
+  uint64_t* p_full = s_free + 2;            // [2]
+  uint64_t* pv_done = p_full + 2;           // [2]  PV of the tile that used P buffer b
+  uint32_t* tmem_slot = (uint32_t*)(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = p.n_qtiles - 1 - blockIdx.x;  // heavy (late) tiles first
@@ -148,117 +163,116 @@ __global__ void __launch_bounds__(320, 1) fa_tc_kernel(const __grid_constant__ C
   const int q_last = min(q0 + BQ, qlen) - 1;
   const int kv_end = cpre + q_last + 1;
   const int n_kt = (kv_end + BKV - 1) / BKV;
-  const int n_pages_total = (kv_end + PAGE - 1) / PAGE;
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < KV_STAGES; ++i) {
       mbar_init(&kv_full[i], 4);  // one arrive per loader warp
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[i], 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(pv_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_before();
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t T_S[2] = {tmem, tmem + 128};
-  const uint32_t T_O = tmem + 256;
+  const uint32_t T_S0 = tmem, T_S1 = tmem + BKV, T_O = tmem + 2 * BKV;
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ Q tile (TMA, two 64-column boxes)
-      mbar_expect_tx(q_full, TILE);
+      mbar_expect_tx(q_full, Q_BYTES);
       tma_load_2d(&map_q, q_full, smem + OFF_Q, head * DH, row0 + q0);
-      tma_load_2d(&map_q, q_full, smem + OFF_Q + SUB, head * DH + 64, row0 + q0);
+      tma_load_2d(&map_q, q_full, smem + OFF_Q + Q_SUB, head * DH + 64, row0 + q0);
     }
   } else if (warp >= 6) {
-    // ------------------------------------------------ K/V loaders: 4 warps of cp.async (16 B per lane)
-    // A 128-key tile is 8 scattered 4 KiB page blocks per tensor; issuing them as TMA boxes costs one
-    // serialized instruction per 2 KiB box, so the gather is spread over 128 threads instead.  Keys past
-    // the causal end are zero-filled (cp.async src-size 0): unwritten page slots may hold anything.
+    // ------------------------------------------------ K/V loaders (4 warps, cp.async, 4-stage ring)
     const int lt = threadIdx.x - 6 * 32;  // 0..127
-    const bf16* Kg = p.k_pool;
-    const bf16* Vg = p.v_pool;
     const size_t page_stride = (size_t)p.hkv * PAGE * DH;
+    // chunk c = lt + 128 i (i < 8) of a [64 keys][16 chunks] tile: key = c / 16, 16-B column = c % 16
     auto issue = [&](int j) {
-      const int s = j & 1;
-      const uint32_t kd = smem_u32(smem + OFF_K + s * TILE), vd = smem_u32(smem + OFF_V + s * TILE);
-#pragma unroll 4
-      for (int i = 0; i < (BKV * 16) / 128; ++i) {  // 2048 16-B chunks per tensor
+      const int st = j % KV_STAGES;
+      const uint32_t kd = smem_u32(smem + OFF_K + st * KV_BYTES), vd = smem_u32(smem + OFF_V + st * KV_BYTES);
+#pragma unroll
+      for (int i = 0; i < (BKV * 16) / 128; ++i) {
         const int c = lt + i * 128;
         const int rr = c >> 4, ch = c & 15;
         const int key = j * BKV + rr;
         const bool v = key < kv_end;
-        const size_t off = v ? (size_t)tab[key / PAGE] * page_stride + ((size_t)kvh * PAGE + (key % PAGE)) * DH + ch * 8
-                             : 0;
-        const uint32_t so = (uint32_t)((ch >> 3) * SUB + rr * 128 + (((ch & 7) ^ (rr & 7)) << 4));
+        const size_t off =
+            v ? (size_t)tab[key / PAGE] * page_stride + ((size_t)kvh * PAGE + (key % PAGE)) * DH + ch * 8 : 0;
+        const uint32_t so = (uint32_t)((ch >> 3) * KV_SUB + rr * 128 + (((ch & 7) ^ (rr & 7)) << 4));
         const int sz = v ? 16 : 0;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(kd + so), "l"(Kg + off), "r"(sz)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(kd + so), "l"(p.k_pool + off), "r"(sz)
                      : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(vd + so), "l"(Vg + off), "r"(sz)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(vd + so), "l"(p.v_pool + off), "r"(sz)
                      : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    auto publish = [&](int j) {  // tile j's copies (this thread's) have landed -> visible to the async proxy
+    int pub = 0;
+    auto publish = [&]() {  // the oldest unpublished tile has landed -> visible to the async proxy
       fence_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&kv_full[j & 1]);
+      if (lane == 0) mbar_arrive(&kv_full[pub % KV_STAGES]);
+      ++pub;
     };
-    // tile j is published as soon as it lands: the MMA issuer needs K_{j} before it can retire
-    // P_{j-1} V_{j-1}, which is what frees the buffer tile j+1 goes to (no publish may wait on a free)
+    // LAG <= KV_STAGES - 2: tile j - KV_STAGES (whose consumption frees slot j) is always published first
     for (int j = 0; j < n_kt; ++j) {
-      mbar_wait(&kv_empty[j & 1], ((j >> 1) & 1) ^ 1);
+      mbar_wait(&kv_empty[j % KV_STAGES], ((j / KV_STAGES) & 1) ^ 1);
       issue(j);
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      publish(j);
+      if (j >= LAG) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(LAG) : "memory");
+        publish();
+      }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    while (pub < n_kt) publish();
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (lane 0 issues; the warp zeroes V tails)
-    constexpr uint32_t ID_S = idesc(false), ID_PV = idesc(true);
+    // ------------------------------------------------ MMA issuer
+    constexpr uint32_t ID_S = idesc(BKV, false), ID_PV = idesc(DH, true);
     const uint32_t sq = smem_u32(smem + OFF_Q);
     mbar_wait(q_full, 0);
     for (int j = 0; j <= n_kt; ++j) {
       if (j < n_kt) {
-        const int s = j & 1;
-        if (j >= 2) mbar_wait(&s_free[s], ((j - 2) >> 1) & 1);
-        mbar_wait(&kv_full[s], (j >> 1) & 1);
+        const int b = j & 1, st = j % KV_STAGES;
+        if (j >= 2) mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);
+        mbar_wait(&kv_full[st], (j / KV_STAGES) & 1);
         tc_after();
         if (lane == 0) {
-          const uint32_t sk = smem_u32(smem + OFF_K + s * TILE);
+          const uint32_t sk = smem_u32(smem + OFF_K + st * KV_BYTES);
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
-            umma(T_S[s], desc_k(sq + off), desc_k(sk + off), ID_S, kk > 0);
+            umma(b ? T_S1 : T_S0, desc_k(sq + (kk >> 2) * Q_SUB + (kk & 3) * 32),
+                 desc_k(sk + (kk >> 2) * KV_SUB + (kk & 3) * 32), ID_S, kk > 0);
           }
-          umma_commit(&s_full[s]);
+          umma_commit(&s_full[b]);
         }
         __syncwarp();
       }
       if (j >= 1) {
-        const int jp = j - 1, sp = jp & 1;
-        const int pg0 = jp * (BKV / PAGE);
-        const int n_pg = min(BKV / PAGE, n_pages_total - pg0);
-        uint8_t* vt = smem + OFF_V + sp * TILE;  // keys >= kv_end were zero-filled by the loaders
-        mbar_wait(p_full, jp & 1);
+        const int jp = j - 1, b = jp & 1, st = jp % KV_STAGES;
+        mbar_wait(&p_full[b], (jp >> 1) & 1);
         tc_after();
         if (lane == 0) {
-          const uint32_t spp = smem_u32(smem + OFF_P), sv = smem_u32(vt);
-          for (int kk = 0; kk < n_pg; ++kk) {  // 16 keys (one page) per UMMA k-step
-            const uint32_t aoff = (kk >> 2) * SUB + (kk & 3) * 32;
-            umma(T_O, desc_k(spp + aoff), desc_mn(sv + kk * PAGE * 128), ID_PV, (jp > 0 || kk > 0));
-          }
-          umma_commit(&kv_empty[sp]);
-          umma_commit(pv_done);
+          const uint32_t spp = smem_u32(smem + OFF_P + b * P_BYTES);
+          const uint32_t sv = smem_u32(smem + OFF_V + st * KV_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)  // 16 keys per UMMA k-step
+            umma(T_O, desc_k(spp + kk * 32), desc_mn(sv + kk * 16 * 128), ID_PV, (jp > 0 || kk > 0));
+          umma_commit(&kv_empty[st]);
+          umma_commit(&pv_done[b]);
         }
         __syncwarp();
       }
@@ -266,38 +280,46 @@ __global__ void __launch_bounds__(320, 1) fa_tc_kernel(const __grid_constant__ C
   } else {
     // ------------------------------------------------ softmax warps: one thread per query row
     const int quad = warp & 3;
-    const int r = quad * 32 + lane;                              // row in tile = TMEM lane
-    const int pos = min(cpre + q0 + r, kv_end - 1);              // clamp rows past the chunk
+    const int r = quad * 32 + lane;                          // row in tile = TMEM lane
+    const int pos = min(cpre + q0 + r, kv_end - 1);          // clamp rows past the chunk
     const float sc = rsqrtf((float)DH) * 1.4426950408889634f;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    uint8_t* prow = smem + OFF_P + r * 128;
     const uint32_t sw = (uint32_t)(r & 7);
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kt; ++j) {
-      const int s = j & 1;
-      mbar_wait(&s_full[s], (j >> 1) & 1);
+      const int b = j & 1;
+      const uint32_t T_S = b ? T_S1 : T_S0;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_after();
       const int kbase = j * BKV;
-      // pass 1: row max over visible keys
+      uint32_t v0[32], v1[32];
+      tmem_ld32(T_S + lane_base, v0);
+      tmem_ld32(T_S + lane_base + 32, v1);
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[b]);  // S buffer b may be overwritten by S_{j+2}
+      const int lim = pos - kbase;  // keys 0..lim of this tile are visible to this row
       float mx = -INFINITY;
+      if (lim >= BKV - 1) {
 #pragma unroll
-      for (int c = 0; c < BKV; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(T_S[s] + lane_base + c, v);
+        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, fmaxf(__uint_as_float(v0[e]), __uint_as_float(v1[e])));
+      } else {
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (kbase + c + e <= pos) mx = fmaxf(mx, __uint_as_float(v[e]) * sc);
+        for (int e = 0; e < 32; ++e) {
+          if (e <= lim) mx = fmaxf(mx, __uint_as_float(v0[e]));
+          if (32 + e <= lim) mx = fmaxf(mx, __uint_as_float(v1[e]));
+        }
       }
-      const float m_new = fmaxf(m_used, mx);
-      const bool rescale = m_new > m_used + RESCALE_THRESHOLD;
-      // P buffer and O are free once PV(j-1) has completed
-      if (j >= 1) {
-        mbar_wait(pv_done, (j - 1) & 1);
-        tc_after();
-      }
-      if (rescale) {
+      const float m_new = fmaxf(m_used, mx * sc);  // sc > 0: the max commutes with the scaling
+      // Re-base the rows whose max grew by more than 2^8.  tcgen05.ld/st are warp-collective
+      // (.sync.aligned), so the decision is made per warp and rows that keep their max scale by 1.
+      const bool mine = m_new > m_used + RESCALE_THRESHOLD;
+      if (__any_sync(0xffffffffu, mine)) {
         if (j >= 1) {
-          const float f = exp2f(m_used - m_new);
+          // O must be quiescent: wait for PV_{j-1} (all earlier ones completed before it)
+          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          tc_after();
+          const float f = mine ? exp2f(m_used - m_new) : 1.f;
           l *= f;
 #pragma unroll 1
           for (int c = 0; c < DH; c += 32) {
@@ -308,41 +330,41 @@ __global__ void __launch_bounds__(320, 1) fa_tc_kernel(const __grid_constant__ C
             tmem_st32(T_O + lane_base + c, v);
           }
         }
-        m_used = m_new;
+        if (mine) m_used = m_new;
       }
-      // pass 2: P = exp2(s - m_used) (masked -> 0), row sum, P row -> smem (SW128, K-major)
+      // P buffer b is free once PV_{j-2} has completed
+      if (j >= 2) {
+        mbar_wait(&pv_done[b], ((j - 2) >> 1) & 1);
+        tc_after();
+      }
+      uint8_t* prow = smem + OFF_P + b * P_BYTES + r * 128;
 #pragma unroll
-      for (int c = 0; c < BKV; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(T_S[s] + lane_base + c, v);
+      for (int h = 0; h < 2; ++h) {
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const float p0 = (kbase + c + e <= pos) ? exp2f(__uint_as_float(v[e]) * sc - m_used) : 0.f;
-          const float p1 = (kbase + c + e + 1 <= pos) ? exp2f(__uint_as_float(v[e + 1]) * sc - m_used) : 0.f;
+          const float s0 = __uint_as_float(h ? v1[e] : v0[e]), s1 = __uint_as_float(h ? v1[e + 1] : v0[e + 1]);
+          const int k0 = h * 32 + e;
+          const float p0 = (k0 <= lim) ? fast_exp2(fmaf(s0, sc, -m_used)) : 0.f;
+          const float p1 = (k0 + 1 <= lim) ? fast_exp2(fmaf(s1, sc, -m_used)) : 0.f;
           l += p0 + p1;
-          __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-          pk[e / 2] = *reinterpret_cast<uint32_t*>(&h);
+          __nv_bfloat162 hh = __floats2bfloat162_rn(p0, p1);
+          pk[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
         }
-        // keys c..c+31 = 4 chunks of 8 keys in sub-tile c / 64
-        uint8_t* sub = prow + (c >> 6) * SUB;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          const uint32_t chunk = (uint32_t)(((c & 63) >> 3) + q4);
-          *reinterpret_cast<uint4*>(sub + ((chunk ^ sw) << 4)) =
+          const uint32_t chunk = (uint32_t)(h * 4 + q4);
+          *reinterpret_cast<uint4*>(prow + ((chunk ^ sw) << 4)) =
               make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
         }
       }
-      tc_before();
       fence_async_smem();
+      tc_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_free[s]);
-        mbar_arrive(p_full);
-      }
+      if (lane == 0) mbar_arrive(&p_full[b]);
     }
     // epilogue: O / l -> bf16 -> global
-    mbar_wait(pv_done, (n_kt - 1) & 1);
+    mbar_wait(&pv_done[(n_kt - 1) & 1], ((n_kt - 1) >> 1) & 1);
     tc_after();
     const bool row_ok = q0 + r < qlen;
     const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -366,7 +388,7 @@ __global__ void __launch_bounds__(320, 1) fa_tc_kernel(const __grid_constant__ C
   __syncthreads();
   if (warp == 1) {
     tc_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
   }
 }
 
@@ -400,8 +422,8 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t c
 }  // namespace fatc
 
 bool fa_tc_supported(const PrefillAttnArgs& a) {
-  return a.dh == fatc::DH && a.page_size == fatc::PAGE && a.n_pages > 0 && a.q_stride % 8 == 0 &&
-         fatc::encode_fn() != nullptr && a.total_rows > 0;
+  return a.dh == fatc::DH && a.page_size == fatc::PAGE && a.q_stride % 8 == 0 && fatc::encode_fn() != nullptr &&
+         a.total_rows > 0;
 }
 
 int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {

@@ -121,6 +121,21 @@ def test_parity_llama_shapes_ragged_prefix():
     _check_outputs(g, y_pre1, y_dec1, TOL["bf16"])
 
 
+def test_parity_large_activations_running_max_rebase():
+    """Inputs scaled x16 (still exact in bf16): attention scores grow along the sequence, so rows re-base
+    their running max at different key tiles (warp-divergent rescale decisions in the flash kernel)."""
+    cfg = configs.get_config("cfg2-mini")
+    wl = workload.build(cfg, k=1)
+    wl.x_pre = (wl.x_pre * 16).astype(np.float32)
+    wl.x_dec = (wl.x_dec * 16).astype(np.float32)
+    y_pre, y_dec, _ = run(wl)
+    ctx = make_ctx(wl, "bf16")
+    g = GpuWorkload(wl, "bf16")
+    g.step(ctx, D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1))
+    torch.cuda.synchronize()
+    _check_outputs(g, y_pre, y_dec, TOL["bf16"])
+
+
 def test_fine_grained_partitions_and_no_graph():
     cfg = configs.get_config("cfg1")
     wl = workload.build(cfg, k=3)
