@@ -103,6 +103,8 @@ struct Side {
   int* meta = nullptr;  // [pos | tok_row | row0 | qlen | cpre | seq_row | step | table]
   float *part_o = nullptr, *part_ml = nullptr;
   int part_rows = 0;
+  float* gemm_ws = nullptr;  // split-K partials of the weight-streaming GEMMs (kernels.h GemmArgs)
+  size_t gemm_ws_floats = 0;
   // offsets into meta (ints)
   size_t o_pos = 0, o_tok = 0, o_row0 = 0, o_qlen = 0, o_cpre = 0, o_seqrow = 0, o_step = 0, o_table = 0, n_meta = 0;
   int* pos() const { return meta + o_pos; }
@@ -199,6 +201,13 @@ static duet_status side_alloc(duet_ctx* c, Side& s, int cap_rows, int cap_seqs, 
   s.part_rows = std::max(part_rows, 1);
   CUDA_TRY(cudaMalloc(&s.part_o, (size_t)s.part_rows * sp.n_q_heads * kMaxSplits * sp.head_dim * sizeof(float)));
   CUDA_TRY(cudaMalloc(&s.part_ml, (size_t)s.part_rows * sp.n_q_heads * kMaxSplits * 2 * sizeof(float)));
+  // split-K workspace: the largest need over the layer's four GEMMs at any M <= min(cap_rows, 128)
+  for (int M : {std::min(cap_rows, 64), std::min(cap_rows, 128)}) {
+    const int shapes[4][3] = {{(int)nqkv, (int)d, EPI_STORE}, {(int)d, (int)nq, EPI_RESIDUAL},
+                              {(int)m, (int)d, EPI_SWIGLU}, {(int)d, (int)m, EPI_RESIDUAL}};
+    for (auto& sh : shapes) s.gemm_ws_floats = std::max(s.gemm_ws_floats, gemm_tc_splitk_need(M, sh[0], sh[1], sh[2]));
+  }
+  if (s.gemm_ws_floats > 0) CUDA_TRY(cudaMalloc(&s.gemm_ws, s.gemm_ws_floats * sizeof(float)));
   size_t off = 0;
   s.o_pos = off; off += R;
   s.o_tok = off; off += R;
@@ -215,7 +224,7 @@ static duet_status side_alloc(duet_ctx* c, Side& s, int cap_rows, int cap_seqs, 
 }
 
 static void side_free(Side& s) {
-  void* ptrs[] = {s.xa, s.xb, s.h, s.x1, s.h2, s.xin, s.ylast, s.qkv, s.o, s.act, s.part_o, s.part_ml, s.meta};
+  void* ptrs[] = {s.xa, s.xb, s.h, s.x1, s.h2, s.xin, s.ylast, s.qkv, s.o, s.act, s.part_o, s.part_ml, s.meta, s.gemm_ws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   s = Side{};
@@ -275,6 +284,10 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
   auto gemm_by = [&](double N, double K, double Nout, bool resid) {
     return (n * K + N * K + n * Nout + (resid ? n * Nout : 0.0)) * e;
   };
+  auto with_ws = [&](GemmArgs& g) {
+    g.ws = S.gemm_ws;
+    g.ws_floats = S.gemm_ws_floats;
+  };
   // DUET_DEBUG_SYNC=1: synchronize after every launch and report it (hang / fault triage only)
   static const bool dbg_sync = getenv("DUET_DEBUG_SYNC") != nullptr;
 #define TIMED(cls, fl, by, call)                                                                  \
@@ -296,6 +309,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e, launch_rmsnorm(dt, X, W.g_norm1, S.h, n_rows, d, eps, st));
     // 2. qkv = h W_qkv^T (+ b)
     GemmArgs g{S.h, W.w_qkv, S.qkv, nullptr, W.b_qkv, n_rows, nqkv, d, d, d, nqkv, 0, EPI_STORE};
+    with_ws(g);
     TIMED(DUET_KCLASS_GEMM, gemm_fl(nqkv, d), gemm_by(nqkv, d, nqkv, false), launch_gemm(dt, g, num_sms, st));
     // 3. RoPE + paged KV append (before attention)
     RopeKvArgs ra{S.qkv, nullptr, n_rows, hq, hkv, dh, S.pos(), S.tok(), S.table(), S.pitch, kPageSize,
@@ -369,14 +383,17 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     }
     // 5. x1 = x + o W_o^T
     GemmArgs go{S.o, W.w_o, S.x1, X, nullptr, n_rows, d, hq * dh, hq * dh, hq * dh, d, d, EPI_RESIDUAL};
+    with_ws(go);
     TIMED(DUET_KCLASS_GEMM, gemm_fl(d, hq * dh), gemm_by(d, hq * dh, d, true), launch_gemm(dt, go, num_sms, st));
     // 6. h2 = RMSNorm(x1) g2
     TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e, launch_rmsnorm(dt, S.x1, W.g_norm2, S.h2, n_rows, d, eps, st));
     // 7. act = silu(h2 W_g^T) * (h2 W_u^T)
     GemmArgs gg{S.h2, W.w_gate_up, S.act, nullptr, nullptr, n_rows, m, d, d, d, m, 0, EPI_SWIGLU};
+    with_ws(gg);
     TIMED(DUET_KCLASS_GEMM, gemm_fl(2.0 * m, d), gemm_by(2.0 * m, d, m, false), launch_gemm(dt, gg, num_sms, st));
     // 8. y = x1 + act W_d^T
     GemmArgs gd{S.act, W.w_down, Y, S.x1, nullptr, n_rows, d, m, m, m, d, d, EPI_RESIDUAL};
+    with_ws(gd);
     TIMED(DUET_KCLASS_GEMM, gemm_fl(d, m), gemm_by(d, m, d, true), launch_gemm(dt, gd, num_sms, st));
   }
 #undef TIMED
@@ -900,6 +917,8 @@ extern "C" duet_status duet_op_gemm(duet_ctx* c, const void* A, const void* B, v
   if (epi < 0 || epi > 2) DUET_FAIL(DUET_ERR_INVALID_ARG, "epi = %d", epi);
   if (epi == DUET_EPI_RESIDUAL && !R) DUET_FAIL(DUET_ERR_INVALID_ARG, "residual epilogue needs R");
   GemmArgs g{A, B, C, R, bias, M, N, K, K, K, N, N, epi};
+  g.ws = c->pre.gemm_ws;  // op calls are stream-ordered by the caller, never concurrent with a step
+  g.ws_floats = c->pre.gemm_ws_floats;
   launch_gemm(c->dt, g, c->total_sms, (cudaStream_t)stream);
   DUET_TRY(check_launch("gemm"));
   return DUET_OK;

@@ -27,7 +27,13 @@ struct GemmArgs {
   int M, N, K;
   int lda, ldb, ldc, ldr;
   int epi;
+  // split-K workspace (fp32 partials) for weight-streaming (swap-AB) launches; nullptr -> no split-K.
+  // A split launch is two kernels (GEMM writing partials, then an ordered reduction + epilogue).
+  float* ws = nullptr;
+  size_t ws_floats = 0;
 };
+// fp32 partial floats a split-K launch of this shape needs (0 when it runs unsplit)
+size_t gemm_tc_splitk_need(int M, int N, int K, int epi);
 
 // num_sms: SMs of the partition the launch runs in (persistent grid sizing).
 // Returns the number of kernels launched (0 on a launch error, checked by the caller).

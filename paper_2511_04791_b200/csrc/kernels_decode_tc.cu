@@ -81,6 +81,12 @@ __device__ __forceinline__ uint32_t movtrans(uint32_t a) {
   asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
   return d;
 }
+// 2^x on the SFU without exp2f's denormal fix-up (arguments <= 0 here; -inf -> +0)
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -130,12 +136,27 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
   for (int k = 0; k < 8; ++k) soff[k] = swz(2 * k + (lane >> 4), lane & 15);
   uint64_t l2_first;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(l2_first));
-  auto issue = [&](int i) {  // page i of this warp into stage i % NST
+  // Page-table entries of this warp's pages, 32 at a time: lane L holds the entry of page slot
+  // i = 32 b + L (prefetched one batch ahead), read with a shuffle when page i is issued, so no
+  // cp.async waits on a dependent global load.
+  auto tab_batch = [&](int b) {
+    const int i = b * 32 + lane;
+    return i < n_mine ? __ldg(tab + first + i * WARPS) : 0;
+  };
+  int pt_cur = tab_batch(0), pt_next = tab_batch(1);
+  auto page_of = [&](int i) {  // warp-uniform i, all lanes participate
+    if ((i & 31) == 0 && i > 0) {
+      pt_cur = pt_next;
+      pt_next = tab_batch((i >> 5) + 1);
+    }
+    return __shfl_sync(0xffffffffu, pt_cur, i & 31);
+  };
+  auto issue = [&](int i, int pid) {  // page i of this warp (pool page pid) into stage i % NST
     const int st = i % NST;
     uint8_t* dk = wsm + st * STAGE_BYTES;
     uint8_t* dv = dk + PAGE_BYTES;
     if constexpr (TMA) {  // lane 0 only
-      const int prow = (tab[first + i * WARPS] * a.hkv + kvh) * PAGE;
+      const int prow = (pid * a.hkv + kvh) * PAGE;
       mbar_expect_tx(&full[st], STAGE_BYTES);
       tma_load_2d(&map_k, &full[st], dk, 0, prow);
       tma_load_2d(&map_k, &full[st], dk + HALF, 64, prow);
@@ -145,7 +166,7 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
       // chunk k*32 + lane of the 4 KiB page block is row 2k + lane/16, 16-B column lane%16: its global
       // offset is (k*32 + lane) * 8 elements and its swizzled smem offset soff[k] (precomputed)
       const int pg = first + i * WARPS;
-      const size_t base = ((size_t)tab[pg] * a.hkv + kvh) * PAGE * DH + lane * 8;
+      const size_t base = ((size_t)pid * a.hkv + kvh) * PAGE * DH + lane * 8;
       const bf16* ks = reinterpret_cast<const bf16*>(a.k_pool) + base;
       const bf16* vs = reinterpret_cast<const bf16*>(a.v_pool) + base;
       const uint32_t sk = smem_u32(dk), sv = smem_u32(dv);
@@ -163,12 +184,14 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
     }
   };
   if constexpr (TMA) {
-    if (lane == 0)
-      for (int i = 0; i < NST - 1 && i < n_mine; ++i) issue(i);
+    for (int i = 0; i < NST - 1 && i < n_mine; ++i) {
+      const int pid = page_of(i);
+      if (lane == 0) issue(i, pid);
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < NST - 1; ++i) {
-      if (i < n_mine) issue(i);
+      if (i < n_mine) issue(i, page_of(i));
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
   }
@@ -183,10 +206,13 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
     // refill the stage consumed in the previous iteration (all lanes are past it: __syncwarp below)
     const int st = i % NST;
     if constexpr (TMA) {
-      if (lane == 0 && i + NST - 1 < n_mine) issue(i + NST - 1);
+      if (i + NST - 1 < n_mine) {
+        const int pid = page_of(i + NST - 1);
+        if (lane == 0) issue(i + NST - 1, pid);
+      }
       mbar_wait(&full[st], (i / NST) & 1);
     } else {
-      if (i + NST - 1 < n_mine) issue(i + NST - 1);
+      if (i + NST - 1 < n_mine) issue(i + NST - 1, page_of(i + NST - 1));
       asm volatile("cp.async.commit_group;" ::: "memory");
       asm volatile("cp.async.wait_group %0;" ::"n"(NST - 1) : "memory");
       __syncwarp();
@@ -228,31 +254,31 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
       mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 8));
       mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 16));
     }
-    // key 0 of a page is always valid, so the new maxima are finite
+    // key 0 of a page is always valid, so the new maxima are finite.  l is kept per lane (its 8
+    // g-lanes are summed once at the end); O is rescaled only when some head's max moved.
     const float mn0 = fmaxf(m[0], mx[0]), mn1 = fmaxf(m[1], mx[1]);
-    const float c0 = exp2f(m[0] - mn0), c1 = exp2f(m[1] - mn1);
-    m[0] = mn0;
-    m[1] = mn1;
-    const float p0 = exp2f(x[0] - mn0), p1 = exp2f(x[1] - mn1), p2 = exp2f(x[2] - mn0), p3 = exp2f(x[3] - mn1);
-    float sum0 = p0 + p2, sum1 = p1 + p3;
-    sum0 += __shfl_xor_sync(0xffffffffu, sum0, 4);
-    sum0 += __shfl_xor_sync(0xffffffffu, sum0, 8);
-    sum0 += __shfl_xor_sync(0xffffffffu, sum0, 16);
-    sum1 += __shfl_xor_sync(0xffffffffu, sum1, 4);
-    sum1 += __shfl_xor_sync(0xffffffffu, sum1, 8);
-    sum1 += __shfl_xor_sync(0xffffffffu, sum1, 16);
-    l[0] = l[0] * c0 + sum0;
-    l[1] = l[1] * c1 + sum1;
+    const bool moved = mn0 != m[0] || mn1 != m[1];
+    const float p0 = fast_exp2(x[0] - mn0), p1 = fast_exp2(x[1] - mn1), p2 = fast_exp2(x[2] - mn0),
+                p3 = fast_exp2(x[3] - mn1);
+    if (__any_sync(0xffffffffu, moved)) {
+      const float c0 = fast_exp2(m[0] - mn0), c1 = fast_exp2(m[1] - mn1);
+      l[0] *= c0;
+      l[1] *= c1;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        o[mt][0] *= c0;
+        o[mt][1] *= c1;
+        o[mt][2] *= c0;
+        o[mt][3] *= c1;
+      }
+      m[0] = mn0;
+      m[1] = mn1;
+    }
+    l[0] += p0 + p2;
+    l[1] += p1 + p3;
     // P^T fragments -> B operand of O^T += V^T P^T
     const uint32_t pb0 = movtrans(pack_bf16(p0, p1));  // keys 0-7
     const uint32_t pb1 = movtrans(pack_bf16(p2, p3));  // keys 8-15
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      o[mt][0] *= c0;
-      o[mt][1] *= c1;
-      o[mt][2] *= c0;
-      o[mt][3] *= c1;
-    }
     const int vkey = (lane & 7) + ((lane >> 4) << 3);
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
@@ -262,8 +288,14 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
     }
     __syncwarp();  // every lane is done with stage st before lane 0 re-arms it
   }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    l[h] += __shfl_xor_sync(0xffffffffu, l[h], 4);
+    l[h] += __shfl_xor_sync(0xffffffffu, l[h], 8);
+    l[h] += __shfl_xor_sync(0xffffffffu, l[h], 16);
+  }
   __syncthreads();
-  // merge the 4 warps (heads h < G); the rings are no longer needed
+  // merge the warps (heads h < G); the rings are no longer needed
   float* sm_o = reinterpret_cast<float*>(smem);  // [WARPS][8 heads][DH]
   float* sm_ml = sm_o + WARPS * 8 * DH;          // [WARPS][8][2]
   if (g == 0) {

@@ -21,6 +21,9 @@
 // reduced over K in one fixed order: results do not depend on the grid, i.e. on the SM partition.
 #include <cuda.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "dev_common.cuh"
 #include "kernels.h"
 
@@ -59,14 +62,14 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(sz) : "memory");
+__device__ __forceinline__ void tma_load_2d_hint(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], "
+      "[%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -125,13 +128,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 template <int BN, int EPI, bool SWAP>
 struct Cfg {
   static constexpr int A_TILES = (SWAP && EPI == EPI_SWIGLU) ? 2 : 1;
-  // swap mode: cp.async producers (CP) or one TMA producer with two CTAs per SM (two TMA issuers and
-  // two MMA/epilogue pipelines per SM: a TMA instruction costs its issuing thread ~0.25 us on B200,
-  // profiles/r01_probe_tma_bw.txt, so one issuer per SM cannot stream a small partition's HBM share)
-  static constexpr bool CP = false;
-  static constexpr int NPROD = (SWAP && CP) ? 4 : 1;         // producer warps
+  // swap mode streams weights from HBM on a possibly small SM partition.  A TMA instruction costs its
+  // issuing thread ~0.1-0.25 us on B200 (profiles/r01_probe_tma_bw.txt: one issuer sustains ~60 GB/s
+  // per SM, two exactly twice that), so swap tiles run two CTAs per SM with two producer warps each
+  // (four issuers per SM) taking alternate pipeline stages.
+  static constexpr int NPROD = SWAP ? 2 : 1;                 // producer warps: 0 (and 6)
   static constexpr int THREADS = 192 + (NPROD - 1) * 32;
-  static constexpr int CTAS = (SWAP && !CP) ? 2 : 1;         // CTAs per SM
+  static constexpr int CTAS = SWAP ? 2 : 1;                  // CTAs per SM
   static constexpr int A_BYTES = A_TILES * BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -143,18 +146,45 @@ struct Cfg {
   static_assert(2 * ACC_COLS <= 512, "TMEM");
 };
 
+// Split-K (swap tiles only).  A skinny decode GEMM has only N/128 weight-row tiles (32 for the O and
+// down projections of Llama-3-8B), fewer than the CTAs of even a 24-SM partition, so the K range is
+// cut into `ksplit` chunks of `kb_per` 64-wide blocks: a work unit is (tile, chunk).  The chunking
+// depends only on the GEMM shape — never on the grid — and each tile's fp32 partials are summed in
+// chunk order 0..ksplit-1 by whichever CTA finishes the tile's last chunk, so results stay
+// independent of the SM partition (and of arrival order).
+constexpr int SPLITK_TARGET_UNITS = 148;   // >= one unit per SM of the full GPU; >= 3 per CTA on a 24-SM partition
+constexpr int SPLITK_MIN_KB = 8;           // >= 512 of K per chunk
+constexpr int SPLITK_MAX = 8;              // partial bytes <= ~15% of the weight bytes at Llama-3-8B shapes
+
 struct Params {
   int M, N, K;        // C is M x N; N = output features (SwiGLU: width of act)
   int num_m, num_n, num_tiles;
+  int ksplit, kb_per, num_units;
   bf16* C;
   const bf16* R;
   const bf16* bias;
   int ldc, ldr;
   int n_up_off;       // SwiGLU: row offset of the up rows in W (= N)
-  const bf16* X;      // swap mode (cp.async producers): activations [M][ldx], weights [rows][ldw]
-  const bf16* W;
-  int ldx, ldw;
+  float* ws;          // split-K partials [num_tiles][ksplit][ACC_COLS][128]
 };
+
+// swap-mode output: thread = feature n, 32 consecutive tokens m0..m0+31 (bias / residual fused)
+template <int EPI, class P>
+__device__ __forceinline__ void swap_store(const P& p, const float (&v)[32], int m0, int n) {
+  float badd = 0.f;
+  if constexpr (EPI == EPI_STORE)
+    if (p.bias) badd = __bfloat162float(p.bias[n]);
+#pragma unroll
+  for (int e = 0; e < 32; ++e) {
+    const int m = m0 + e;
+    if (m < p.M) {
+      float o = v[e];
+      if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)m * p.ldr + n]);
+      if constexpr (EPI == EPI_STORE) o += badd;
+      p.C[(size_t)m * p.ldc + n] = __float2bfloat16_rn(o);
+    }
+  }
+}
 
 template <int BN, int EPI, bool SWAP>
 __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP>::CTAS)
@@ -173,12 +203,19 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_k = p.K / BK;
+  // unit u -> tile u % num_tiles, K chunk u / num_tiles: blocks [kb0, kb1)
+  auto unit_k = [&](int u, int& tile, int& kb0, int& kb1) {
+    tile = u % p.num_tiles;
+    const int ch = u / p.num_tiles;
+    kb0 = ch * p.kb_per;
+    kb1 = min(num_k, kb0 + p.kb_per);
+  };
 
   if (warp == 0 && lane == 0) {
     prefetch_map(&map_x);
     prefetch_map(&map_w);
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], CF::NPROD);
+      mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -197,86 +234,30 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (SWAP && CF::CP && (warp == 0 || warp >= 6)) {
-    // ---------------- swap mode: 4 producer warps (128 threads) stream the weight tile and the token
-    // tile with cp.async (16 B per lane) into the SW128 K-major layout.  On a small SM partition a TMA
-    // unit sustains only ~60 GB/s per SM from HBM (profiles/r01_probe_tma_bw.txt) while cp.async from
-    // 128 threads reaches ~130 GB/s; the decode-side GEMMs are weight-streaming, so this is their bound.
-    // A stage is published (fence.proxy.async + mbarrier arrive) LAG stages after it was issued, with
-    // LAG <= STAGES - 2 so that a publication never waits on the slot it frees.
-    constexpr int LAG = S - 2;
-    const int pt = (warp == 0 ? 0 : warp - 5) * 32 + lane;  // 0..127
-    const bf16* X = p.X;
-    const bf16* Wt = p.W;
-    int s = 0, ps = 0, inflight = 0;
-    uint32_t ph = 0;
-    auto publish = [&]() {
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&full[ps]);
-      if (++ps == S) ps = 0;
-    };
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      const int mb = t % p.num_m, nb = t / p.num_m;
-      for (int kb = 0; kb < num_k; ++kb) {
-        mbar_wait(&empty[s], ph ^ 1);
-        const uint32_t a_dst = smem_u32(sA + s * CF::A_BYTES), b_dst = smem_u32(sB + s * CF::B_BYTES);
-        // weight rows (gate rows, then up rows for SwiGLU): 128 rows x 8 chunks per tile
-#pragma unroll
-        for (int tt = 0; tt < CF::A_TILES; ++tt) {
-          const int roff = tt ? p.n_up_off : 0;
-#pragma unroll
-          for (int i = 0; i < (BM * 8) / 128; ++i) {
-            const int c = pt + i * 128, row = c >> 3, c16 = c & 7;
-            const int n = nb * BM + row;
-            const bool v = n < p.N;
-            const bf16* src = Wt + (v ? (size_t)(roff + n) * p.ldw + (size_t)kb * BK + c16 * 8 : 0);
-            cp_async16(a_dst + tt * BM * BK * 2 + row * 128 + ((c16 ^ (row & 7)) << 4), src, v);
-          }
-        }
-        // token rows: BN rows x 8 chunks
-#pragma unroll
-        for (int i = 0; i < (BN * 8 + 127) / 128; ++i) {
-          const int c = pt + i * 128;
-          if (c < BN * 8) {
-            const int row = c >> 3, c16 = c & 7;
-            const int m = mb * BN + row;
-            const bool v = m < p.M;
-            const bf16* src = X + (v ? (size_t)m * p.ldx + (size_t)kb * BK + c16 * 8 : 0);
-            cp_async16(b_dst + row * 128 + ((c16 ^ (row & 7)) << 4), src, v);
-          }
-        }
-        cp_commit();
-        if (++inflight > LAG) {
-          cp_wait<LAG>();
-          publish();
-          --inflight;
-        }
-        if (++s == S) {
-          s = 0;
-          ph ^= 1;
-        }
-      }
-    }
-    cp_wait<0>();
-    while (inflight-- > 0) publish();
-  } else if (warp == 0) {
+  if (warp == 0 || warp >= 6) {
     if (lane == 0) {
-      // ---------------- TMA producer (normal tiles)
-      int s = 0;
-      uint32_t ph = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      // ---------------- TMA producer(s): producer `pr` issues the k-blocks it with it % NPROD == pr
+      const int pr = warp == 0 ? 0 : warp - 5;
+      uint64_t pol_w = 0;
+      if constexpr (SWAP)  // weights are streamed once per step: evict-first keeps split-K partials in L2
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
+      int it = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+        int t, kb0, kb1;
+        unit_k(u, t, kb0, kb1);
         const int mb = t % p.num_m, nb = t / p.num_m;
-        for (int kb = 0; kb < num_k; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          if (it % CF::NPROD != pr) continue;
+          const int s = it % S;
+          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           mbar_expect_tx(&full[s], CF::STAGE_BYTES);
           uint8_t* a_dst = sA + s * CF::A_BYTES;
           uint8_t* b_dst = sB + s * CF::B_BYTES;
           if constexpr (SWAP) {
             const int j0 = nb * BM;
-            tma_load_2d(&map_w, &full[s], a_dst, kb * BK, j0);
+            tma_load_2d_hint(&map_w, &full[s], a_dst, kb * BK, j0, pol_w);
             if constexpr (EPI == EPI_SWIGLU)
-              tma_load_2d(&map_w, &full[s], a_dst + BM * BK * 2, kb * BK, p.n_up_off + j0);
+              tma_load_2d_hint(&map_w, &full[s], a_dst + BM * BK * 2, kb * BK, p.n_up_off + j0, pol_w);
             tma_load_2d(&map_x, &full[s], b_dst, kb * BK, mb * BN);
           } else {
             tma_load_2d(&map_x, &full[s], a_dst, kb * BK, mb * BM);
@@ -288,10 +269,6 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
               tma_load_2d(&map_w, &full[s], b_dst, kb * BK, nb * BN);
             }
           }
-          if (++s == S) {
-            s = 0;
-            ph ^= 1;
-          }
         }
       }
     }
@@ -299,32 +276,29 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
     if (lane == 0) {
       // ---------------- MMA issuer
       constexpr uint32_t idesc = idesc_bf16(BM, BN);
-      int s = 0;
-      uint32_t ph = 0;
-      int i = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++i) {
+      int it = 0, i = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++i) {
+        int t, kb0, kb1;
+        unit_k(u, t, kb0, kb1);
         const int acc = i & 1;
         const uint32_t aph = (i >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * CF::ACC_COLS;
-        for (int kb = 0; kb < num_k; ++kb) {
-          mbar_wait(&full[s], ph);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % S;
+          mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + s * CF::A_BYTES);
           const uint32_t b0 = smem_u32(sB + s * CF::B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            umma_bf16(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (kb | k) != 0);
+            umma_bf16(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (kb > kb0 || k) != 0);
             if constexpr (SWAP && EPI == EPI_SWIGLU)
               umma_bf16(d_tmem + BN, sw128_desc(a0 + BM * BK * 2 + k * 32), sw128_desc(b0 + k * 32), idesc,
-                        (kb | k) != 0);
+                        (kb > kb0 || k) != 0);
           }
           umma_commit(&empty[s]);
-          if (++s == S) {
-            s = 0;
-            ph ^= 1;
-          }
         }
         umma_commit(&tfull[acc]);
       }
@@ -334,7 +308,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
     const int quad = warp & 3;
     const int lane_row = quad * 32 + lane;
     int i = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++i) {
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++i) {
+      int t, kb0, kb1;
+      unit_k(u, t, kb0, kb1);
       const int acc = i & 1;
       const uint32_t aph = (i >> 1) & 1;
       const int mb = t % p.num_m, nb = t / p.num_m;
@@ -387,7 +363,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
                 store16<bf16>(dst + q * 8, o8);
               }
             } else {
-              for (int e = 0; e < 32 && n0 + c + e < p.N; ++e) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                if (n0 + c + e >= p.N) continue;
                 float o = v[e];
                 if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)row * p.ldr + n0 + c + e]);
                 if constexpr (EPI == EPI_STORE)
@@ -397,13 +375,10 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
             }
           }
         }
-      } else {
+      } else if (p.ksplit == 1) {
         // lane = output feature n, columns = tokens m
         const int n = nb * BM + lane_row;
         const bool n_ok = n < p.N;
-        float badd = 0.f;
-        if constexpr (EPI == EPI_STORE)
-          if (p.bias && n_ok) badd = __bfloat162float(p.bias[n]);
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           const int m0 = mb * BN + c;
@@ -416,18 +391,19 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[e] = silu_f(v[e]) * u[e];
           }
-          if (n_ok) {
+          if (n_ok) swap_store<EPI>(p, v, m0, n);
+        }
+      } else {
+        // split-K: this chunk's fp32 partial, column-major [ACC_COLS][128 rows] so both this store
+        // and the reduction kernel's loads are coalesced across the 128 weight rows
+        const int ch = u / p.num_tiles;
+        float* part = p.ws + ((size_t)t * p.ksplit + ch) * CF::ACC_COLS * BM + lane_row;
+#pragma unroll 1
+        for (int c = 0; c < CF::ACC_COLS; c += 32) {
+          float v[32];
+          tmem_ld32(tbase + c, v);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const int m = m0 + e;
-              if (m < p.M) {
-                float o = v[e];
-                if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)m * p.ldr + n]);
-                if constexpr (EPI == EPI_STORE) o += badd;
-                p.C[(size_t)m * p.ldc + n] = __float2bfloat16_rn(o);
-              }
-            }
-          }
+          for (int e = 0; e < 32; ++e) __stcg(part + (size_t)(c + e) * BM, v[e]);
         }
       }
       tc_fence_before();
@@ -440,6 +416,55 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(CF::TMEM_COLS));
+  }
+}
+
+// Split-K reduction + epilogue: one CTA per (tile, 16-token slice), thread = weight row n.  Sums the
+// ksplit partials of each output in chunk order 0..ksplit-1 (a fixed order, independent of the grid
+// and of which CTA computed which chunk), then applies the fused epilogue and stores C[m][n].
+template <int EPI>
+__global__ void __launch_bounds__(128) splitk_reduce_kernel(Params p, int bn, int acc_cols) {
+  const int t = blockIdx.x, r = threadIdx.x;
+  const int mb = t % p.num_m, nb = t / p.num_m;
+  const int n = nb * BM + r;
+  if (n >= p.N) return;
+  const size_t chunk = (size_t)acc_cols * BM;
+  const float* base = p.ws + (size_t)t * p.ksplit * chunk + r;
+  float badd = 0.f;
+  if constexpr (EPI == EPI_STORE)
+    if (p.bias) badd = __bfloat162float(p.bias[n]);
+#pragma unroll 1
+  for (int j0 = 0; j0 < 16; j0 += 4) {
+    float v[4], g[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int ml = blockIdx.y * 16 + j0 + j;
+      float f[SPLITK_MAX], h[SPLITK_MAX];
+#pragma unroll
+      for (int k = 0; k < SPLITK_MAX; ++k)
+        if (k < p.ksplit) {
+          f[k] = __ldcg(base + k * chunk + (size_t)ml * BM);
+          if constexpr (EPI == EPI_SWIGLU) h[k] = __ldcg(base + k * chunk + (size_t)(bn + ml) * BM);
+        }
+      v[j] = f[0];
+      g[j] = EPI == EPI_SWIGLU ? h[0] : 0.f;
+#pragma unroll
+      for (int k = 1; k < SPLITK_MAX; ++k)
+        if (k < p.ksplit) {
+          v[j] += f[k];
+          if constexpr (EPI == EPI_SWIGLU) g[j] += h[k];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = mb * bn + blockIdx.y * 16 + j0 + j;
+      if (m >= p.M) continue;
+      float o = v[j];
+      if constexpr (EPI == EPI_SWIGLU) o = silu_f(o) * g[j];
+      if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)m * p.ldr + n]);
+      if constexpr (EPI == EPI_STORE) o += badd;
+      p.C[(size_t)m * p.ldc + n] = __float2bfloat16_rn(o);
+    }
   }
 }
 
@@ -474,6 +499,16 @@ static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int l
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// K chunking of a split-K launch: a function of the shape only (see SPLITK_TARGET_UNITS)
+static void splitk_plan(int num_tiles, int num_k, int* ks_out, int* kb_out) {
+  int ks = (SPLITK_TARGET_UNITS + num_tiles - 1) / num_tiles;
+  ks = std::min(std::min(ks, SPLITK_MAX), num_k / SPLITK_MIN_KB);
+  if (ks < 1) ks = 1;
+  const int kb = (num_k + ks - 1) / ks;
+  *ks_out = (num_k + kb - 1) / kb;
+  *kb_out = kb;
+}
+
 template <int BN, int EPI, bool SWAP>
 static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   using CF = Cfg<BN, EPI, SWAP>;
@@ -496,23 +531,38 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
     p.num_n = (a.N + out_cols - 1) / out_cols;
   } else {
     if (!make_map(&mx, a.A, a.M, a.K, a.lda, BN)) return -1;
-    if (!make_map(&mw, a.B, w_rows, a.K, a.ldb, BM / CF::NPROD)) return -1;
+    if (!make_map(&mw, a.B, w_rows, a.K, a.ldb, BM)) return -1;
     p.num_m = (a.M + BN - 1) / BN;
     p.num_n = (a.N + BM - 1) / BM;
   }
   p.num_tiles = p.num_m * p.num_n;
+  p.ksplit = 1;
+  p.kb_per = a.K / BK;
+  if constexpr (SWAP) {
+    int ks, kb;
+    splitk_plan(p.num_tiles, a.K / BK, &ks, &kb);
+    const size_t need = (size_t)p.num_tiles * ks * BM * CF::ACC_COLS;
+    static const bool splitk_on = !getenv("DUET_SPLITK") || atoi(getenv("DUET_SPLITK")) != 0;  // A/B switch
+    if (splitk_on && ks > 1 && a.ws && need <= a.ws_floats) {
+      p.ksplit = ks;
+      p.kb_per = kb;
+      p.ws = a.ws;
+    }
+  }
+  p.num_units = p.num_tiles * p.ksplit;
+
   p.C = (bf16*)a.C;
   p.R = (const bf16*)a.R;
   p.bias = (const bf16*)a.bias;
   p.ldc = a.ldc;
   p.ldr = a.ldr;
   p.n_up_off = a.N;
-  p.X = (const bf16*)a.A;
-  p.W = (const bf16*)a.B;
-  p.ldx = a.lda;
-  p.ldw = a.ldb;
-  const int grid = p.num_tiles < CF::CTAS * num_sms ? p.num_tiles : CF::CTAS * num_sms;
+  const int grid = p.num_units < CF::CTAS * num_sms ? p.num_units : CF::CTAS * num_sms;
   gemm_tc_kernel<BN, EPI, SWAP><<<grid, CF::THREADS, CF::SMEM, st>>>(mx, mw, p);
+  if (p.ksplit > 1) {
+    splitk_reduce_kernel<EPI><<<dim3(p.num_tiles, BN / 16), 128, 0, st>>>(p, BN, CF::ACC_COLS);
+    return 2;
+  }
   return 1;
 }
 
@@ -532,6 +582,16 @@ bool gemm_tc_supported(const GemmArgs& a) {
   if (a.epi == EPI_SWIGLU && a.N % 128) return false;
   if (!tc::encode_fn()) return false;
   return true;
+}
+
+size_t gemm_tc_splitk_need(int M, int N, int K, int epi) {
+  if (M <= 0 || M > 128 || K % tc::BK) return 0;
+  const int bn = M <= 64 ? 64 : 128;
+  const int num_tiles = ((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
+  int ks, kb;
+  tc::splitk_plan(num_tiles, K / tc::BK, &ks, &kb);
+  if (ks <= 1) return 0;
+  return (size_t)num_tiles * ks * tc::BM * (epi == EPI_SWIGLU ? 2 * bn : bn);
 }
 
 int launch_gemm_tc(const GemmArgs& a, int num_sms, cudaStream_t st) {

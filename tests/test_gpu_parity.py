@@ -150,15 +150,23 @@ def test_fine_grained_partitions_and_no_graph():
         _check_outputs(g, y_pre, y_dec, TOL["fp32"])
 
 
-def test_temporal_equals_spatial_bitwise_k1():
+def test_temporal_vs_spatial_k1_and_run_to_run_determinism():
+    """Temporal and spatial modes compute the same function (split-K weight-streaming GEMMs on a
+    <= 128-row side reduce in another fp32 grouping than the 128-row tiles of the joint batch, so the
+    two agree to rounding, not bitwise); a repeated step of the same split is bitwise identical."""
     cfg = configs.get_config("cfg1-bf16")
     wl = workload.build(cfg, k=1)
     gt, ctx = _run_split(wl, "bf16", lambda c: D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1))
     gs = GpuWorkload(wl, "bf16")
     gs.step(ctx, D.split_struct(D.DUET_MODE_SPATIAL, 132, 16, 1))
     torch.cuda.synchronize()
-    assert torch.equal(gt.y_dec, gs.y_dec)
-    assert torch.equal(gt.y_pre, gs.y_pre)
+    assert rel_err(gs.y_dec.float().cpu().numpy(), gt.y_dec.float().cpu().numpy()) <= 1e-2
+    assert rel_err(gs.y_pre.float().cpu().numpy(), gt.y_pre.float().cpu().numpy()) <= 1e-2
+    gs2 = GpuWorkload(wl, "bf16")
+    gs2.step(ctx, D.split_struct(D.DUET_MODE_SPATIAL, 132, 16, 1))
+    torch.cuda.synchronize()
+    assert torch.equal(gs.y_dec, gs2.y_dec)
+    assert torch.equal(gs.y_pre, gs2.y_pre)
 
 
 def test_decode_after_prefill_invariant_gpu():
@@ -231,6 +239,12 @@ def test_op_gemm_bf16(M, N, K, epi):
         ref = g / (1 + torch.exp(-g)) * u
     e = (C.double() - ref).abs().max().item() / ref.abs().max().item()
     assert e < 1e-2, e
+    # split-K launches (M <= 128, long K) re-arm their tile counters and reduce in a fixed order:
+    # a second call is bitwise identical
+    C2 = torch.empty_like(C)
+    ctx.op_gemm(A, B, C2, R if epi == 1 else None, bias if epi == 3 else None, 0 if epi == 3 else epi)
+    torch.cuda.synchronize()
+    assert torch.equal(C, C2)
 
 
 @pytest.mark.slow
