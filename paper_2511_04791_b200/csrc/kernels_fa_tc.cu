@@ -1,19 +1,23 @@
 // Causal prefill attention over the paged KV cache on 5th-generation tensor cores (tcgen05 / TMEM).
 //
 // Chunked prefill (§4.1; readings #2, #6, #7): a chunk of q tokens at positions
-// c..c+q-1 attends to its c-token prefix and to itself causally.  One CTA = 128 query rows of one
-// query head; the keys stream in 64-key tiles (4 pages of 16 tokens).
-//   warp 0      Q tile by TMA (two 64-column SWIZZLE_128B boxes)
-//   warp 1      TMEM allocator + tcgen05.mma issuer: S_j = Q K_j^T (UMMA 128x64x16, both operands
-//               K-major) into one of two TMEM S buffers, then O += P_{j-1} V_{j-1} (A = P from smem,
-//               B = V MN-major) — the MMAs of S_{j+1} overlap the softmax of tile j
-//   warps 2..5  softmax, one thread per query row (= TMEM lane): max / exp2 / sum in registers, P
-//               written to one of two smem buffers in the UMMA SW128 layout; the running max is re-based
-//               (O rescaled in TMEM) only when it grows by more than 2^8, so P <= 256
-//   warps 6..9  K/V loaders: cp.async gathers of the scattered 4 KiB page blocks into a 4-stage ring
-//               (a TMA box costs its issuing thread ~0.25 us on B200 — profiles/r01_probe_tma_bw.txt —
-//               and a page needs four), published LAG = 2 tiles behind the issue front
-// Keys past the causal end of the tile are zero-filled (cp.async src-size 0) and masked.
+// c..c+q-1 attends to its c-token prefix and to itself causally.  One CTA = the same 128 query rows
+// of TWO query heads of one GQA group (reading #6: they read the same kv head), so every K/V tile is
+// gathered once for two 128x64 score tiles; keys stream in 64-key tiles (4 pages of 16 tokens).
+//   warp 0        Q tiles by TMA (2 heads x two 64-column SWIZZLE_128B boxes)
+//   warp 1        TMEM allocator (all 512 columns) + tcgen05.mma issuer: for key tile j,
+//                 S_j^h = Q^h K_j^T for both heads (UMMA 128x64x16, K-major operands) into one of two
+//                 S buffers per head, then O^h += P_{j-1}^h V_{j-1} (A = P from smem, B = V MN-major)
+//   warps 2..5    softmax of head A, one thread per query row (= TMEM lane)
+//   warps 6..9    softmax of head B — each SM sub-partition runs one warp of each head, so the
+//                 exp/FMA work of one head overlaps the other's waits (and the MMAs)
+//   warps 10..13  K/V loaders: cp.async gathers of the scattered 4 KiB page blocks into a 4-stage ring
+//                 (a TMA box costs its issuing thread ~0.25 us on B200 — profiles/r01_probe_tma_bw.txt —
+//                 and a page needs four); each thread's copies are tracked by the stage's mbarrier
+//                 (cp.async.mbarrier.arrive.noinc), so a tile is published the moment it lands
+// The running max is re-based (O rescaled in TMEM) only when it grows by more than 2^8; the decision is
+// taken per warp because tcgen05.ld/st are warp-collective.  Keys past the causal end of a tile are
+// zero-filled (cp.async src-size 0) and masked.  An odd last head of a group runs alone (has_b = 0).
 #include <cuda.h>
 
 #include "dev_common.cuh"
@@ -22,20 +26,22 @@
 namespace duet {
 namespace fatc {
 
-constexpr int BQ = 128, BKV = 64, DH = 128, PAGE = 16, KV_STAGES = 4, LAG = 2;
+constexpr int BQ = 128, BKV = 64, DH = 128, PAGE = 16, KV_STAGES = 4;
 constexpr int Q_SUB = BQ * 128;            // [128 rows][64 cols] SW128 sub-tile = 16 KiB
 constexpr int KV_SUB = BKV * 128;          // [64 rows][64 cols] = 8 KiB
-constexpr int Q_BYTES = 2 * Q_SUB;         // 32 KiB
+constexpr int Q_BYTES = 2 * Q_SUB;         // 32 KiB per head
 constexpr int KV_BYTES = 2 * KV_SUB;       // 16 KiB per tensor per stage
-constexpr int P_BYTES = BQ * BKV * 2;      // [128 rows][64 keys] = one SW128 sub-tile, 16 KiB
-constexpr int OFF_Q = 0;
-constexpr int OFF_K = OFF_Q + Q_BYTES;
+constexpr int P_BYTES = BQ * BKV * 2;      // [128 rows][64 keys] = one SW128 sub-tile, 16 KiB per head
+constexpr int OFF_Q = 0;                   // head A, head B
+constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
 constexpr int OFF_V = OFF_K + KV_STAGES * KV_BYTES;
-constexpr int OFF_P = OFF_V + KV_STAGES * KV_BYTES;
+constexpr int OFF_P = OFF_V + KV_STAGES * KV_BYTES;  // head A, head B
 constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
-constexpr int TMEM_COLS = 256;             // S0 (64) | S1 (64) | O (128)
+constexpr int THREADS = 14 * 32;
+constexpr int TMEM_COLS = 512;             // per head: S0 (64) | S1 (64) | O (128)
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
+static_assert(SMEM <= 227 * 1024, "smem");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -132,31 +138,37 @@ struct Params {
   const int* cpre;
   const int* seq_row;
   const int* table;
-  int max_pages, hq, hkv, n_qtiles;
+  int max_pages, hq, hkv, n_qtiles, n_pairs;
   bf16* o;
   const bf16* k_pool;
   const bf16* v_pool;
 };
 
-__global__ void __launch_bounds__(320, 1) fa_tc_kernel(const __grid_constant__ CUtensorMap map_q, Params p) {
+__global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant__ CUtensorMap map_q, Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bar = (uint64_t*)(smem + OFF_BAR);
   uint64_t* q_full = bar;                   // 1
   uint64_t* kv_full = bar + 1;              // [KV_STAGES]
   uint64_t* kv_empty = kv_full + KV_STAGES; // [KV_STAGES]
-  uint64_t* s_full = kv_empty + KV_STAGES;  // [2]
-  uint64_t* s_free = s_full + 2;            // [2]
-  uint64_t* p_full = s_free + 2;            // [2]
-  uint64_t* pv_done = p_full + 2;           // [2]  PV of the tile that used P buffer b
+  uint64_t* s_full = kv_empty + KV_STAGES;  // [head][2]
+  uint64_t* s_free = s_full + 4;            // [head][2]
+  uint64_t* p_full = s_free + 4;            // [head]
+  uint64_t* pv_done = p_full + 2;           // [head]
   uint32_t* tmem_slot = (uint32_t*)(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = p.n_qtiles - 1 - blockIdx.x;  // heavy (late) tiles first
-  const int head = blockIdx.y, s_id = blockIdx.z;
+  const int pair = blockIdx.x;
+  const int qt = p.n_qtiles - 1 - blockIdx.y;  // heavy (late) tiles first, all pairs of a tile together
+  const int s_id = blockIdx.z;
   const int qlen = p.qlen[s_id];
   if (qt * BQ >= qlen) return;
-  const int G = p.hq / p.hkv, kvh = head / G;
+  const int G = p.hq / p.hkv;
+  const int pairs_per_group = (G + 1) / 2;
+  const int kvh = pair / pairs_per_group;
+  const int head_a = kvh * G + (pair % pairs_per_group) * 2;
+  const bool has_b = head_a + 1 < (kvh + 1) * G;
+  const int n_heads = has_b ? 2 : 1;
   const int row0 = p.row0[s_id], cpre = p.cpre[s_id];
   const int* tab = p.table + (size_t)p.seq_row[s_id] * p.max_pages;
   const int q0 = qt * BQ;
@@ -167,12 +179,14 @@ __global__ void __launch_bounds__(320, 1) fa_tc_kernel(const __grid_constant__ C
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
     for (int i = 0; i < KV_STAGES; ++i) {
-      mbar_init(&kv_full[i], 4);  // one arrive per loader warp
+      mbar_init(&kv_full[i], 128);  // one cp.async-tracked (noinc) arrive per loader thread
       mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
     }
@@ -187,22 +201,27 @@ __global__ void __launch_bounds__(320, 1) fa_tc_kernel(const __grid_constant__ C
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t T_S0 = tmem, T_S1 = tmem + BKV, T_O = tmem + 2 * BKV;
+  // head h: S buffers at h*256 + {0, 64}, O at h*256 + 128
+  auto T_S = [&](int h, int b) { return tmem + h * 256 + b * BKV; };
+  auto T_O = [&](int h) { return tmem + h * 256 + 2 * BKV; };
 
   if (warp == 0) {
     if (lane == 0) {
-      // ------------------------------------------------ Q tile (TMA, two 64-column boxes)
-      mbar_expect_tx(q_full, Q_BYTES);
-      tma_load_2d(&map_q, q_full, smem + OFF_Q, head * DH, row0 + q0);
-      tma_load_2d(&map_q, q_full, smem + OFF_Q + Q_SUB, head * DH + 64, row0 + q0);
+      // ------------------------------------------------ Q tiles (TMA, two 64-column boxes per head)
+      mbar_expect_tx(q_full, n_heads * Q_BYTES);
+      for (int h = 0; h < n_heads; ++h) {
+        tma_load_2d(&map_q, q_full, smem + OFF_Q + h * Q_BYTES, (head_a + h) * DH, row0 + q0);
+        tma_load_2d(&map_q, q_full, smem + OFF_Q + h * Q_BYTES + Q_SUB, (head_a + h) * DH + 64, row0 + q0);
+      }
     }
-  } else if (warp >= 6) {
+  } else if (warp >= 10) {
     // ------------------------------------------------ K/V loaders (4 warps, cp.async, 4-stage ring)
-    const int lt = threadIdx.x - 6 * 32;  // 0..127
+    const int lt = threadIdx.x - 10 * 32;  // 0..127
     const size_t page_stride = (size_t)p.hkv * PAGE * DH;
     // chunk c = lt + 128 i (i < 8) of a [64 keys][16 chunks] tile: key = c / 16, 16-B column = c % 16
-    auto issue = [&](int j) {
+    for (int j = 0; j < n_kt; ++j) {
       const int st = j % KV_STAGES;
+      mbar_wait(&kv_empty[st], ((j / KV_STAGES) & 1) ^ 1);
       const uint32_t kd = smem_u32(smem + OFF_K + st * KV_BYTES), vd = smem_u32(smem + OFF_V + st * KV_BYTES);
 #pragma unroll
       for (int i = 0; i < (BKV * 16) / 128; ++i) {
@@ -219,167 +238,163 @@ __global__ void __launch_bounds__(320, 1) fa_tc_kernel(const __grid_constant__ C
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(vd + so), "l"(p.v_pool + off), "r"(sz)
                      : "memory");
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    int pub = 0;
-    auto publish = [&]() {  // the oldest unpublished tile has landed -> visible to the async proxy
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&kv_full[pub % KV_STAGES]);
-      ++pub;
-    };
-    // LAG <= KV_STAGES - 2: tile j - KV_STAGES (whose consumption frees slot j) is always published first
-    for (int j = 0; j < n_kt; ++j) {
-      mbar_wait(&kv_empty[j % KV_STAGES], ((j / KV_STAGES) & 1) ^ 1);
-      issue(j);
-      if (j >= LAG) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(LAG) : "memory");
-        publish();
-      }
+      // the barrier phase completes when every loader thread's copies of this tile have landed
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kv_full[st])) : "memory");
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    while (pub < n_kt) publish();
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     constexpr uint32_t ID_S = idesc(BKV, false), ID_PV = idesc(DH, true);
-    const uint32_t sq = smem_u32(smem + OFF_Q);
     mbar_wait(q_full, 0);
     for (int j = 0; j <= n_kt; ++j) {
       if (j < n_kt) {
         const int b = j & 1, st = j % KV_STAGES;
-        if (j >= 2) mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);
         mbar_wait(&kv_full[st], (j / KV_STAGES) & 1);
+        fence_async_smem();  // the loaders' cp.async (generic proxy) writes -> visible to the MMA (async proxy)
         tc_after();
-        if (lane == 0) {
-          const uint32_t sk = smem_u32(smem + OFF_K + st * KV_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk) {
-            umma(b ? T_S1 : T_S0, desc_k(sq + (kk >> 2) * Q_SUB + (kk & 3) * 32),
-                 desc_k(sk + (kk >> 2) * KV_SUB + (kk & 3) * 32), ID_S, kk > 0);
+        const uint32_t sk = smem_u32(smem + OFF_K + st * KV_BYTES);
+        for (int h = 0; h < n_heads; ++h) {
+          if (j >= 2) {
+            mbar_wait(&s_free[h * 2 + b], ((j - 2) >> 1) & 1);
+            tc_after();
           }
-          umma_commit(&s_full[b]);
+          if (lane == 0) {
+            const uint32_t sq = smem_u32(smem + OFF_Q + h * Q_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < DH / 16; ++kk)
+              umma(T_S(h, b), desc_k(sq + (kk >> 2) * Q_SUB + (kk & 3) * 32),
+                   desc_k(sk + (kk >> 2) * KV_SUB + (kk & 3) * 32), ID_S, kk > 0);
+            umma_commit(&s_full[h * 2 + b]);
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
       if (j >= 1) {
-        const int jp = j - 1, b = jp & 1, st = jp % KV_STAGES;
-        mbar_wait(&p_full[b], (jp >> 1) & 1);
-        tc_after();
-        if (lane == 0) {
-          const uint32_t spp = smem_u32(smem + OFF_P + b * P_BYTES);
-          const uint32_t sv = smem_u32(smem + OFF_V + st * KV_BYTES);
+        const int jp = j - 1, st = jp % KV_STAGES;
+        const uint32_t sv = smem_u32(smem + OFF_V + st * KV_BYTES);
+        for (int h = 0; h < n_heads; ++h) {
+          mbar_wait(&p_full[h], jp & 1);
+          tc_after();
+          if (lane == 0) {
+            const uint32_t spp = smem_u32(smem + OFF_P + h * P_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk)  // 16 keys per UMMA k-step
-            umma(T_O, desc_k(spp + kk * 32), desc_mn(sv + kk * 16 * 128), ID_PV, (jp > 0 || kk > 0));
-          umma_commit(&kv_empty[st]);
-          umma_commit(&pv_done[b]);
+            for (int kk = 0; kk < BKV / 16; ++kk)  // 16 keys per UMMA k-step
+              umma(T_O(h), desc_k(spp + kk * 32), desc_mn(sv + kk * 16 * 128), ID_PV, (jp > 0 || kk > 0));
+            umma_commit(&pv_done[h]);
+            if (h == n_heads - 1) umma_commit(&kv_empty[st]);
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   } else {
     // ------------------------------------------------ softmax warps: one thread per query row
-    const int quad = warp & 3;
-    const int r = quad * 32 + lane;                          // row in tile = TMEM lane
-    const int pos = min(cpre + q0 + r, kv_end - 1);          // clamp rows past the chunk
-    const float sc = rsqrtf((float)DH) * 1.4426950408889634f;
-    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    const uint32_t sw = (uint32_t)(r & 7);
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kt; ++j) {
-      const int b = j & 1;
-      const uint32_t T_S = b ? T_S1 : T_S0;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
-      tc_after();
-      const int kbase = j * BKV;
-      uint32_t v0[32], v1[32];
-      tmem_ld32(T_S + lane_base, v0);
-      tmem_ld32(T_S + lane_base + 32, v1);
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[b]);  // S buffer b may be overwritten by S_{j+2}
-      const int lim = pos - kbase;  // keys 0..lim of this tile are visible to this row
-      float mx = -INFINITY;
-      if (lim >= BKV - 1) {
+    const int h = (warp - 2) >> 2;  // head A (warps 2..5) or B (6..9)
+    if (h < n_heads) {
+      const int quad = warp & 3;
+      const int r = quad * 32 + lane;                          // row in tile = TMEM lane
+      const int pos = min(cpre + q0 + r, kv_end - 1);          // clamp rows past the chunk
+      const float sc = rsqrtf((float)DH) * 1.4426950408889634f;
+      const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+      const uint32_t sw = (uint32_t)(r & 7);
+      uint8_t* prow = smem + OFF_P + h * P_BYTES + r * 128;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_kt; ++j) {
+        const int b = j & 1;
+        mbar_wait(&s_full[h * 2 + b], (j >> 1) & 1);
+        tc_after();
+        const int kbase = j * BKV;
+        uint32_t v0[32], v1[32];
+        tmem_ld32(T_S(h, b) + lane_base, v0);
+        tmem_ld32(T_S(h, b) + lane_base + 32, v1);
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[h * 2 + b]);  // S buffer b may be overwritten by S_{j+2}
+        const int lim = pos - kbase;  // keys 0..lim of this tile are visible to this row
+        float mx = -INFINITY;
+        if (lim >= BKV - 1) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, fmaxf(__uint_as_float(v0[e]), __uint_as_float(v1[e])));
-      } else {
+          for (int e = 0; e < 32; e += 2)
+            mx = fmaxf(mx, fmaxf(fmaxf(__uint_as_float(v0[e]), __uint_as_float(v0[e + 1])),
+                                 fmaxf(__uint_as_float(v1[e]), __uint_as_float(v1[e + 1]))));
+        } else {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          if (e <= lim) mx = fmaxf(mx, __uint_as_float(v0[e]));
-          if (32 + e <= lim) mx = fmaxf(mx, __uint_as_float(v1[e]));
-        }
-      }
-      const float m_new = fmaxf(m_used, mx * sc);  // sc > 0: the max commutes with the scaling
-      // Re-base the rows whose max grew by more than 2^8.  tcgen05.ld/st are warp-collective
-      // (.sync.aligned), so the decision is made per warp and rows that keep their max scale by 1.
-      const bool mine = m_new > m_used + RESCALE_THRESHOLD;
-      if (__any_sync(0xffffffffu, mine)) {
-        if (j >= 1) {
-          // O must be quiescent: wait for PV_{j-1} (all earlier ones completed before it)
-          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-          tc_after();
-          const float f = mine ? exp2f(m_used - m_new) : 1.f;
-          l *= f;
-#pragma unroll 1
-          for (int c = 0; c < DH; c += 32) {
-            uint32_t v[32];
-            tmem_ld32(T_O + lane_base + c, v);
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * f);
-            tmem_st32(T_O + lane_base + c, v);
+          for (int e = 0; e < 32; ++e) {
+            if (e <= lim) mx = fmaxf(mx, __uint_as_float(v0[e]));
+            if (32 + e <= lim) mx = fmaxf(mx, __uint_as_float(v1[e]));
           }
         }
-        if (mine) m_used = m_new;
-      }
-      // P buffer b is free once PV_{j-2} has completed
-      if (j >= 2) {
-        mbar_wait(&pv_done[b], ((j - 2) >> 1) & 1);
-        tc_after();
-      }
-      uint8_t* prow = smem + OFF_P + b * P_BYTES + r * 128;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float s0 = __uint_as_float(h ? v1[e] : v0[e]), s1 = __uint_as_float(h ? v1[e + 1] : v0[e + 1]);
-          const int k0 = h * 32 + e;
-          const float p0 = (k0 <= lim) ? fast_exp2(fmaf(s0, sc, -m_used)) : 0.f;
-          const float p1 = (k0 + 1 <= lim) ? fast_exp2(fmaf(s1, sc, -m_used)) : 0.f;
-          l += p0 + p1;
-          __nv_bfloat162 hh = __floats2bfloat162_rn(p0, p1);
-          pk[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
-        }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const uint32_t chunk = (uint32_t)(h * 4 + q4);
-          *reinterpret_cast<uint4*>(prow + ((chunk ^ sw) << 4)) =
-              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
-        }
-      }
-      fence_async_smem();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[b]);
-    }
-    // epilogue: O / l -> bf16 -> global
-    mbar_wait(&pv_done[(n_kt - 1) & 1], ((n_kt - 1) >> 1) & 1);
-    tc_after();
-    const bool row_ok = q0 + r < qlen;
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    bf16* dst = p.o + (size_t)(row0 + q0 + r) * p.hq * DH + (size_t)head * DH;
+        const float m_new = fmaxf(m_used, mx * sc);  // sc > 0: the max commutes with the scaling
+        // PV_{j-1} must be complete before O is rescaled or P is overwritten
+        bool pv_waited = j == 0;
+        const bool mine = m_new > m_used + RESCALE_THRESHOLD;
+        if (__any_sync(0xffffffffu, mine)) {
+          if (j >= 1) {
+            mbar_wait(&pv_done[h], (j - 1) & 1);
+            tc_after();
+            pv_waited = true;
+            const float f = mine ? exp2f(m_used - m_new) : 1.f;
+            l *= f;
 #pragma unroll 1
-    for (int c = 0; c < DH; c += 32) {
-      uint32_t v[32];
-      tmem_ld32(T_O + lane_base + c, v);
-      if (row_ok) {
+            for (int c = 0; c < DH; c += 32) {
+              uint32_t v[32];
+              tmem_ld32(T_O(h) + lane_base + c, v);
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          float o8[8];
+              for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * f);
+              tmem_st32(T_O(h) + lane_base + c, v);
+            }
+          }
+          if (mine) m_used = m_new;
+        }
+        // exponentials into packed bf16 pairs (registers), then publish P once PV_{j-1} is done
+        uint32_t pk[32];
+        float l0 = 0.f, l1 = 0.f;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) o8[e] = __uint_as_float(v[q4 * 8 + e]) * inv;
-          store16<bf16>(dst + c + q4 * 8, o8);
+        for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float s0 = __uint_as_float(hh ? v1[e] : v0[e]), s1 = __uint_as_float(hh ? v1[e + 1] : v0[e + 1]);
+            const int k0 = hh * 32 + e;
+            const float p0 = (k0 <= lim) ? fast_exp2(fmaf(s0, sc, -m_used)) : 0.f;
+            const float p1 = (k0 + 1 <= lim) ? fast_exp2(fmaf(s1, sc, -m_used)) : 0.f;
+            l0 += p0;
+            l1 += p1;
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
+            pk[hh * 16 + e / 2] = *reinterpret_cast<uint32_t*>(&t2);
+          }
+        }
+        l += l0 + l1;
+        if (!pv_waited) {
+          mbar_wait(&pv_done[h], (j - 1) & 1);
+          tc_after();
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)
+          *reinterpret_cast<uint4*>(prow + (((uint32_t)q4 ^ sw) << 4)) =
+              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+        fence_async_smem();
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[h]);
+      }
+      // epilogue: O / l -> bf16 -> global
+      mbar_wait(&pv_done[h], (n_kt - 1) & 1);
+      tc_after();
+      const bool row_ok = q0 + r < qlen;
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      bf16* dst = p.o + (size_t)(row0 + q0 + r) * p.hq * DH + (size_t)(head_a + h) * DH;
+#pragma unroll 1
+      for (int c = 0; c < DH; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(T_O(h) + lane_base + c, v);
+        if (row_ok) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            float o8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o8[e] = __uint_as_float(v[q4 * 8 + e]) * inv;
+            store16<bf16>(dst + c + q4 * 8, o8);
+          }
         }
       }
     }
@@ -434,12 +449,13 @@ int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   }
   CUtensorMap mq;
   if (!fatc::make_map(&mq, a.q, (uint64_t)a.total_rows, (uint64_t)a.q_stride, (uint64_t)a.q_stride, 128)) return -1;
-  fatc::Params p{a.row0,  a.qlen, a.cpre,       a.seq_row,           a.table, a.max_pages,
-                 a.hq,    a.hkv,  0,            (bf16*)a.o,          (const bf16*)a.k_pool,
-                 (const bf16*)a.v_pool};
+  fatc::Params p{a.row0, a.qlen, a.cpre, a.seq_row, a.table, a.max_pages, a.hq, a.hkv, 0, 0,
+                 (bf16*)a.o, (const bf16*)a.k_pool, (const bf16*)a.v_pool};
+  const int G = a.hq / a.hkv;
   p.n_qtiles = (a.max_q + fatc::BQ - 1) / fatc::BQ;
-  dim3 grid(p.n_qtiles, a.hq, a.n_seqs);
-  fatc::fa_tc_kernel<<<grid, 320, fatc::SMEM, st>>>(mq, p);
+  p.n_pairs = a.hkv * ((G + 1) / 2);
+  dim3 grid(p.n_pairs, p.n_qtiles, a.n_seqs);
+  fatc::fa_tc_kernel<<<grid, fatc::THREADS, fatc::SMEM, st>>>(mq, p);
   return 1;
 }
 
