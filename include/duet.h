@@ -233,7 +233,8 @@ duet_status duet_last_step_times(duet_ctx* ctx, duet_step_times* out);
 
 /* Measures Pi_SM(S) and B_HBM(S) for S = every partition size the ctx can provision (both
  * sides of every split, and the full device) with the library's own kernels, the recipe of
- * a streaming-read kernel over a >= 1 GiB buffer and a bf16 GEMM.
+ * a streaming-read kernel over a >= 512 MiB buffer (8 KiB pages through a cp.async
+ * shared-memory ring, the decode side's memory pipeline) and an 8192^3 bf16 GEMM.
  * flops_at_sms / bw_at_sms: host arrays of total_sms+1 doubles; entries for sizes that
  * cannot be provisioned are filled by linear interpolation between measured neighbours.
  * Errors: INVALID_ARG, CUDA. */

@@ -965,7 +965,7 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
     std::vector<float> tb, tf;
     for (int rep = 0; rep < 7; ++rep) {
       CUDA_TRY(cudaEventRecord(e0, st));
-      launch_stream_read(buf, n_bytes, sink, sms, st);
+      launch_stream_pages(buf, n_bytes, sink, sms, st);
       CUDA_TRY(cudaEventRecord(e1, st));
       CUDA_TRY(cudaEventSynchronize(e1));
       float ms;

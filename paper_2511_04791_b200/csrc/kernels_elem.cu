@@ -213,4 +213,53 @@ int launch_stream_read(const void* buf, size_t n_bytes, unsigned long long* sink
   return 1;
 }
 
+// B_HBM(S) for the predictor: HBM read bandwidth achievable on S SMs by the memory pipeline
+// the decode side uses — 8 KiB "pages" (a 4 KiB K block + a 4 KiB V block) streamed with 16-B
+// cp.async into a 3-stage ring per warp, 4 warps per CTA, 2 CTAs per SM (kernels_decode_tc.cu).
+// (Plain LDG streaming from 2048 threads per SM reaches more per SM on a small partition, but no
+// kernel that stages operands in shared memory can; profiles/r01_probe_tma_bw.txt.)
+__global__ void __launch_bounds__(128, 2) stream_pages_kernel(const uint4* __restrict__ buf, size_t n_pages,
+                                                                unsigned long long* sink) {
+  constexpr int NST = 3, PAGE_VEC = 512;  // 8 KiB = 512 x 16 B
+  extern __shared__ uint4 ring[];         // [4 warps][NST][512]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint4* my = ring + warp * NST * PAGE_VEC;
+  const size_t nw = (size_t)gridDim.x * 4, first = (size_t)blockIdx.x * 4 + warp;
+  const size_t n_mine = first < n_pages ? (n_pages - first + nw - 1) / nw : 0;
+  auto issue = [&](size_t i) {
+    const uint4* src = buf + (first + i * nw) * PAGE_VEC;
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(my + (i % NST) * PAGE_VEC);
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + (k * 32 + lane) * 16), "l"(src + k * 32 + lane)
+                   : "memory");
+  };
+  for (int i = 0; i < NST - 1; ++i) {
+    if ((size_t)i < n_mine) issue(i);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  uint32_t acc = 0;
+  for (size_t i = 0; i < n_mine; ++i) {
+    if (i + NST - 1 < n_mine) issue(i + NST - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(NST - 1) : "memory");
+    __syncwarp();
+    const uint4 v = my[(i % NST) * PAGE_VEC + lane * 16];
+    acc ^= v.x ^ v.w;
+    __syncwarp();
+  }
+  if (acc == 0x9E3779B9u) sink[blockIdx.x] = acc;
+}
+
+int launch_stream_pages(const void* buf, size_t n_bytes, unsigned long long* sink, int num_sms, cudaStream_t st) {
+  constexpr int SMEM = 4 * 3 * 8192;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(stream_pages_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  stream_pages_kernel<<<num_sms * 2, 128, SMEM, st>>>((const uint4*)buf, n_bytes / 8192, sink);
+  return 1;
+}
+
 }  // namespace duet

@@ -8,10 +8,11 @@
 //   warp 1        TMEM allocator (all 512 columns) + tcgen05.mma issuer: for key tile j,
 //                 S_j^h = Q^h K_j^T for both heads (UMMA 128x64x16, K-major operands) into one of two
 //                 S buffers per head, then O^h += P_{j-1}^h V_{j-1} (A = P from smem, B = V MN-major)
-//   warps 2..5    softmax of head A, one thread per query row (= TMEM lane)
+//   warps 2..5    softmax of head A, one thread per query row (= TMEM lane); P goes to one of two smem
+//                 buffers per head, so tile j's softmax waits only for PV_{j-2}, never for PV_{j-1}
 //   warps 6..9    softmax of head B — each SM sub-partition runs one warp of each head, so the
 //                 exp/FMA work of one head overlaps the other's waits (and the MMAs)
-//   warps 10..13  K/V loaders: cp.async gathers of the scattered 4 KiB page blocks into a 4-stage ring
+//   warps 10..13  K/V loaders: cp.async gathers of the scattered 4 KiB page blocks into a 3-stage ring
 //                 (a TMA box costs its issuing thread ~0.25 us on B200 — profiles/r01_probe_tma_bw.txt —
 //                 and a page needs four); each thread's copies are tracked by the stage's mbarrier
 //                 (cp.async.mbarrier.arrive.noinc), so a tile is published the moment it lands
@@ -20,13 +21,16 @@
 // zero-filled (cp.async src-size 0) and masked.  An odd last head of a group runs alone (has_b = 0).
 #include <cuda.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "dev_common.cuh"
 #include "kernels.h"
 
 namespace duet {
 namespace fatc {
 
-constexpr int BQ = 128, BKV = 64, DH = 128, PAGE = 16, KV_STAGES = 4;
+constexpr int BQ = 128, BKV = 64, DH = 128, PAGE = 16, KV_STAGES = 3;
 constexpr int Q_SUB = BQ * 128;            // [128 rows][64 cols] SW128 sub-tile = 16 KiB
 constexpr int KV_SUB = BKV * 128;          // [64 rows][64 cols] = 8 KiB
 constexpr int Q_BYTES = 2 * Q_SUB;         // 32 KiB per head
@@ -35,9 +39,11 @@ constexpr int P_BYTES = BQ * BKV * 2;      // [128 rows][64 keys] = one SW128 su
 constexpr int OFF_Q = 0;                   // head A, head B
 constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
 constexpr int OFF_V = OFF_K + KV_STAGES * KV_BYTES;
-constexpr int OFF_P = OFF_V + KV_STAGES * KV_BYTES;  // head A, head B
-constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
-constexpr int SMEM = OFF_BAR + 256 + 1024;
+constexpr int OFF_P = OFF_V + KV_STAGES * KV_BYTES;  // [head][2 buffers]
+constexpr int OFF_BAR = OFF_P + 4 * P_BYTES;
+constexpr int OFF_TRACE = OFF_BAR + 256;   // DUET_FA_TRACE: per-tile clock stamps of CTA (0,0,0)
+constexpr int TRACE_EV = 10, TRACE_MAXJ = 32;
+constexpr int SMEM = OFF_TRACE + TRACE_EV * TRACE_MAXJ * 4 + 1024;
 constexpr int THREADS = 14 * 32;
 constexpr int TMEM_COLS = 512;             // per head: S0 (64) | S1 (64) | O (128)
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
@@ -109,6 +115,25 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100)
+__device__ __forceinline__ uint64_t pack_f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack_f2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
@@ -138,7 +163,7 @@ struct Params {
   const int* cpre;
   const int* seq_row;
   const int* table;
-  int max_pages, hq, hkv, n_qtiles, n_pairs;
+  int max_pages, hq, hkv, n_qtiles, n_pairs, trace;
   bf16* o;
   const bf16* k_pool;
   const bf16* v_pool;
@@ -149,13 +174,15 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bar = (uint64_t*)(smem + OFF_BAR);
   uint64_t* q_full = bar;                   // 1
-  uint64_t* kv_full = bar + 1;              // [KV_STAGES]
-  uint64_t* kv_empty = kv_full + KV_STAGES; // [KV_STAGES]
-  uint64_t* s_full = kv_empty + KV_STAGES;  // [head][2]
+  uint64_t* k_full = bar + 1;               // [KV_STAGES] K ring: freed by the S MMAs
+  uint64_t* k_empty = k_full + KV_STAGES;
+  uint64_t* v_full = k_empty + KV_STAGES;   // [KV_STAGES] V ring: freed by the PV MMAs
+  uint64_t* v_empty = v_full + KV_STAGES;
+  uint64_t* s_full = v_empty + KV_STAGES;   // [head][2]
   uint64_t* s_free = s_full + 4;            // [head][2]
-  uint64_t* p_full = s_free + 4;            // [head]
-  uint64_t* pv_done = p_full + 2;           // [head]
-  uint32_t* tmem_slot = (uint32_t*)(pv_done + 2);
+  uint64_t* p_full = s_free + 4;            // [head][P buffer]
+  uint64_t* pv_done = p_full + 4;           // [head][P buffer]: PV of the tile that used that buffer
+  uint32_t* tmem_slot = (uint32_t*)(pv_done + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = blockIdx.x;
@@ -179,14 +206,16 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
     for (int i = 0; i < KV_STAGES; ++i) {
-      mbar_init(&kv_full[i], 128);  // one cp.async-tracked (noinc) arrive per loader thread
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 64);  // one cp.async-tracked (noinc) arrive per loader thread of the tensor
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 64);
+      mbar_init(&v_empty[i], 1);
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 4);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
     }
@@ -202,6 +231,13 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   tc_after();
   const uint32_t tmem = *tmem_slot;
   // head h: S buffers at h*256 + {0, 64}, O at h*256 + 128
+  // timeline debugging (DUET_FA_TRACE=1): event e of tile j, clock() relative to kernel start
+  uint32_t* trace = (uint32_t*)(smem + OFF_TRACE);
+  const bool tr = p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  const uint32_t t_start = (uint32_t)clock();
+  auto stamp = [&](int e, int j) {
+    if (tr && lane == 0 && j < TRACE_MAXJ) trace[e * TRACE_MAXJ + j] = (uint32_t)clock() - t_start;
+  };
   auto T_S = [&](int h, int b) { return tmem + h * 256 + b * BKV; };
   auto T_O = [&](int h) { return tmem + h * 256 + 2 * BKV; };
 
@@ -215,77 +251,90 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
       }
     }
   } else if (warp >= 10) {
-    // ------------------------------------------------ K/V loaders (4 warps, cp.async, 4-stage ring)
-    const int lt = threadIdx.x - 10 * 32;  // 0..127
+    // ------------------------------------------------ loaders: warps 10-11 stream K, warps 12-13 stream V
+    // (separate rings: a K slot frees when the S MMAs of its tile complete, long before its V slot)
+    const int tensor = (warp - 10) >> 1;           // 0 = K, 1 = V
+    const int lt = threadIdx.x - (10 + 2 * tensor) * 32;  // 0..63
+    const bf16* pool = tensor ? p.v_pool : p.k_pool;
+    uint64_t* full = tensor ? v_full : k_full;
+    uint64_t* empty = tensor ? v_empty : k_empty;
+    const int off_ring = tensor ? OFF_V : OFF_K;
     const size_t page_stride = (size_t)p.hkv * PAGE * DH;
-    // chunk c = lt + 128 i (i < 8) of a [64 keys][16 chunks] tile: key = c / 16, 16-B column = c % 16
+    // chunk c = lt + 64 i (i < 16) of a [64 keys][16 chunks] tile: key = c / 16, 16-B column = c % 16
     for (int j = 0; j < n_kt; ++j) {
       const int st = j % KV_STAGES;
-      mbar_wait(&kv_empty[st], ((j / KV_STAGES) & 1) ^ 1);
-      const uint32_t kd = smem_u32(smem + OFF_K + st * KV_BYTES), vd = smem_u32(smem + OFF_V + st * KV_BYTES);
+      mbar_wait(&empty[st], ((j / KV_STAGES) & 1) ^ 1);
+      if (warp == 10) stamp(0, j);
+      const uint32_t dst = smem_u32(smem + off_ring + st * KV_BYTES);
 #pragma unroll
-      for (int i = 0; i < (BKV * 16) / 128; ++i) {
-        const int c = lt + i * 128;
+      for (int i = 0; i < (BKV * 16) / 64; ++i) {
+        const int c = lt + i * 64;
         const int rr = c >> 4, ch = c & 15;
         const int key = j * BKV + rr;
         const bool v = key < kv_end;
         const size_t off =
             v ? (size_t)tab[key / PAGE] * page_stride + ((size_t)kvh * PAGE + (key % PAGE)) * DH + ch * 8 : 0;
         const uint32_t so = (uint32_t)((ch >> 3) * KV_SUB + rr * 128 + (((ch & 7) ^ (rr & 7)) << 4));
-        const int sz = v ? 16 : 0;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(kd + so), "l"(p.k_pool + off), "r"(sz)
-                     : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(vd + so), "l"(p.v_pool + off), "r"(sz)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + so), "l"(pool + off), "r"(v ? 16 : 0)
                      : "memory");
       }
       // the barrier phase completes when every loader thread's copies of this tile have landed
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kv_full[st])) : "memory");
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[st])) : "memory");
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     constexpr uint32_t ID_S = idesc(BKV, false), ID_PV = idesc(DH, true);
     mbar_wait(q_full, 0);
-    for (int j = 0; j <= n_kt; ++j) {
-      if (j < n_kt) {
-        const int b = j & 1, st = j % KV_STAGES;
-        mbar_wait(&kv_full[st], (j / KV_STAGES) & 1);
-        fence_async_smem();  // the loaders' cp.async (generic proxy) writes -> visible to the MMA (async proxy)
-        tc_after();
-        const uint32_t sk = smem_u32(smem + OFF_K + st * KV_BYTES);
-        for (int h = 0; h < n_heads; ++h) {
-          if (j >= 2) {
-            mbar_wait(&s_free[h * 2 + b], ((j - 2) >> 1) & 1);
-            tc_after();
-          }
-          if (lane == 0) {
-            const uint32_t sq = smem_u32(smem + OFF_Q + h * Q_BYTES);
-#pragma unroll
-            for (int kk = 0; kk < DH / 16; ++kk)
-              umma(T_S(h, b), desc_k(sq + (kk >> 2) * Q_SUB + (kk & 3) * 32),
-                   desc_k(sk + (kk >> 2) * KV_SUB + (kk & 3) * 32), ID_S, kk > 0);
-            umma_commit(&s_full[h * 2 + b]);
-          }
-          __syncwarp();
-        }
-      }
-      if (j >= 1) {
-        const int jp = j - 1, st = jp % KV_STAGES;
-        const uint32_t sv = smem_u32(smem + OFF_V + st * KV_BYTES);
-        for (int h = 0; h < n_heads; ++h) {
-          mbar_wait(&p_full[h], jp & 1);
+    // S_j^h = Q^h K_j^T into S buffer j & 1 (free once softmax_{j-2}^h has loaded S_{j-2}^h)
+    auto issue_s = [&](int j) {
+      const int b = j & 1, st = j % KV_STAGES;
+      mbar_wait(&k_full[st], (j / KV_STAGES) & 1);
+      stamp(1, j);
+      fence_async_smem();  // the loaders' cp.async (generic proxy) writes -> visible to the MMA (async proxy)
+      tc_after();
+      const uint32_t sk = smem_u32(smem + OFF_K + st * KV_BYTES);
+      for (int h = 0; h < n_heads; ++h) {
+        if (j >= 2) {
+          mbar_wait(&s_free[h * 2 + b], ((j - 2) >> 1) & 1);
           tc_after();
-          if (lane == 0) {
-            const uint32_t spp = smem_u32(smem + OFF_P + h * P_BYTES);
-#pragma unroll
-            for (int kk = 0; kk < BKV / 16; ++kk)  // 16 keys per UMMA k-step
-              umma(T_O(h), desc_k(spp + kk * 32), desc_mn(sv + kk * 16 * 128), ID_PV, (jp > 0 || kk > 0));
-            umma_commit(&pv_done[h]);
-            if (h == n_heads - 1) umma_commit(&kv_empty[st]);
-          }
-          __syncwarp();
         }
+        if (lane == 0) {
+          const uint32_t sq = smem_u32(smem + OFF_Q + h * Q_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk)
+            umma(T_S(h, b), desc_k(sq + (kk >> 2) * Q_SUB + (kk & 3) * 32),
+                 desc_k(sk + (kk >> 2) * KV_SUB + (kk & 3) * 32), ID_S, kk > 0);
+          umma_commit(&s_full[h * 2 + b]);
+          if (h == n_heads - 1) umma_commit(&k_empty[st]);
+        }
+        __syncwarp();
       }
+      stamp(2, j);
+    };
+    // The S MMAs run two key tiles ahead of the PV MMAs: S_{j+2} is issued as soon as softmax_j has
+    // read S_j — never behind P_j — so softmax_{j+1} finds its scores ready when softmax_j ends.
+    for (int j = 0; j < 2 && j < n_kt; ++j) issue_s(j);
+    for (int j = 0; j < n_kt; ++j) {
+      if (j + 2 < n_kt) issue_s(j + 2);
+      const int st = j % KV_STAGES, pb = j & 1;
+      const uint32_t sv = smem_u32(smem + OFF_V + st * KV_BYTES);
+      mbar_wait(&v_full[st], (j / KV_STAGES) & 1);
+      fence_async_smem();
+      for (int h = 0; h < n_heads; ++h) {
+        mbar_wait(&p_full[h * 2 + pb], (j >> 1) & 1);
+        tc_after();
+        if (lane == 0) {
+          const uint32_t spp = smem_u32(smem + OFF_P + (h * 2 + pb) * P_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)  // 16 keys per UMMA k-step
+            umma(T_O(h), desc_k(spp + kk * 32), desc_mn(sv + kk * 16 * 128), ID_PV, (j > 0 || kk > 0));
+          umma_commit(&pv_done[h * 2 + pb]);
+          if (h == n_heads - 1) umma_commit(&v_empty[st]);
+        }
+        __syncwarp();
+      }
+      stamp(3, j);
     }
   } else {
     // ------------------------------------------------ softmax warps: one thread per query row
@@ -297,11 +346,12 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
       const float sc = rsqrtf((float)DH) * 1.4426950408889634f;
       const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
       const uint32_t sw = (uint32_t)(r & 7);
-      uint8_t* prow = smem + OFF_P + h * P_BYTES + r * 128;
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_kt; ++j) {
         const int b = j & 1;
         mbar_wait(&s_full[h * 2 + b], (j >> 1) & 1);
+        if (warp == 2) stamp(4, j);
+        if (warp == 6) stamp(7, j);
         tc_after();
         const int kbase = j * BKV;
         uint32_t v0[32], v1[32];
@@ -325,14 +375,12 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
           }
         }
         const float m_new = fmaxf(m_used, mx * sc);  // sc > 0: the max commutes with the scaling
-        // PV_{j-1} must be complete before O is rescaled or P is overwritten
-        bool pv_waited = j == 0;
+        // O is rescaled only after PV_{j-1} (and every earlier PV) completed
         const bool mine = m_new > m_used + RESCALE_THRESHOLD;
         if (__any_sync(0xffffffffu, mine)) {
           if (j >= 1) {
-            mbar_wait(&pv_done[h], (j - 1) & 1);
+            mbar_wait(&pv_done[h * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
             tc_after();
-            pv_waited = true;
             const float f = mine ? exp2f(m_used - m_new) : 1.f;
             l *= f;
 #pragma unroll 1
@@ -346,28 +394,52 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
           }
           if (mine) m_used = m_new;
         }
-        // exponentials into packed bf16 pairs (registers), then publish P once PV_{j-1} is done
+        // exponentials into packed bf16 pairs (registers), then publish P once PV_{j-1} is done.
+        // Fully visible tiles (all but the diagonal ones) take the unmasked path with packed
+        // f32x2 FMA / add: per key pair one FFMA2, two MUFU.EX2, one FADD2, one F2FP.
         uint32_t pk[32];
         float l0 = 0.f, l1 = 0.f;
+        if (lim >= BKV - 1) {
+          const uint64_t sc2 = pack_f2(sc, sc), nm2 = pack_f2(-m_used, -m_used);
+          uint64_t acc2 = pack_f2(0.f, 0.f);
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
+          for (int e = 0; e < 64; e += 2) {
+            const uint32_t* src = e < 32 ? v0 : v1;
+            const int ee = e & 31;
+            const uint64_t t2 = ffma2(pack_f2(__uint_as_float(src[ee]), __uint_as_float(src[ee + 1])), sc2, nm2);
+            float t0, t1;
+            unpack_f2(t2, t0, t1);
+            const float p0 = fast_exp2(t0), p1 = fast_exp2(t1);
+            acc2 = fadd2(acc2, pack_f2(p0, p1));
+            __nv_bfloat162 t = __floats2bfloat162_rn(p0, p1);
+            pk[e / 2] = *reinterpret_cast<uint32_t*>(&t);
+          }
+          unpack_f2(acc2, l0, l1);
+        } else {
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const float s0 = __uint_as_float(hh ? v1[e] : v0[e]), s1 = __uint_as_float(hh ? v1[e + 1] : v0[e + 1]);
-            const int k0 = hh * 32 + e;
-            const float p0 = (k0 <= lim) ? fast_exp2(fmaf(s0, sc, -m_used)) : 0.f;
-            const float p1 = (k0 + 1 <= lim) ? fast_exp2(fmaf(s1, sc, -m_used)) : 0.f;
-            l0 += p0;
-            l1 += p1;
-            __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
-            pk[hh * 16 + e / 2] = *reinterpret_cast<uint32_t*>(&t2);
+          for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const float s0 = __uint_as_float(hh ? v1[e] : v0[e]), s1 = __uint_as_float(hh ? v1[e + 1] : v0[e + 1]);
+              const int k0 = hh * 32 + e;
+              const float p0 = (k0 <= lim) ? fast_exp2(fmaf(s0, sc, -m_used)) : 0.f;
+              const float p1 = (k0 + 1 <= lim) ? fast_exp2(fmaf(s1, sc, -m_used)) : 0.f;
+              l0 += p0;
+              l1 += p1;
+              __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
+              pk[hh * 16 + e / 2] = *reinterpret_cast<uint32_t*>(&t2);
+            }
           }
         }
         l += l0 + l1;
-        if (!pv_waited) {
-          mbar_wait(&pv_done[h], (j - 1) & 1);
+        if (warp == 2) stamp(5, j);
+        if (warp == 6) stamp(8, j);
+        // P buffer j & 1 is free once PV_{j-2} has completed
+        if (j >= 2) {
+          mbar_wait(&pv_done[h * 2 + b], ((j - 2) >> 1) & 1);
           tc_after();
         }
+        uint8_t* prow = smem + OFF_P + (h * 2 + b) * P_BYTES + r * 128;
 #pragma unroll
         for (int q4 = 0; q4 < 8; ++q4)
           *reinterpret_cast<uint4*>(prow + (((uint32_t)q4 ^ sw) << 4)) =
@@ -375,10 +447,12 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
         fence_async_smem();
         tc_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[h]);
+        if (lane == 0) mbar_arrive(&p_full[h * 2 + b]);
+        if (warp == 2) stamp(6, j);
+        if (warp == 6) stamp(9, j);
       }
       // epilogue: O / l -> bf16 -> global
-      mbar_wait(&pv_done[h], (n_kt - 1) & 1);
+      mbar_wait(&pv_done[h * 2 + ((n_kt - 1) & 1)], ((n_kt - 1) >> 1) & 1);
       tc_after();
       const bool row_ok = q0 + r < qlen;
       const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -401,6 +475,13 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   }
   tc_before();
   __syncthreads();
+  if (tr && threadIdx.x == 0) {
+    printf("FA_TRACE n_kt=%d (clock cycles; ev: 0 load-issue 1 kv_full 2 S-issued 3 PV-issued 4 s_full 5 exps-done 6 P-published)\n", n_kt);
+    for (int j = 0; j < n_kt && j < TRACE_MAXJ; ++j)
+      printf("FA_TRACE j=%2d %8u %8u %8u %8u | A %8u %8u %8u | B %8u %8u %8u\n", j, trace[j], trace[TRACE_MAXJ + j],
+             trace[2 * TRACE_MAXJ + j], trace[3 * TRACE_MAXJ + j], trace[4 * TRACE_MAXJ + j], trace[5 * TRACE_MAXJ + j],
+             trace[6 * TRACE_MAXJ + j], trace[7 * TRACE_MAXJ + j], trace[8 * TRACE_MAXJ + j], trace[9 * TRACE_MAXJ + j]);
+  }
   if (warp == 1) {
     tc_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
@@ -449,11 +530,13 @@ int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   }
   CUtensorMap mq;
   if (!fatc::make_map(&mq, a.q, (uint64_t)a.total_rows, (uint64_t)a.q_stride, (uint64_t)a.q_stride, 128)) return -1;
-  fatc::Params p{a.row0, a.qlen, a.cpre, a.seq_row, a.table, a.max_pages, a.hq, a.hkv, 0, 0,
+  fatc::Params p{a.row0, a.qlen, a.cpre, a.seq_row, a.table, a.max_pages, a.hq, a.hkv, 0, 0, 0,
                  (bf16*)a.o, (const bf16*)a.k_pool, (const bf16*)a.v_pool};
   const int G = a.hq / a.hkv;
   p.n_qtiles = (a.max_q + fatc::BQ - 1) / fatc::BQ;
   p.n_pairs = a.hkv * ((G + 1) / 2);
+  static const bool trace = getenv("DUET_FA_TRACE") != nullptr;
+  p.trace = trace ? 1 : 0;
   dim3 grid(p.n_pairs, p.n_qtiles, a.n_seqs);
   fatc::fa_tc_kernel<<<grid, fatc::THREADS, fatc::SMEM, st>>>(mq, p);
   return 1;
