@@ -6,13 +6,16 @@
 // gathered once for two 128x64 score tiles; keys stream in 64-key tiles (4 pages of 16 tokens).
 //   warp 0        Q tiles by TMA (2 heads x two 64-column SWIZZLE_128B boxes)
 //   warp 1        TMEM allocator (all 512 columns) + tcgen05.mma issuer: for key tile j,
-//                 S_j^h = Q^h K_j^T for both heads (UMMA 128x64x16, K-major operands) into one of two
-//                 S buffers per head, then O^h += P_{j-1}^h V_{j-1} (A = P from smem, B = V MN-major)
-//   warps 2..5    softmax of head A, one thread per query row (= TMEM lane); P goes to one of two smem
-//                 buffers per head, so tile j's softmax waits only for PV_{j-2}, never for PV_{j-1}
+//                 S_j^h = Q^h K_j^T for both heads (UMMA 128x64x16, K-major smem operands) into one of
+//                 two TMEM buffers per head, issued one tile ahead of the softmax; then
+//                 O^h += P_j^h V_j with A = P_j read straight from TMEM (the softmax overwrites S_j with
+//                 its bf16 probabilities in place) and B = V (smem, MN-major)
+//   warps 2..5    softmax of head A, one thread per query row (= TMEM lane): tcgen05.ld S_j, max,
+//                 exp2, tcgen05.st P_j — no shared-memory round trip, no proxy fence
 //   warps 6..9    softmax of head B — each SM sub-partition runs one warp of each head, so the
 //                 exp/FMA work of one head overlaps the other's waits (and the MMAs)
-//   warps 10..13  K/V loaders: cp.async gathers of the scattered 4 KiB page blocks into a 3-stage ring
+//   warps 10..13  K/V loaders (2 warps per tensor): cp.async gathers of the scattered 4 KiB page blocks
+//                 into separate 5-stage K and V rings
 //                 (a TMA box costs its issuing thread ~0.25 us on B200 — profiles/r01_probe_tma_bw.txt —
 //                 and a page needs four); each thread's copies are tracked by the stage's mbarrier
 //                 (cp.async.mbarrier.arrive.noinc), so a tile is published the moment it lands
@@ -30,22 +33,20 @@
 namespace duet {
 namespace fatc {
 
-constexpr int BQ = 128, BKV = 64, DH = 128, PAGE = 16, KV_STAGES = 3;
+constexpr int BQ = 128, BKV = 64, DH = 128, PAGE = 16, KV_STAGES = 5;
 constexpr int Q_SUB = BQ * 128;            // [128 rows][64 cols] SW128 sub-tile = 16 KiB
 constexpr int KV_SUB = BKV * 128;          // [64 rows][64 cols] = 8 KiB
 constexpr int Q_BYTES = 2 * Q_SUB;         // 32 KiB per head
 constexpr int KV_BYTES = 2 * KV_SUB;       // 16 KiB per tensor per stage
-constexpr int P_BYTES = BQ * BKV * 2;      // [128 rows][64 keys] = one SW128 sub-tile, 16 KiB per head
 constexpr int OFF_Q = 0;                   // head A, head B
 constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
 constexpr int OFF_V = OFF_K + KV_STAGES * KV_BYTES;
-constexpr int OFF_P = OFF_V + KV_STAGES * KV_BYTES;  // [head][2 buffers]
-constexpr int OFF_BAR = OFF_P + 4 * P_BYTES;
-constexpr int OFF_TRACE = OFF_BAR + 256;   // DUET_FA_TRACE: per-tile clock stamps of CTA (0,0,0)
+constexpr int OFF_BAR = OFF_V + KV_STAGES * KV_BYTES;
+constexpr int OFF_TRACE = OFF_BAR + 384;   // DUET_FA_TRACE: per-tile clock stamps of CTA (0,0,0)
 constexpr int TRACE_EV = 10, TRACE_MAXJ = 32;
 constexpr int SMEM = OFF_TRACE + TRACE_EV * TRACE_MAXJ * 4 + 1024;
 constexpr int THREADS = 14 * 32;
-constexpr int TMEM_COLS = 512;             // per head: S0 (64) | S1 (64) | O (128)
+constexpr int TMEM_COLS = 512;             // per head: S/P buffer 0 (64) | S/P buffer 1 (64) | O (128)
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 static_assert(SMEM <= 227 * 1024, "smem");
 
@@ -100,6 +101,16 @@ __device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+// D (TMEM) += A (TMEM, row = lane, bf16 pairs along columns) . B (smem descriptor)
+__device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -178,10 +189,9 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   uint64_t* k_empty = k_full + KV_STAGES;
   uint64_t* v_full = k_empty + KV_STAGES;   // [KV_STAGES] V ring: freed by the PV MMAs
   uint64_t* v_empty = v_full + KV_STAGES;
-  uint64_t* s_full = v_empty + KV_STAGES;   // [head][2]
-  uint64_t* s_free = s_full + 4;            // [head][2]
-  uint64_t* p_full = s_free + 4;            // [head][P buffer]
-  uint64_t* pv_done = p_full + 4;           // [head][P buffer]: PV of the tile that used that buffer
+  uint64_t* s_full = v_empty + KV_STAGES;   // [head][buffer]
+  uint64_t* p_full = s_full + 4;            // [head][buffer]
+  uint64_t* pv_done = p_full + 4;           // [head][buffer]: PV of the tile that used that buffer
   uint32_t* tmem_slot = (uint32_t*)(pv_done + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -213,9 +223,6 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
-    }
-    for (int i = 0; i < 4; ++i) {
       mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
     }
@@ -230,7 +237,6 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tmem_slot;
-  // head h: S buffers at h*256 + {0, 64}, O at h*256 + 128
   // timeline debugging (DUET_FA_TRACE=1): event e of tile j, clock() relative to kernel start
   uint32_t* trace = (uint32_t*)(smem + OFF_TRACE);
   const bool tr = p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
@@ -238,6 +244,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   auto stamp = [&](int e, int j) {
     if (tr && lane == 0 && j < TRACE_MAXJ) trace[e * TRACE_MAXJ + j] = (uint32_t)clock() - t_start;
   };
+  // head h, buffer b: S_j (fp32, 64 columns); P_j (bf16 pairs) overwrites its first 32 columns
   auto T_S = [&](int h, int b) { return tmem + h * 256 + b * BKV; };
   auto T_O = [&](int h) { return tmem + h * 256 + 2 * BKV; };
 
@@ -284,52 +291,47 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
+    // tcgen05.mma from one thread executes in issue order, so S_{j+2} (written into the TMEM buffer that
+    // holds P_j) may be issued as soon as PV_j (which reads P_j) has been issued.
     constexpr uint32_t ID_S = idesc(BKV, false), ID_PV = idesc(DH, true);
     mbar_wait(q_full, 0);
-    // S_j^h = Q^h K_j^T into S buffer j & 1 (free once softmax_{j-2}^h has loaded S_{j-2}^h)
     auto issue_s = [&](int j) {
       const int b = j & 1, st = j % KV_STAGES;
       mbar_wait(&k_full[st], (j / KV_STAGES) & 1);
       stamp(1, j);
       fence_async_smem();  // the loaders' cp.async (generic proxy) writes -> visible to the MMA (async proxy)
       tc_after();
-      const uint32_t sk = smem_u32(smem + OFF_K + st * KV_BYTES);
-      for (int h = 0; h < n_heads; ++h) {
-        if (j >= 2) {
-          mbar_wait(&s_free[h * 2 + b], ((j - 2) >> 1) & 1);
-          tc_after();
-        }
-        if (lane == 0) {
+      if (lane == 0) {
+        const uint32_t sk = smem_u32(smem + OFF_K + st * KV_BYTES);
+        for (int h = 0; h < n_heads; ++h) {
           const uint32_t sq = smem_u32(smem + OFF_Q + h * Q_BYTES);
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk)
             umma(T_S(h, b), desc_k(sq + (kk >> 2) * Q_SUB + (kk & 3) * 32),
                  desc_k(sk + (kk >> 2) * KV_SUB + (kk & 3) * 32), ID_S, kk > 0);
           umma_commit(&s_full[h * 2 + b]);
-          if (h == n_heads - 1) umma_commit(&k_empty[st]);
         }
-        __syncwarp();
+        umma_commit(&k_empty[st]);
       }
+      __syncwarp();
       stamp(2, j);
     };
-    // The S MMAs run two key tiles ahead of the PV MMAs: S_{j+2} is issued as soon as softmax_j has
-    // read S_j — never behind P_j — so softmax_{j+1} finds its scores ready when softmax_j ends.
-    for (int j = 0; j < 2 && j < n_kt; ++j) issue_s(j);
+    issue_s(0);
     for (int j = 0; j < n_kt; ++j) {
-      if (j + 2 < n_kt) issue_s(j + 2);
-      const int st = j % KV_STAGES, pb = j & 1;
-      const uint32_t sv = smem_u32(smem + OFF_V + st * KV_BYTES);
+      // S_{j+1} goes to buffer (j+1)&1, last read by PV_{j-1} (issued in the previous iteration)
+      if (j + 1 < n_kt) issue_s(j + 1);
+      const int st = j % KV_STAGES, b = j & 1;
       mbar_wait(&v_full[st], (j / KV_STAGES) & 1);
       fence_async_smem();
+      const uint32_t sv = smem_u32(smem + OFF_V + st * KV_BYTES);
       for (int h = 0; h < n_heads; ++h) {
-        mbar_wait(&p_full[h * 2 + pb], (j >> 1) & 1);
+        mbar_wait(&p_full[h * 2 + b], (j >> 1) & 1);
         tc_after();
         if (lane == 0) {
-          const uint32_t spp = smem_u32(smem + OFF_P + (h * 2 + pb) * P_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk)  // 16 keys per UMMA k-step
-            umma(T_O(h), desc_k(spp + kk * 32), desc_mn(sv + kk * 16 * 128), ID_PV, (j > 0 || kk > 0));
-          umma_commit(&pv_done[h * 2 + pb]);
+          for (int kk = 0; kk < BKV / 16; ++kk)  // 16 keys per UMMA k-step: A = P (TMEM, 8 columns), B = V
+            umma_ts(T_O(h), T_S(h, b) + kk * 8, desc_mn(sv + kk * 16 * 128), ID_PV, (j > 0 || kk > 0));
+          umma_commit(&pv_done[h * 2 + b]);
           if (h == n_heads - 1) umma_commit(&v_empty[st]);
         }
         __syncwarp();
@@ -345,7 +347,6 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
       const int pos = min(cpre + q0 + r, kv_end - 1);          // clamp rows past the chunk
       const float sc = rsqrtf((float)DH) * 1.4426950408889634f;
       const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-      const uint32_t sw = (uint32_t)(r & 7);
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_kt; ++j) {
         const int b = j & 1;
@@ -357,9 +358,6 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
         uint32_t v0[32], v1[32];
         tmem_ld32(T_S(h, b) + lane_base, v0);
         tmem_ld32(T_S(h, b) + lane_base + 32, v1);
-        tc_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[h * 2 + b]);  // S buffer b may be overwritten by S_{j+2}
         const int lim = pos - kbase;  // keys 0..lim of this tile are visible to this row
         float mx = -INFINITY;
         if (lim >= BKV - 1) {
@@ -394,9 +392,8 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
           }
           if (mine) m_used = m_new;
         }
-        // exponentials into packed bf16 pairs (registers), then publish P once PV_{j-1} is done.
-        // Fully visible tiles (all but the diagonal ones) take the unmasked path with packed
-        // f32x2 FMA / add: per key pair one FFMA2, two MUFU.EX2, one FADD2, one F2FP.
+        // exponentials -> packed bf16 pairs.  Fully visible tiles (all but the diagonal ones) take the
+        // unmasked path with packed f32x2 FMA / add: per key pair one FFMA2, two MUFU.EX2, one FADD2, one F2FP.
         uint32_t pk[32];
         float l0 = 0.f, l1 = 0.f;
         if (lim >= BKV - 1) {
@@ -434,17 +431,8 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
         l += l0 + l1;
         if (warp == 2) stamp(5, j);
         if (warp == 6) stamp(8, j);
-        // P buffer j & 1 is free once PV_{j-2} has completed
-        if (j >= 2) {
-          mbar_wait(&pv_done[h * 2 + b], ((j - 2) >> 1) & 1);
-          tc_after();
-        }
-        uint8_t* prow = smem + OFF_P + (h * 2 + b) * P_BYTES + r * 128;
-#pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4)
-          *reinterpret_cast<uint4*>(prow + (((uint32_t)q4 ^ sw) << 4)) =
-              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
-        fence_async_smem();
+        // P_j -> TMEM (the first 32 columns of S_j's buffer), the A operand of PV_j
+        tmem_st32(T_S(h, b) + lane_base, pk);
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[h * 2 + b]);
