@@ -3,22 +3,22 @@
 // Chunked prefill (§4.1; readings #2, #6, #7): a chunk of q tokens at positions
 // c..c+q-1 attends to its c-token prefix and to itself causally.  One CTA = the same 128 query rows
 // of TWO query heads of one GQA group (reading #6: they read the same kv head), so every K/V tile is
-// gathered once for two 128x64 score tiles; keys stream in 64-key tiles (4 pages of 16 tokens).
+// gathered once for two score tiles; keys stream in 128-key tiles (8 pages of 16 tokens), so the
+// score MMA is 128x128x16 (an N = 64 UMMA reads 6 KiB of operands for half the work and runs at ~44%
+// of the tensor rate, N = 128 at ~88%: profiles/r01_probe_umma_rate.txt).
 //   warp 0        Q tiles by TMA (2 heads x two 64-column SWIZZLE_128B boxes)
-//   warp 1        TMEM allocator (all 512 columns) + tcgen05.mma issuer: for key tile j,
-//                 S_j^h = Q^h K_j^T for both heads (UMMA 128x64x16, K-major smem operands) into one of
-//                 two TMEM buffers per head, issued one tile ahead of the softmax; then
-//                 O^h += P_j^h V_j with A = P_j read straight from TMEM (the softmax overwrites S_j with
-//                 its bf16 probabilities in place) and B = V (smem, MN-major)
-//   warps 2..5    softmax of head A, one thread per query row (= TMEM lane): tcgen05.ld S_j, max,
-//                 exp2, tcgen05.st P_j — no shared-memory round trip, no proxy fence
-//   warps 6..9    softmax of head B — each SM sub-partition runs one warp of each head, so the
-//                 exp/FMA work of one head overlaps the other's waits (and the MMAs)
-//   warps 10..13  K/V loaders (2 warps per tensor): cp.async gathers of the scattered 4 KiB page blocks
-//                 into separate 5-stage K and V rings
-//                 (a TMA box costs its issuing thread ~0.25 us on B200 — profiles/r01_probe_tma_bw.txt —
-//                 and a page needs four); each thread's copies are tracked by the stage's mbarrier
-//                 (cp.async.mbarrier.arrive.noinc), so a tile is published the moment it lands
+//   warp 1        TMEM allocator (all 512 columns: per head S_j/P_j 128 | O 128) + tcgen05.mma issuer,
+//                 per head: PV_j (A = P_j straight from TMEM, B = V from smem, MN-major), then
+//                 S_{j+1} = Q K_{j+1}^T over the same TMEM columns (MMAs execute in issue order)
+//   warps 2..5    softmax of head A, one thread per query row (= TMEM lane): two passes over the 128
+//                 S columns (max, then exp2 -> bf16 P written in place with tcgen05.st) — no
+//                 shared-memory round trip, no proxy fence
+//   warps 6..9    softmax of head B — each SM sub-partition runs one warp of each head, so one head's
+//                 exp work overlaps the other head's MMAs
+//   warps 10..13  loaders (2 warps per tensor): cp.async gathers of the scattered 4 KiB page blocks
+//                 into a 2-stage K ring and a 3-stage V ring, each thread's copies tracked by the stage
+//                 mbarrier (cp.async.mbarrier.arrive.noinc); a TMA box costs its issuing thread
+//                 ~0.25 us on B200 (profiles/r01_probe_tma_bw.txt) and a page would need four
 // The running max is re-based (O rescaled in TMEM) only when it grows by more than 2^8; the decision is
 // taken per warp because tcgen05.ld/st are warp-collective.  Keys past the causal end of a tile are
 // zero-filled (cp.async src-size 0) and masked.  An odd last head of a group runs alone (has_b = 0).
@@ -33,20 +33,20 @@
 namespace duet {
 namespace fatc {
 
-constexpr int BQ = 128, BKV = 64, DH = 128, PAGE = 16, KV_STAGES = 5;
+constexpr int BQ = 128, BKV = 128, DH = 128, PAGE = 16, K_STAGES = 2, V_STAGES = 3;
 constexpr int Q_SUB = BQ * 128;            // [128 rows][64 cols] SW128 sub-tile = 16 KiB
-constexpr int KV_SUB = BKV * 128;          // [64 rows][64 cols] = 8 KiB
+constexpr int KV_SUB = BKV * 128;          // [128 keys][64 cols] = 16 KiB
 constexpr int Q_BYTES = 2 * Q_SUB;         // 32 KiB per head
-constexpr int KV_BYTES = 2 * KV_SUB;       // 16 KiB per tensor per stage
+constexpr int KV_BYTES = 2 * KV_SUB;       // 32 KiB per tensor per stage
 constexpr int OFF_Q = 0;                   // head A, head B
 constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
-constexpr int OFF_V = OFF_K + KV_STAGES * KV_BYTES;
-constexpr int OFF_BAR = OFF_V + KV_STAGES * KV_BYTES;
-constexpr int OFF_TRACE = OFF_BAR + 384;   // DUET_FA_TRACE: per-tile clock stamps of CTA (0,0,0)
-constexpr int TRACE_EV = 10, TRACE_MAXJ = 32;
+constexpr int OFF_V = OFF_K + K_STAGES * KV_BYTES;
+constexpr int OFF_BAR = OFF_V + V_STAGES * KV_BYTES;
+constexpr int OFF_TRACE = OFF_BAR + 256;   // DUET_FA_TRACE: per-tile clock stamps of CTA (0,0,0)
+constexpr int TRACE_EV = 10, TRACE_MAXJ = 16;
 constexpr int SMEM = OFF_TRACE + TRACE_EV * TRACE_MAXJ * 4 + 1024;
 constexpr int THREADS = 14 * 32;
-constexpr int TMEM_COLS = 512;             // per head: S/P buffer 0 (64) | S/P buffer 1 (64) | O (128)
+constexpr int TMEM_COLS = 512;             // per head: S_j / P_j (128) | O (128)
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 static_assert(SMEM <= 227 * 1024, "smem");
 
@@ -185,14 +185,14 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bar = (uint64_t*)(smem + OFF_BAR);
   uint64_t* q_full = bar;                   // 1
-  uint64_t* k_full = bar + 1;               // [KV_STAGES] K ring: freed by the S MMAs
-  uint64_t* k_empty = k_full + KV_STAGES;
-  uint64_t* v_full = k_empty + KV_STAGES;   // [KV_STAGES] V ring: freed by the PV MMAs
-  uint64_t* v_empty = v_full + KV_STAGES;
-  uint64_t* s_full = v_empty + KV_STAGES;   // [head][buffer]
-  uint64_t* p_full = s_full + 4;            // [head][buffer]
-  uint64_t* pv_done = p_full + 4;           // [head][buffer]: PV of the tile that used that buffer
-  uint32_t* tmem_slot = (uint32_t*)(pv_done + 4);
+  uint64_t* k_full = bar + 1;               // [K_STAGES] K ring: freed by the S MMAs
+  uint64_t* k_empty = k_full + K_STAGES;
+  uint64_t* v_full = k_empty + K_STAGES;    // [V_STAGES] V ring: freed by the PV MMAs
+  uint64_t* v_empty = v_full + V_STAGES;
+  uint64_t* s_full = v_empty + V_STAGES;    // [head]
+  uint64_t* p_full = s_full + 2;            // [head]
+  uint64_t* o_done = p_full + 2;            // [head]: the last PV
+  uint32_t* tmem_slot = (uint32_t*)(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = blockIdx.x;
@@ -215,16 +215,18 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < KV_STAGES; ++i) {
+    for (int i = 0; i < K_STAGES; ++i) {
       mbar_init(&k_full[i], 64);  // one cp.async-tracked (noinc) arrive per loader thread of the tensor
       mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < V_STAGES; ++i) {
       mbar_init(&v_full[i], 64);
       mbar_init(&v_empty[i], 1);
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
-      mbar_init(&pv_done[i], 1);
+      mbar_init(&o_done[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -244,9 +246,9 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   auto stamp = [&](int e, int j) {
     if (tr && lane == 0 && j < TRACE_MAXJ) trace[e * TRACE_MAXJ + j] = (uint32_t)clock() - t_start;
   };
-  // head h, buffer b: S_j (fp32, 64 columns); P_j (bf16 pairs) overwrites its first 32 columns
-  auto T_S = [&](int h, int b) { return tmem + h * 256 + b * BKV; };
-  auto T_O = [&](int h) { return tmem + h * 256 + 2 * BKV; };
+  // head h: S_j (fp32, 128 columns), overwritten in place by P_j (bf16 pairs, columns 0..63); O
+  auto T_S = [&](int h) { return tmem + h * 256; };
+  auto T_O = [&](int h) { return tmem + h * 256 + BKV; };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -266,14 +268,15 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
     uint64_t* full = tensor ? v_full : k_full;
     uint64_t* empty = tensor ? v_empty : k_empty;
     const int off_ring = tensor ? OFF_V : OFF_K;
+    const int nst = tensor ? V_STAGES : K_STAGES;
     const size_t page_stride = (size_t)p.hkv * PAGE * DH;
-    // chunk c = lt + 64 i (i < 16) of a [64 keys][16 chunks] tile: key = c / 16, 16-B column = c % 16
+    // chunk c = lt + 64 i (i < 32) of a [128 keys][16 chunks] tile: key = c / 16, 16-B column = c % 16
     for (int j = 0; j < n_kt; ++j) {
-      const int st = j % KV_STAGES;
-      mbar_wait(&empty[st], ((j / KV_STAGES) & 1) ^ 1);
+      const int st = j % nst;
+      mbar_wait(&empty[st], ((j / nst) & 1) ^ 1);
       if (warp == 10) stamp(0, j);
       const uint32_t dst = smem_u32(smem + off_ring + st * KV_BYTES);
-#pragma unroll
+#pragma unroll 8
       for (int i = 0; i < (BKV * 16) / 64; ++i) {
         const int c = lt + i * 64;
         const int rr = c >> 4, ch = c & 15;
@@ -291,52 +294,54 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    // tcgen05.mma from one thread executes in issue order, so S_{j+2} (written into the TMEM buffer that
-    // holds P_j) may be issued as soon as PV_j (which reads P_j) has been issued.
+    // tcgen05.mma from one thread executes in issue order: S_{j+1}^h (written over P_j^h) is issued right
+    // after PV_j^h (which reads P_j^h), and a commit tracks every earlier MMA, so s_full also
+    // certifies that PV_{j-1} has completed.
     constexpr uint32_t ID_S = idesc(BKV, false), ID_PV = idesc(DH, true);
     mbar_wait(q_full, 0);
-    auto issue_s = [&](int j) {
-      const int b = j & 1, st = j % KV_STAGES;
-      mbar_wait(&k_full[st], (j / KV_STAGES) & 1);
+    auto wait_k = [&](int j) {
+      mbar_wait(&k_full[j % K_STAGES], (j / K_STAGES) & 1);
       stamp(1, j);
       fence_async_smem();  // the loaders' cp.async (generic proxy) writes -> visible to the MMA (async proxy)
       tc_after();
+    };
+    auto issue_s = [&](int j, int h) {  // S_j^h = Q^h K_j^T
       if (lane == 0) {
-        const uint32_t sk = smem_u32(smem + OFF_K + st * KV_BYTES);
-        for (int h = 0; h < n_heads; ++h) {
-          const uint32_t sq = smem_u32(smem + OFF_Q + h * Q_BYTES);
+        const uint32_t sk = smem_u32(smem + OFF_K + (j % K_STAGES) * KV_BYTES);
+        const uint32_t sq = smem_u32(smem + OFF_Q + h * Q_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk)
-            umma(T_S(h, b), desc_k(sq + (kk >> 2) * Q_SUB + (kk & 3) * 32),
-                 desc_k(sk + (kk >> 2) * KV_SUB + (kk & 3) * 32), ID_S, kk > 0);
-          umma_commit(&s_full[h * 2 + b]);
-        }
-        umma_commit(&k_empty[st]);
+        for (int kk = 0; kk < DH / 16; ++kk)
+          umma(T_S(h), desc_k(sq + (kk >> 2) * Q_SUB + (kk & 3) * 32), desc_k(sk + (kk >> 2) * KV_SUB + (kk & 3) * 32),
+               ID_S, kk > 0);
+        umma_commit(&s_full[h]);
+        if (h == n_heads - 1) umma_commit(&k_empty[j % K_STAGES]);
       }
       __syncwarp();
-      stamp(2, j);
     };
-    issue_s(0);
+    wait_k(0);
+    for (int h = 0; h < n_heads; ++h) issue_s(0, h);
+    stamp(2, 0);
     for (int j = 0; j < n_kt; ++j) {
-      // S_{j+1} goes to buffer (j+1)&1, last read by PV_{j-1} (issued in the previous iteration)
-      if (j + 1 < n_kt) issue_s(j + 1);
-      const int st = j % KV_STAGES, b = j & 1;
-      mbar_wait(&v_full[st], (j / KV_STAGES) & 1);
+      const int st = j % V_STAGES;
+      mbar_wait(&v_full[st], (j / V_STAGES) & 1);
       fence_async_smem();
       const uint32_t sv = smem_u32(smem + OFF_V + st * KV_BYTES);
+      if (j + 1 < n_kt) wait_k(j + 1);
       for (int h = 0; h < n_heads; ++h) {
-        mbar_wait(&p_full[h * 2 + b], (j >> 1) & 1);
+        mbar_wait(&p_full[h], j & 1);
         tc_after();
         if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk)  // 16 keys per UMMA k-step: A = P (TMEM, 8 columns), B = V
-            umma_ts(T_O(h), T_S(h, b) + kk * 8, desc_mn(sv + kk * 16 * 128), ID_PV, (j > 0 || kk > 0));
-          umma_commit(&pv_done[h * 2 + b]);
+            umma_ts(T_O(h), T_S(h) + kk * 8, desc_mn(sv + kk * 16 * 128), ID_PV, (j > 0 || kk > 0));
+          if (j == n_kt - 1) umma_commit(&o_done[h]);
           if (h == n_heads - 1) umma_commit(&v_empty[st]);
         }
         __syncwarp();
+        if (j + 1 < n_kt) issue_s(j + 1, h);
       }
       stamp(3, j);
+      if (j + 1 < n_kt) stamp(2, j + 1);
     }
   } else {
     // ------------------------------------------------ softmax warps: one thread per query row
@@ -347,38 +352,40 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
       const int pos = min(cpre + q0 + r, kv_end - 1);          // clamp rows past the chunk
       const float sc = rsqrtf((float)DH) * 1.4426950408889634f;
       const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+      const uint32_t t_s = T_S(h) + lane_base;
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_kt; ++j) {
-        const int b = j & 1;
-        mbar_wait(&s_full[h * 2 + b], (j >> 1) & 1);
+        mbar_wait(&s_full[h], j & 1);
         if (warp == 2) stamp(4, j);
         if (warp == 6) stamp(7, j);
         tc_after();
-        const int kbase = j * BKV;
-        uint32_t v0[32], v1[32];
-        tmem_ld32(T_S(h, b) + lane_base, v0);
-        tmem_ld32(T_S(h, b) + lane_base + 32, v1);
-        const int lim = pos - kbase;  // keys 0..lim of this tile are visible to this row
+        const int lim = pos - j * BKV;  // keys 0..lim of this tile are visible to this row
+        const bool full_tile = lim >= BKV - 1;
+        // pass 1: row max over the visible keys (two 64-column halves)
         float mx = -INFINITY;
-        if (lim >= BKV - 1) {
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v0[32], v1[32];
+          tmem_ld32(t_s + c * 64, v0);
+          tmem_ld32(t_s + c * 64 + 32, v1);
+          if (full_tile) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 2)
-            mx = fmaxf(mx, fmaxf(fmaxf(__uint_as_float(v0[e]), __uint_as_float(v0[e + 1])),
-                                 fmaxf(__uint_as_float(v1[e]), __uint_as_float(v1[e + 1]))));
-        } else {
+            for (int e = 0; e < 32; e += 2)
+              mx = fmaxf(mx, fmaxf(fmaxf(__uint_as_float(v0[e]), __uint_as_float(v0[e + 1])),
+                                   fmaxf(__uint_as_float(v1[e]), __uint_as_float(v1[e + 1]))));
+          } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            if (e <= lim) mx = fmaxf(mx, __uint_as_float(v0[e]));
-            if (32 + e <= lim) mx = fmaxf(mx, __uint_as_float(v1[e]));
+            for (int e = 0; e < 32; ++e) {
+              if (c * 64 + e <= lim) mx = fmaxf(mx, __uint_as_float(v0[e]));
+              if (c * 64 + 32 + e <= lim) mx = fmaxf(mx, __uint_as_float(v1[e]));
+            }
           }
         }
         const float m_new = fmaxf(m_used, mx * sc);  // sc > 0: the max commutes with the scaling
-        // O is rescaled only after PV_{j-1} (and every earlier PV) completed
+        // re-base when the max grew by more than 2^8; PV_{j-1} is complete (s_full tracks it)
         const bool mine = m_new > m_used + RESCALE_THRESHOLD;
         if (__any_sync(0xffffffffu, mine)) {
           if (j >= 1) {
-            mbar_wait(&pv_done[h * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
-            tc_after();
             const float f = mine ? exp2f(m_used - m_new) : 1.f;
             l *= f;
 #pragma unroll 1
@@ -392,55 +399,61 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
           }
           if (mine) m_used = m_new;
         }
-        // exponentials -> packed bf16 pairs.  Fully visible tiles (all but the diagonal ones) take the
-        // unmasked path with packed f32x2 FMA / add: per key pair one FFMA2, two MUFU.EX2, one FADD2, one F2FP.
-        uint32_t pk[32];
+        // pass 2: exponentials -> bf16 pairs -> TMEM columns 32c..32c+31 (over S columns already read)
         float l0 = 0.f, l1 = 0.f;
-        if (lim >= BKV - 1) {
-          const uint64_t sc2 = pack_f2(sc, sc), nm2 = pack_f2(-m_used, -m_used);
-          uint64_t acc2 = pack_f2(0.f, 0.f);
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v0[32], v1[32], pk[32];
+          tmem_ld32(t_s + c * 64, v0);
+          tmem_ld32(t_s + c * 64 + 32, v1);
+          if (full_tile) {
+            const uint64_t sc2 = pack_f2(sc, sc), nm2 = pack_f2(-m_used, -m_used);
+            uint64_t acc2 = pack_f2(0.f, 0.f);
 #pragma unroll
-          for (int e = 0; e < 64; e += 2) {
-            const uint32_t* src = e < 32 ? v0 : v1;
-            const int ee = e & 31;
-            const uint64_t t2 = ffma2(pack_f2(__uint_as_float(src[ee]), __uint_as_float(src[ee + 1])), sc2, nm2);
-            float t0, t1;
-            unpack_f2(t2, t0, t1);
-            const float p0 = fast_exp2(t0), p1 = fast_exp2(t1);
-            acc2 = fadd2(acc2, pack_f2(p0, p1));
-            __nv_bfloat162 t = __floats2bfloat162_rn(p0, p1);
-            pk[e / 2] = *reinterpret_cast<uint32_t*>(&t);
-          }
-          unpack_f2(acc2, l0, l1);
-        } else {
+            for (int e = 0; e < 64; e += 2) {
+              const uint32_t* src = e < 32 ? v0 : v1;
+              const int ee = e & 31;
+              const uint64_t t2 = ffma2(pack_f2(__uint_as_float(src[ee]), __uint_as_float(src[ee + 1])), sc2, nm2);
+              float t0, t1;
+              unpack_f2(t2, t0, t1);
+              const float p0 = fast_exp2(t0), p1 = fast_exp2(t1);
+              acc2 = fadd2(acc2, pack_f2(p0, p1));
+              __nv_bfloat162 t = __floats2bfloat162_rn(p0, p1);
+              pk[e / 2] = *reinterpret_cast<uint32_t*>(&t);
+            }
+            float a0, a1;
+            unpack_f2(acc2, a0, a1);
+            l0 += a0;
+            l1 += a1;
+          } else {
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
+            for (int hh = 0; hh < 2; ++hh) {
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              const float s0 = __uint_as_float(hh ? v1[e] : v0[e]), s1 = __uint_as_float(hh ? v1[e + 1] : v0[e + 1]);
-              const int k0 = hh * 32 + e;
-              const float p0 = (k0 <= lim) ? fast_exp2(fmaf(s0, sc, -m_used)) : 0.f;
-              const float p1 = (k0 + 1 <= lim) ? fast_exp2(fmaf(s1, sc, -m_used)) : 0.f;
-              l0 += p0;
-              l1 += p1;
-              __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
-              pk[hh * 16 + e / 2] = *reinterpret_cast<uint32_t*>(&t2);
+              for (int e = 0; e < 32; e += 2) {
+                const float s0 = __uint_as_float(hh ? v1[e] : v0[e]), s1 = __uint_as_float(hh ? v1[e + 1] : v0[e + 1]);
+                const int k0 = c * 64 + hh * 32 + e;
+                const float p0 = (k0 <= lim) ? fast_exp2(fmaf(s0, sc, -m_used)) : 0.f;
+                const float p1 = (k0 + 1 <= lim) ? fast_exp2(fmaf(s1, sc, -m_used)) : 0.f;
+                l0 += p0;
+                l1 += p1;
+                __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
+                pk[hh * 16 + e / 2] = *reinterpret_cast<uint32_t*>(&t2);
+              }
             }
           }
+          tmem_st32(t_s + c * 32, pk);
         }
         l += l0 + l1;
         if (warp == 2) stamp(5, j);
         if (warp == 6) stamp(8, j);
-        // P_j -> TMEM (the first 32 columns of S_j's buffer), the A operand of PV_j
-        tmem_st32(T_S(h, b) + lane_base, pk);
         tc_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[h * 2 + b]);
+        if (lane == 0) mbar_arrive(&p_full[h]);
         if (warp == 2) stamp(6, j);
         if (warp == 6) stamp(9, j);
       }
       // epilogue: O / l -> bf16 -> global
-      mbar_wait(&pv_done[h * 2 + ((n_kt - 1) & 1)], ((n_kt - 1) >> 1) & 1);
+      mbar_wait(&o_done[h], 0);
       tc_after();
       const bool row_ok = q0 + r < qlen;
       const float inv = l > 0.f ? 1.f / l : 0.f;
