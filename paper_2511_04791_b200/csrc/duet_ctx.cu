@@ -959,13 +959,67 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
+  // B_HBM(S) is the bandwidth the library's memory-bound hot kernel achieves on S SMs: paged decode
+  // attention (bf16) over a synthetic batch whose K/V pools fill the buffer (64 requests, identity page
+  // tables), else (fp32 contexts) an 8 KiB-page cp.async streaming kernel.
+  const auto& sp = c->spec;
+  const int n_req = std::min(64, c->dec.part_rows);
+  const size_t page_bytes = (size_t)sp.n_kv_heads * kPageSize * sp.head_dim * es;  // one page, all kv heads
+  const int pages_per_req = (int)std::min<size_t>((n_bytes / 2) / page_bytes / std::max(n_req, 1), 4096);
+  DecodeAttnArgs da{};
+  int* d_meta = nullptr;
+  void *dq = nullptr, *dout = nullptr;
+  double attn_bytes = 0;
+  bool use_attn = c->dt == DT::BF16 && n_req > 0 && pages_per_req >= 8;
+  if (use_attn) {
+    std::vector<int> meta((size_t)n_req * (pages_per_req + 2));
+    int* h_pos = meta.data();
+    int* h_tok = h_pos + n_req;
+    int* h_tab = h_tok + n_req;
+    const int len = pages_per_req * kPageSize;
+    for (int r = 0; r < n_req; ++r) {
+      h_pos[r] = len - 1;
+      h_tok[r] = r;
+      for (int j = 0; j < pages_per_req; ++j) h_tab[(size_t)r * pages_per_req + j] = r * pages_per_req + j;
+    }
+    CUDA_TRY(cudaMalloc(&d_meta, meta.size() * sizeof(int)));
+    CUDA_TRY(cudaMemcpy(d_meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMalloc(&dq, (size_t)n_req * sp.n_q_heads * sp.head_dim * es));
+    CUDA_TRY(cudaMemset(dq, 0, (size_t)n_req * sp.n_q_heads * sp.head_dim * es));
+    CUDA_TRY(cudaMalloc(&dout, (size_t)n_req * sp.n_q_heads * sp.head_dim * es));
+    da.q = dq;
+    da.q_stride = sp.n_q_heads * sp.head_dim;
+    da.o = dout;
+    da.n = n_req;
+    da.hq = sp.n_q_heads;
+    da.hkv = sp.n_kv_heads;
+    da.dh = sp.head_dim;
+    da.pos = d_meta;
+    da.tok_row = d_meta + n_req;
+    da.table = d_meta + 2 * n_req;
+    da.max_pages = pages_per_req;
+    da.page_size = kPageSize;
+    da.k_pool = buf;
+    da.v_pool = (const char*)buf + (size_t)n_req * pages_per_req * page_bytes;
+    da.part_o = c->dec.part_o;
+    da.part_ml = c->dec.part_ml;
+    da.max_splits = kMaxSplits;
+    da.max_len = len;
+    da.n_pages = n_req * pages_per_req;
+    attn_bytes = 2.0 * (double)n_req * pages_per_req * page_bytes;
+  }
   std::vector<double> mf(c->total_sms + 1, 0.0), mb(c->total_sms + 1, 0.0);
   auto measure = [&](cudaStream_t st, int sms) -> duet_status {
     if (mf[sms] > 0) return DUET_OK;
     std::vector<float> tb, tf;
     for (int rep = 0; rep < 7; ++rep) {
       CUDA_TRY(cudaEventRecord(e0, st));
-      launch_stream_pages(buf, n_bytes, sink, sms, st);
+      if (use_attn) {
+        da.num_sms = sms;
+        launch_decode_attn(c->dt, da, st);
+      } else {
+        launch_stream_pages(buf, n_bytes, sink, sms, st);
+      }
       CUDA_TRY(cudaEventRecord(e1, st));
       CUDA_TRY(cudaEventSynchronize(e1));
       float ms;
@@ -986,7 +1040,7 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
     DUET_TRY(check_launch("calibration"));
     std::sort(tb.begin(), tb.end());
     std::sort(tf.begin(), tf.end());
-    mb[sms] = (double)n_bytes / (tb[tb.size() / 2] * 1e-3);
+    mb[sms] = (use_attn ? attn_bytes : (double)n_bytes) / (tb[tb.size() / 2] * 1e-3);
     mf[sms] = 2.0 * G * (double)G * G / (tf[tf.size() / 2] * 1e-3);
     return DUET_OK;
   };
@@ -998,6 +1052,9 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(buf);
+  if (d_meta) cudaFree(d_meta);
+  if (dq) cudaFree(dq);
+  if (dout) cudaFree(dout);
   cudaFree(sink);
   cudaFree(A);
   cudaFree(B);
