@@ -245,12 +245,16 @@ duet_status duet_calibrate(duet_ctx* ctx, double* flops_at_sms, double* bw_at_sm
  * launching stream around every kernel it launches outside CUDA graphs (the prefill side of a
  * spatial step and every kernel of a temporal step), per kernel class, together with the
  * algorithmic FLOPs and bytes of each launch (causal attention FLOPs,
- * weights/activations read once).  duet_profile_enable(ctx, 1) resets the counters;
- * duet_profile_read synchronizes on the recorded events and returns DUET_KCLASS_N entries. */
+ * weights/activations read once).  duet_profile_enable(ctx, mask) resets the counters and times the
+ * classes whose bit (1 << DUET_KCLASS_*) is set in mask (0 = off; DUET_PROFILE_ALL = every class);
+ * each timed launch costs two event records on its stream (~1 us), so a timed region usually enables
+ * only the class it reports.  duet_profile_read synchronizes on the recorded events and returns
+ * DUET_KCLASS_N entries. */
 enum { DUET_KCLASS_GEMM = 0, DUET_KCLASS_PREFILL_ATTN = 1, DUET_KCLASS_DECODE_ATTN = 2, DUET_KCLASS_OTHER = 3,
        DUET_KCLASS_N = 4 };
+#define DUET_PROFILE_ALL 0xF
 typedef struct { int32_t launches; double seconds, flops, bytes; } duet_kernel_stats;
-duet_status duet_profile_enable(duet_ctx* ctx, int32_t enable);
+duet_status duet_profile_enable(duet_ctx* ctx, int32_t class_mask);
 duet_status duet_profile_read(duet_ctx* ctx, duet_kernel_stats* out);
 
 /* ----------------------------------------------------------------- single operators

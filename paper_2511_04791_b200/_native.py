@@ -78,6 +78,7 @@ class duet_kv_pages(C.Structure):
 
 
 DUET_KCLASS_N = 4
+DUET_PROFILE_ALL = 0xF
 
 
 class duet_kernel_stats(C.Structure):
@@ -269,8 +270,10 @@ class Ctx:
         _check(lib().duet_last_step_times(self.h, C.byref(out)))
         return {n: getattr(out, n) for n, _ in duet_step_times._fields_}
 
-    def profile_enable(self, on: bool = True):
-        _check(lib().duet_profile_enable(self.h, int(on)))
+    def profile_enable(self, on=True):
+        """on: False/0 = off, True = every kernel class, or a bitmask of 1 << DUET_KCLASS_*."""
+        mask = DUET_PROFILE_ALL if on is True else int(on)
+        _check(lib().duet_profile_enable(self.h, mask))
 
     def profile_read(self) -> dict:
         arr = (duet_kernel_stats * DUET_KCLASS_N)()

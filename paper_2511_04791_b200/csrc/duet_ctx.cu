@@ -149,6 +149,7 @@ struct duet_ctx {
   bool last_has_dec = false, last_has_pre = false;
   // live kernel timing
   bool prof_on = false, capturing = false;
+  int prof_mask = 0;
   struct ProfRec {
     int cls, idx;
     double flops, bytes;
@@ -159,8 +160,8 @@ struct duet_ctx {
   duet_kernel_stats prof_acc[DUET_KCLASS_N] = {};
 };
 
-static int prof_begin(duet_ctx* c, cudaStream_t st) {
-  if (!c->prof_on || c->capturing) return -1;
+static int prof_begin(duet_ctx* c, cudaStream_t st, int cls) {
+  if (!c->prof_on || c->capturing || !(c->prof_mask & (1 << cls))) return -1;
   if (c->prof_used == c->prof_pool.size()) {
     cudaEvent_t a, b;
     if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return -1;
@@ -292,7 +293,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
   static const bool dbg_sync = getenv("DUET_DEBUG_SYNC") != nullptr;
 #define TIMED(cls, fl, by, call)                                                                  \
   do {                                                                                            \
-    const int pi_ = prof_begin(c, st);                                                            \
+    const int pi_ = prof_begin(c, st, cls);                                                       \
     nk += (call);                                                                                 \
     prof_end(c, st, pi_, cls, fl, by);                                                            \
     if (dbg_sync && !c->capturing) {                                                              \
@@ -343,7 +344,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       pa.max_len = ap.max_len_pre;
       pa.n_pages = kv->n_pages;
       pa.total_rows = n_rows;
-      const int pi = prof_begin(c, st);
+      const int pi = prof_begin(c, st, DUET_KCLASS_PREFILL_ATTN);
       const int r = launch_prefill_attn(dt, pa, st);
       if (r < 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "prefill attention: unsupported head layout");
       prof_end(c, st, pi, DUET_KCLASS_PREFILL_ATTN, ap.attn_flops_pre, ap.attn_bytes_pre);
@@ -375,7 +376,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       da.num_sms = num_sms;
       da.max_len = ((ap.max_len_dec + 1023) / 1024) * 1024;  // same bucket in both modes
       da.n_pages = kv->n_pages;
-      const int pi = prof_begin(c, st);
+      const int pi = prof_begin(c, st, DUET_KCLASS_DECODE_ATTN);
       const int r = launch_decode_attn(dt, da, st);
       if (r < 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "decode attention: unsupported head layout");
       prof_end(c, st, pi, DUET_KCLASS_DECODE_ATTN, ap.attn_flops_dec, ap.attn_bytes_dec);
@@ -1090,10 +1091,11 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
 
 // ---------------------------------------------------------------------------------- live timing
 
-extern "C" duet_status duet_profile_enable(duet_ctx* c, int32_t enable) {
+extern "C" duet_status duet_profile_enable(duet_ctx* c, int32_t class_mask) {
   clear_error();
   if (!c) DUET_FAIL(DUET_ERR_INVALID_ARG, "ctx is NULL");
-  c->prof_on = enable != 0;
+  c->prof_on = (class_mask & DUET_PROFILE_ALL) != 0;
+  c->prof_mask = class_mask & DUET_PROFILE_ALL;
   c->prof_pending.clear();
   c->prof_used = 0;
   for (auto& s : c->prof_acc) s = duet_kernel_stats{};
