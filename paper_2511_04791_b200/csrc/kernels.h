@@ -41,6 +41,9 @@ int launch_gemm(DT dt, const GemmArgs& a, int num_sms, cudaStream_t st);
 int launch_gemm_simt(DT dt, const GemmArgs& a, cudaStream_t st);
 int launch_gemm_tc(const GemmArgs& a, int num_sms, cudaStream_t st);
 bool gemm_tc_supported(const GemmArgs& a);
+// CTA-pair (cta_group::2) 256x256 tiles for M > 128 on partitions of >= 2 SMs (kernels_gemm2.cu)
+bool gemm2_supported(const GemmArgs& a, int num_sms);
+int launch_gemm2(const GemmArgs& a, int num_sms, cudaStream_t st);
 
 // ---------------------------------------------------------------- RMSNorm
 // h[n][d] = x * rsqrt(mean(x^2) + eps) * g     (reading #1)

@@ -1,0 +1,373 @@
+// CTA-pair (cta_group::2) tcgen05 GEMM for the token-major linear operators of the layer when the
+// batch has more than 128 rows (prefill chunks, temporal mode): QKV, O, gate-up + SwiGLU, down
+// (§2, §4.1).  C[M][N] = epi(X[M][K] . W[N][K]^T), bf16 in, fp32 in TMEM.
+//
+// Two CTAs of a cluster (one TPC) compute a 256-row x 256-column tile with UMMA 256x256x16:
+//   * each CTA TMA-loads its own 128 rows of X and its own 128 rows of W (for SwiGLU: CTA 0 the gate
+//     rows, CTA 1 the matching up rows) into the same shared-memory offsets; both loads signal the
+//     leader CTA's `full` mbarrier (.cta_group::2 TMA);
+//   * the leader's single MMA thread issues tcgen05.mma.cta_group::2, which reads A from both CTAs'
+//     shared memory (M halves) and B from both (N halves) and writes each CTA's 128 rows x 256
+//     columns of fp32 into that CTA's TMEM; tcgen05.commit ... multicast::cluster frees the stage in
+//     both CTAs and publishes the accumulator to both epilogues;
+//   * each CTA's 4 epilogue warps drain their own TMEM rows and signal the leader's `tempty`.
+// Per SM this halves the shared-memory operand traffic of the 1-CTA 128x256 tile (each UMMA reads
+// 16 KiB per SM instead of 24 KiB per 128x256x16, and TMA writes 32 instead of 48 KiB per k-block),
+// the limit of the 1-CTA kernel (profiles/r01_probe_umma_rate.txt, profiles/r01_ncu_full_cfg2.md).
+// Tiles are assigned statically, every output is reduced over K in one fixed order.
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "dev_common.cuh"
+#include "kernels.h"
+
+namespace duet {
+namespace tc2 {
+
+constexpr int BM = 128, BK = 64, PAIR_M = 256, BN_PAIR = 256;
+constexpr int A_BYTES = BM * BK * 2;      // this CTA's 128 rows of X
+constexpr int B_BYTES = 128 * BK * 2;     // this CTA's 128 rows of W
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int STAGES = 6;
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int THREADS = 192;
+constexpr int TMEM_COLS = 512;            // two 256-column accumulators
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA box into this CTA's shared memory, completion bytes counted on the leader CTA's mbarrier
+__device__ __forceinline__ void tma_load_2cta(const CUtensorMap* map, uint32_t leader_bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) |
+         ((uint64_t)2 << 61);
+}
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                      uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// arrive on the mbarrier at this offset in both CTAs once every earlier MMA of the pair completed
+__device__ __forceinline__ void commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct Params {
+  int M, N, K;
+  int num_m2, num_n, num_tiles;
+  bf16* C;
+  const bf16* R;
+  const bf16* bias;
+  int ldc, ldr;
+  int n_up_off;  // SwiGLU: row offset of the up rows in W (= N)
+};
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, Params p) {
+  constexpr int OUT_COLS = EPI == EPI_SWIGLU ? 128 : 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int num_k = p.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);   // leader: its producer's expect_tx (bytes of both CTAs)
+      mbar_init(&empty[i], 1);  // both: the leader's multicast commit
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);  // leader: 4 local + 4 peer epilogue warps
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers initialised and TMEM allocated in both CTAs before any remote access
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs): own X rows and own W rows; leader's `full` counts both
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = pair; t < p.num_tiles; t += n_pairs) {
+        const int mp = t % p.num_m2, nb = t / p.num_m2;
+        const int row_x = mp * PAIR_M + (int)rank * BM;
+        const int row_w = EPI == EPI_SWIGLU ? (rank ? p.n_up_off : 0) + nb * 128 : nb * BN_PAIR + (int)rank * 128;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t lbar = mapa(smem_u32(&full[s]), 0);
+          if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+          tma_load_2cta(&map_x, lbar, sA + s * A_BYTES, kb * BK, row_x);
+          tma_load_2cta(&map_w, lbar, sB + s * B_BYTES, kb * BK, row_w);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ---------------- MMA issuer (leader only): UMMA 256 x 256 x 16 over the CTA pair
+      constexpr uint32_t idesc = idesc_bf16(PAIR_M, BN_PAIR);
+      int s = 0;
+      uint32_t ph = 0;
+      int i = 0;
+      for (int t = pair; t < p.num_tiles; t += n_pairs, ++i) {
+        const int acc = i & 1;
+        mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN_PAIR;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma2(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (kb | k) != 0);
+          commit_both(&empty[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        commit_both(&tfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5 (both CTAs): this CTA's 128 rows, TMEM quadrant = warp % 4
+    const int quad = warp & 3;
+    const int lane_row = quad * 32 + lane;
+    const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
+    int i = 0;
+    for (int t = pair; t < p.num_tiles; t += n_pairs, ++i) {
+      const int acc = i & 1;
+      const int mp = t % p.num_m2, nb = t / p.num_m2;
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN_PAIR;
+      const int row = mp * PAIR_M + (int)rank * BM + lane_row;
+      const int n0 = nb * OUT_COLS;
+#pragma unroll 1
+      for (int c = 0; c < OUT_COLS; c += 32) {
+        float v[32];
+        tmem_ld32(tbase + c, v);
+        if constexpr (EPI == EPI_SWIGLU) {
+          float u[32];
+          tmem_ld32(tbase + 128 + c, u);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = silu_f(v[e]) * u[e];
+        }
+        if (row < p.M && n0 + c < p.N) {
+          bf16* dst = p.C + (size_t)row * p.ldc + n0 + c;
+          if (n0 + c + 32 <= p.N) {
+            if constexpr (EPI == EPI_RESIDUAL) {
+              const bf16* rsrc = p.R + (size_t)row * p.ldr + n0 + c;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                float rf[8];
+                load16<bf16>(rsrc + q * 8, rf);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[q * 8 + e] += rf[e];
+              }
+            } else if constexpr (EPI == EPI_STORE) {
+              if (p.bias) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  float bf[8];
+                  load16<bf16>(p.bias + n0 + c + q * 8, bf);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) v[q * 8 + e] += bf[e];
+                }
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float o8[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) o8[e] = v[q * 8 + e];
+              store16<bf16>(dst + q * 8, o8);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              if (n0 + c + e >= p.N) continue;
+              float o = v[e];
+              if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)row * p.ldr + n0 + c + e]);
+              if constexpr (EPI == EPI_STORE)
+                if (p.bias) o += __bfloat162float(p.bias[n0 + c + e]);
+              dst[e] = __float2bfloat16_rn(o);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty0 + acc * 8);  // the leader's tempty[acc]
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // no CTA leaves while its peer may still signal its barriers or read its smem
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  }
+  return fn;
+}
+static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int EPI>
+static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm2_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  CUtensorMap mx, mw;
+  const int w_rows = EPI == EPI_SWIGLU ? 2 * a.N : a.N;
+  if (!make_map(&mx, a.A, a.M, a.K, a.lda, BM) || !make_map(&mw, a.B, w_rows, a.K, a.ldb, 128)) return -1;
+  Params p{};
+  p.M = a.M;
+  p.N = a.N;
+  p.K = a.K;
+  p.num_m2 = (a.M + PAIR_M - 1) / PAIR_M;
+  p.num_n = (a.N + (EPI == EPI_SWIGLU ? 128 : 256) - 1) / (EPI == EPI_SWIGLU ? 128 : 256);
+  p.num_tiles = p.num_m2 * p.num_n;
+  p.C = (bf16*)a.C;
+  p.R = (const bf16*)a.R;
+  p.bias = (const bf16*)a.bias;
+  p.ldc = a.ldc;
+  p.ldr = a.ldr;
+  p.n_up_off = a.N;
+  const int pairs = p.num_tiles < num_sms / 2 ? p.num_tiles : num_sms / 2;
+  gemm2_kernel<EPI><<<2 * pairs, THREADS, SMEM, st>>>(mx, mw, p);
+  return 1;
+}
+
+}  // namespace tc2
+
+bool gemm2_supported(const GemmArgs& a, int num_sms) {
+  static const bool on = !getenv("DUET_GEMM2") || atoi(getenv("DUET_GEMM2")) != 0;  // A/B switch
+  return on && a.M > 128 && num_sms >= 2 && a.K % tc2::BK == 0 && a.lda % 8 == 0 && a.ldb % 8 == 0 &&
+         a.ldc % 8 == 0 && (!a.R || a.ldr % 8 == 0) && (a.epi != EPI_SWIGLU || a.N % 128 == 0);
+}
+
+int launch_gemm2(const GemmArgs& a, int num_sms, cudaStream_t st) {
+  if (a.epi == EPI_SWIGLU) return tc2::launch<EPI_SWIGLU>(a, num_sms, st);
+  if (a.epi == EPI_RESIDUAL) return tc2::launch<EPI_RESIDUAL>(a, num_sms, st);
+  return tc2::launch<EPI_STORE>(a, num_sms, st);
+}
+
+}  // namespace duet

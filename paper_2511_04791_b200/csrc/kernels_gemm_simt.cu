@@ -87,6 +87,10 @@ int launch_gemm_simt(DT dt, const GemmArgs& a, cudaStream_t st) {
 
 // Dispatcher: bf16 shapes the tcgen05 kernel tiles go there; everything else is SIMT.
 int launch_gemm(DT dt, const GemmArgs& a, int num_sms, cudaStream_t st) {
+  if (dt == DT::BF16 && gemm2_supported(a, num_sms)) {
+    const int r = launch_gemm2(a, num_sms, st);
+    if (r > 0) return r;
+  }
   if (dt == DT::BF16 && gemm_tc_supported(a)) return launch_gemm_tc(a, num_sms, st);
   return launch_gemm_simt(dt, a, st);
 }
