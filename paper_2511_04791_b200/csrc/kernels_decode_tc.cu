@@ -394,10 +394,19 @@ int launch_decode_tc(const DecodeAttnArgs& a, int pps, int n_splits, cudaStream_
   CUtensorMap mk, mv;
   const uint64_t rows = (uint64_t)a.n_pages * a.hkv * dtc::PAGE;
   if (!dtc::pool_map(&mk, a.k_pool, rows) || !dtc::pool_map(&mv, a.v_pool, rows)) return -1;
-  // variant (A/B measurements): DUET_DECODE = tma8x3 | cp4x6 | cp8x3 | cp4x3x2 (2 CTAs/SM)
+  // variant (A/B measurements, tools/gpu/run_dec_ab.sh): DUET_DECODE = cp4x2 | cp4x3x2 | cp3x3 | cp2x3 |
+  // tma8x3 | cp4x6 | cp8x3.  (A two-pages-per-iteration variant with 4-6 warps per SM was measured
+  // 20-40 % slower on 8-48 SM partitions: warps hide the latency better than ILP.)
   static const char* v = getenv("DUET_DECODE");
-  const char* sel = v ? v : "cp4x3x2";
-  if (!strcmp(sel, "tma8x3")) launch_variant<8, 3, true>(mk, mv, a, pps, n_splits, st);
+  // Default: 4 warps per CTA with the per-warp ring depth chosen by the partition size — 2 stages
+  // (3 CTAs = 12 warps per SM) on small partitions, where the kernel is latency-bound and warps hide
+  // it best, 3 stages (2 CTAs per SM) on the full GPU.  Page -> warp assignment and the merge order
+  // depend only on the 4 warps, so both give bitwise-identical results.
+  const char* sel = v ? v : (a.num_sms < 120 ? "cp4x2" : "cp4x3x2");
+  if (!strcmp(sel, "cp4x2")) launch_variant<4, 2, false>(mk, mv, a, pps, n_splits, st);   // 3 CTAs/SM
+  else if (!strcmp(sel, "cp3x3")) launch_variant<3, 3, false>(mk, mv, a, pps, n_splits, st);   // 3 CTAs/SM
+  else if (!strcmp(sel, "cp2x3")) launch_variant<2, 3, false>(mk, mv, a, pps, n_splits, st);   // 4 CTAs/SM
+  else if (!strcmp(sel, "tma8x3")) launch_variant<8, 3, true>(mk, mv, a, pps, n_splits, st);
   else if (!strcmp(sel, "cp8x3")) launch_variant<8, 3, false>(mk, mv, a, pps, n_splits, st);
   else if (!strcmp(sel, "cp4x6")) launch_variant<4, 6, false>(mk, mv, a, pps, n_splits, st);
   else if (!strcmp(sel, "cp2x4x3")) launch_variant<2, 4, false>(mk, mv, a, pps, n_splits, st);

@@ -211,10 +211,11 @@ def test_page_table_errors_are_caught_before_launch():
 @pytest.mark.parametrize("M,N,K,epi", [(1, 256, 256, 0), (130, 384, 512, 1), (257, 160, 1024, 2),
                                        (2048, 6144, 4096, 0), (64, 4096, 14336, 1), (64, 14336, 4096, 2),
                                        (100, 512, 256, 2), (8, 768, 256, 3), (77, 6144, 4096, 3),
-                                       (300, 1000, 512, 3), (128, 200, 128, 1)])
+                                       (300, 1000, 512, 3), (128, 200, 128, 1), (600, 768, 2048, 1),
+                                       (520, 256, 1024, 2), (2112, 4096, 4096, 1)])
 def test_op_gemm_bf16(M, N, K, epi):
-    """tcgen05 GEMM vs float64 torch: normal tiles (M > 128) and swap-AB tiles (M <= 128), every
-    epilogue (3 = store + bias), ragged M / N."""
+    """tcgen05 GEMM vs float64 torch: CTA-pair 256x256 tiles (M > 128), swap-AB tiles with shape-only
+    split-K (M <= 128), every epilogue (3 = store + bias), ragged M / N, M spanning several CTA pairs."""
     torch.manual_seed(0)
     cfg = configs.get_config("cfg2")
     wl = workload.build(cfg, pre_seqs=[(16, 0)], dec_ctx=[], k=1, with_weights=False)
