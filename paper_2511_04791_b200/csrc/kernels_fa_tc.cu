@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   const uint32_t tmem = *tmem_slot;
   // timeline debugging (DUET_FA_TRACE=1): event e of tile j, clock() relative to kernel start
   uint32_t* trace = (uint32_t*)(smem + OFF_TRACE);
-  const bool tr = p.trace == 1 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  const bool tr = (p.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
   const uint32_t t_start = (uint32_t)clock();
   auto stamp = [&](int e, int j) {
     if (tr && lane == 0 && j < TRACE_MAXJ) trace[e * TRACE_MAXJ + j] = (uint32_t)clock() - t_start;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
       mbar_wait(&empty[st], ((j / nst) & 1) ^ 1);
       if (warp == 10) stamp(0, j);
       const uint32_t dst = smem_u32(smem + off_ring + st * KV_BYTES) + so0;
-      if (p.trace == 2) {  // timing experiment only (DUET_FA_TRACE=noload): no K/V traffic, garbage result
+      if (p.trace & 2) {  // timing experiment only (DUET_FA_TRACE=noload): no K/V traffic, garbage result
         mbar_arrive(&full[st]);
         continue;
       }
@@ -551,7 +551,9 @@ int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   p.n_qtiles = (a.max_q + fatc::BQ - 1) / fatc::BQ;
   p.n_pairs = a.hkv * ((G + 1) / 2);
   static const char* trace = getenv("DUET_FA_TRACE");
-  p.trace = trace ? (trace[0] == 'n' ? 2 : 1) : 0;
+  // DUET_FA_TRACE: any value prints the timeline of CTA (0,0,0); "noload" skips the K/V loads instead
+  // (timing experiment, garbage output); "tn" does both
+  p.trace = trace ? (trace[0] == 'n' ? 2 : (trace[0] == 't' && trace[1] == 'n' ? 3 : 1)) : 0;
   dim3 grid(p.n_pairs, p.n_qtiles, a.n_seqs);
   fatc::fa_tc_kernel<<<grid, fatc::THREADS, fatc::SMEM, st>>>(mq, p);
   return 1;
