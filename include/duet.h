@@ -235,7 +235,8 @@ duet_status duet_last_step_times(duet_ctx* ctx, duet_step_times* out);
  * sides of every split, and the full device) with the library's own kernels, the recipe of
  * B_HBM(S) is the HBM bandwidth the library's memory-bound hot kernel (paged decode
  * attention, bf16; 64 requests whose K/V pages fill a >= 512 MiB buffer) achieves on S SMs — fp32
- * contexts use an 8 KiB-page cp.async streaming kernel — and Pi_SM(S) is an 8192^3 GEMM's rate.
+ * contexts use an 8 KiB-page cp.async streaming kernel — and Pi_SM(S) is the rate of a GEMM with the
+ * model's gate-up shape (M = max_prefill_tokens clamped to 256..8192, N = 2 ffn_dim, K = d_model).
  * flops_at_sms / bw_at_sms: host arrays of total_sms+1 doubles; entries for sizes that
  * cannot be provisioned are filled by linear interpolation between measured neighbours.
  * Errors: INVALID_ARG, CUDA. */

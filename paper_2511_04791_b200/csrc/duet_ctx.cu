@@ -949,14 +949,17 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
   CUDA_TRY(cudaMalloc(&buf, n_bytes));
   CUDA_TRY(cudaMemset(buf, 1, n_bytes));
   CUDA_TRY(cudaMalloc(&sink, 4096 * sizeof(unsigned long long)));
-  const int G = 8192;
+  // Pi_SM(S): the achievable rate of the model's largest linear operator ("gemm
+  // microbenchmark"): gate-up shape, M = the prefill chunk capacity (256..8192 rows), N = 2 m, K = d
+  const int GM = std::max(256, std::min(8192, ((c->lim.max_prefill_tokens + 255) / 256) * 256));
+  const int GN = ((2 * c->spec.ffn_dim + 255) / 256) * 256, GK = ((c->spec.d_model + 63) / 64) * 64;
   const size_t es = dt_size(c->dt);
   void *A = nullptr, *B = nullptr, *C = nullptr;
-  CUDA_TRY(cudaMalloc(&A, (size_t)G * G * es));
-  CUDA_TRY(cudaMalloc(&B, (size_t)G * G * es));
-  CUDA_TRY(cudaMalloc(&C, (size_t)G * G * es));
-  CUDA_TRY(cudaMemset(A, 0, (size_t)G * G * es));
-  CUDA_TRY(cudaMemset(B, 0, (size_t)G * G * es));
+  CUDA_TRY(cudaMalloc(&A, (size_t)GM * GK * es));
+  CUDA_TRY(cudaMalloc(&B, (size_t)GN * GK * es));
+  CUDA_TRY(cudaMalloc(&C, (size_t)GM * GN * es));
+  CUDA_TRY(cudaMemset(A, 0, (size_t)GM * GK * es));
+  CUDA_TRY(cudaMemset(B, 0, (size_t)GN * GK * es));
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
@@ -1027,7 +1030,7 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
       CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
       tb.push_back(ms);
     }
-    GemmArgs g{A, B, C, nullptr, nullptr, G, G, G, G, G, G, 0, EPI_STORE};
+    GemmArgs g{A, B, C, nullptr, nullptr, GM, GN, GK, GK, GK, GN, 0, EPI_STORE};
     const int reps = c->dt == DT::BF16 ? 5 : 1;
     for (int rep = 0; rep < reps; ++rep) {
       CUDA_TRY(cudaEventRecord(e0, st));
@@ -1042,7 +1045,7 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
     std::sort(tb.begin(), tb.end());
     std::sort(tf.begin(), tf.end());
     mb[sms] = (use_attn ? attn_bytes : (double)n_bytes) / (tb[tb.size() / 2] * 1e-3);
-    mf[sms] = 2.0 * G * (double)G * G / (tf[tf.size() / 2] * 1e-3);
+    mf[sms] = 2.0 * GM * (double)GN * GK / (tf[tf.size() / 2] * 1e-3);
     return DUET_OK;
   };
   DUET_TRY(measure(c->s_full, c->total_sms));
