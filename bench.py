@@ -245,6 +245,9 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="also time every SM split")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="a few steps, no extras (for ncu)")
+    ap.add_argument("--tp", type=int, default=1,
+                    help="head-sharded tensor parallelism over the torchrun ranks (= WORLD_SIZE; default config "
+                         "cfg5): one batch per step across all ranks, NCCL allreduce after O and down")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3 if not args.profile_only else args.warmup)
 
@@ -263,6 +266,11 @@ def main():
         free, _ = torch.cuda.mem_get_info()
         if free < 190e9:
             args.config = "cfg3-fit"
+    tp = args.tp
+    if tp > 1 and tp != ws:
+        raise SystemExit(f"--tp {tp} needs WORLD_SIZE = {tp} (torchrun --nproc-per-node {tp})")
+    if tp > 1 and args.config == "cfg2":
+        args.config = "cfg5"
     cfg = configs.get_config(args.config)
     dev = torch.device("cuda", torch.cuda.current_device())
     tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
@@ -273,19 +281,31 @@ def main():
                                    + sum(2 * m.n_kv_heads * m.head_dim * (c + 1) for c in cfg.batch.decode))
     wl = workload.build(cfg, k=k_max, with_weights=False)  # pages for up to k_max look-ahead steps
     log(f"config {args.config}: generating weights")
-    W = [layer_weights_gpu(m, l, cfg.seed, dev, tdt) for l in range(m.n_layers)]
+    if tp > 1:   # this rank's head shard (synth.tp; the full layer is generated, sliced, freed)
+        from synth import tp as TP
+        W = [TP.shard_layer_weights(layer_weights_gpu(m, l, cfg.seed, dev, tdt), m.n_q_heads, m.n_kv_heads,
+                                    m.head_dim, m.ffn_dim, rank, tp) for l in range(m.n_layers)]
+    else:
+        W = [layer_weights_gpu(m, l, cfg.seed, dev, tdt) for l in range(m.n_layers)]
     x_pre, x_dec = inputs_gpu(wl, dev, tdt)
     torch.cuda.empty_cache()  # hand the generator's temporaries back: libduet allocates with cudaMalloc
     n_p, n_d = x_pre.shape[0], x_dec.shape[0]
     y_pre = torch.empty_like(x_pre)
     y_dec = torch.empty((8,) + tuple(x_dec.shape), dtype=tdt, device=dev)
     spec = D.make_spec(m.n_layers, m.d_model, m.ffn_dim, m.n_q_heads, m.n_kv_heads, m.head_dim, m.vocab,
-                       2 if cfg.dtype == "bf16" else 4, 1, int(m.qkv_bias), 1, m.rope_theta, m.norm_eps)
+                       2 if cfg.dtype == "bf16" else 4, 1, int(m.qkv_bias), tp, m.rope_theta, m.norm_eps)
     max_pages = max(wl.pre_tables.shape[1], wl.dec_tables.shape[1])
     max_pos = max([c + q for q, c in wl.pre_seqs] + [c + 8 for c in wl.dec_ctx]) + 16
     ctx = D.Ctx(spec, n_p, len(wl.pre_seqs), n_d, 8, max_pages, max_pos,
                 D.DUET_DTYPE_BF16 if cfg.dtype == "bf16" else D.DUET_DTYPE_FP32)
     parts, total = ctx.partitions()
+    nvl_bw, ar_alpha = 900e9, 3e-6
+    if tp > 1:
+        import torch.distributed as dist
+        ids = [D.nccl_unique_id(), D.nccl_unique_id()] if rank == 0 else [None, None]
+        dist.broadcast_object_list(ids, src=0)
+        ctx.set_comms(rank, ids[0], ids[1])
+        ar_alpha, nvl_bw = ctx.calibrate_allreduce()   # P:237 alpha and B_NVLink, measured
 
     # L0 calibration: Pi_SM(S), B_HBM(S) on this GPU with our kernels
     t0 = time.perf_counter()
@@ -296,9 +316,14 @@ def main():
     else:
         fl, bw = ctx.calibrate(total)
     t_cal = time.perf_counter() - t0
-    hw = D.HwProfile(total, parts, fl, bw)
+    hw = D.HwProfile(total, parts, fl, bw, nvlink_bw=nvl_bw, allreduce_alpha=ar_alpha)
     log(f"calibrated in {t_cal:.1f}s; generating the KV history")
     Kp, Vp = kv_pools_gpu(wl, dev, tdt)   # after calibration: the pools take most of HBM at cfg3
+    if tp > 1:
+        from synth import tp as TP
+        for l in range(len(Kp)):
+            Kp[l] = TP.shard_kv_pool(Kp[l], m.n_kv_heads, rank, tp)
+            Vp[l] = TP.shard_kv_pool(Vp[l], m.n_kv_heads, rank, tp)
     log("KV ready; warm-up")
     torch.cuda.empty_cache()
     tau = args.tau if args.tau is not None else cfg.batch.tbt_slo_s
@@ -374,6 +399,8 @@ def main():
     times = ctx.last_step_times()
     kernels = times["kernels"] * args.steps
     value, t_max_s = whole_job_rate(tokens, t_ms * 1e-3, ws)
+    if tp > 1:   # the TP group processes ONE batch per step: units are not multiplied by the ranks
+        value /= ws
     ms_per_step = t_max_s * 1e3 / args.steps
     split = s
 
@@ -462,7 +489,7 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         te = max_over_ranks(a.elapsed_time(b), ws)
-        e2e = {"value": tok * ws / (te * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": tok * (1 if tp > 1 else ws) / (te * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h)}
 
     # ------------------------------------------------ roofline of the dominant kernel class
@@ -500,13 +527,14 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if tp > 1 else "weak",
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded counter generator, random weights)",
             "config": {"workload": f"{args.config}: {cfg.note}", "mode": ["temporal", "spatial"][split.mode],
                        "s_p": split.s_p, "s_d": split.s_d, "k": split.k, "flags": split.flags,
                        "tau_ms": tau * 1e3, "prefill_tokens": n_p, "decode_reqs": n_d,
                        "l2": f"inputs > L2 ({step_bytes / 1e9:.1f} GB of weights + KV read per step), no flush",
-                       "parallelism": f"dp{ws} (independent replicas)", "calibration_s": round(t_cal, 2)},
+                       "parallelism": f"tp{tp} (head-sharded, NCCL allreduce after O and down)" if tp > 1
+                       else f"dp{ws} (independent replicas)", "calibration_s": round(t_cal, 2)},
             "predictor": {"t_pred_ms": t_pred * 1e3, "t_meas_ms": side["t_window"] * 1e3, "err": pred_err,
                           "t_meas_decode_ms": side["t_decode"] * 1e3, "t_meas_prefill_ms": side["t_prefill"] * 1e3},
             "comparison": comp,

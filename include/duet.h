@@ -35,7 +35,8 @@ typedef enum {
                                   dividing heads/ffn, inconsistent model spec          */
   DUET_ERR_UNSUPPORTED = -4,   /* a shape the kernels do not implement (e.g. head_dim != 64/128) */
   DUET_ERR_CUDA = -5,          /* a CUDA runtime / driver call failed                          */
-  DUET_ERR_CAPACITY = -6       /* a request exceeds the limits the ctx was created with        */
+  DUET_ERR_CAPACITY = -6,      /* a request exceeds the limits the ctx was created with        */
+  DUET_ERR_NCCL = -7           /* libnccl missing or an NCCL call failed (tensor parallelism)  */
 } duet_status;
 
 /* Message of the last failure on this thread ("" if none).  Library-owned, valid until the
@@ -154,6 +155,30 @@ typedef struct {
 duet_status duet_ctx_create(int32_t device, const duet_model_spec* spec,
                             const duet_ctx_limits* limits, duet_ctx** out);
 duet_status duet_ctx_destroy(duet_ctx* ctx);
+
+/* ----------------------------------------------------------------- tensor parallelism (§8 a9)
+ * Head-sharded TP (reading #13).  A ctx created with spec->tp = N
+ * computes the shard of rank r: h_q/N query heads, h_kv/N kv heads and ffn_dim/N FFN columns
+ * (N must divide all three).  The caller passes that rank's weights to duet_step — w_qkv rows of
+ * its q, k and v heads ([(h_q + 2 h_kv)/N d_h][d]), w_o columns of its q heads ([d][h_q/N d_h]),
+ * w_gate_up rows [gate rows of its columns ; up rows] ([2 ffn_dim/N][d]), w_down columns
+ * ([d][ffn_dim/N]); norm gains whole — and KV pools holding its kv heads ([n_pages][h_kv/N][P][d_h]).
+ * The O and down projections then produce partial sums: rank 0 adds the residual and the
+ * [rows][d] partials are all-reduced (sum) over NCCL right after each, on the side's own
+ * communicator (decode and prefill/temporal sides run concurrently in spatial mode).
+ *
+ * duet_nccl_unique_id: an ncclUniqueId (128 bytes) into out (len >= 128); rank 0 creates two (one
+ *   per side) and broadcasts them (e.g. with torch.distributed).
+ * duet_ctx_set_comms: collective over the N ranks (each calls it with its rank and the same two
+ *   ids): creates the ctx's decode-side and prefill-side communicators (ncclCommInitRank).  With
+ *   spec->tp = 1 it creates single-rank communicators (the allreduce path, as a no-op copy).
+ * duet_calibrate_allreduce: alpha (s) and B_NVLink (B/s) of the P:237 ring model from timed
+ *   allreduces of 16 B and 64 MiB on the prefill communicator (0, 0 when tp = 1).
+ * libnccl.so.2 is resolved at run time (the one PyTorch loads).  Errors: INVALID_ARG,
+ * OUT_OF_RANGE (rank), NCCL, CUDA. */
+duet_status duet_nccl_unique_id(void* out, int32_t len);
+duet_status duet_ctx_set_comms(duet_ctx* ctx, int32_t rank, const void* id_decode, const void* id_prefill);
+duet_status duet_calibrate_allreduce(duet_ctx* ctx, double* alpha_s, double* bw_bytes_s);
 
 /* The achievable decode-partition sizes, ascending (host array of capacity *n on input;
  * *n is set to the count).  total_sms: SMs of the device. */

@@ -164,9 +164,15 @@ class Model:
 
 
 def layer_forward(m: Model, w: dict, layer: int, x: np.ndarray, pos: np.ndarray,
-                  tables: list, kv: PagedKV) -> np.ndarray:
+                  tables: list, kv: PagedKV, allreduce=None) -> np.ndarray:
     """One layer over rows ``x`` [n, d]; row i is at absolute position pos[i] of the sequence
-    whose page-table row is tables[i].  Steps follow C-2 in order."""
+    whose page-table row is tables[i].  Steps follow C-2 in order.
+
+    Head-sharded tensor parallelism (reading #13): with ``m`` and ``w``
+    the shard of one rank (h_q/N query heads, h_kv/N kv heads, m/N FFN columns; W_qkv / W_gate_up
+    rows and W_o / W_down columns of those heads and columns) and ``allreduce`` the sum over the N
+    ranks, the two row-parallel projections (O and down) produce partial sums that are all-reduced
+    before the residual add.  ``allreduce=None`` is the unsharded layer."""
     x = np.asarray(x, dtype=np.float64)
     n = x.shape[0]
     hq, hkv, dh = m.n_q_heads, m.n_kv_heads, m.head_dim
@@ -187,15 +193,17 @@ def layer_forward(m: Model, w: dict, layer: int, x: np.ndarray, pos: np.ndarray,
         kv.write(layer, tables[i], int(pos[i]), k[i], v[i])
     # 5. causal attention over the paged cache
     o = paged_causal_attention(q, pos, tables, kv, layer, hkv)
-    # 6. x1 = x + o W_o^T
-    x1 = x + o.reshape(n, hq * dh) @ np.asarray(w["w_o"], dtype=np.float64).T
+    # 6. x1 = x + o W_o^T   (TP: x + allreduce(o_shard W_o,shard^T))
+    part = o.reshape(n, hq * dh) @ np.asarray(w["w_o"], dtype=np.float64).T
+    x1 = x + (part if allreduce is None else allreduce(part))
     # 7. h2 = RMSNorm(x1) * g2
     h2 = rmsnorm(x1, w["g_norm2"], m.norm_eps)
     # 8. y = x1 + (silu(h2 W_g^T) * h2 W_u^T) W_d^T     (gate_up rows = [gate; up])
     gu = h2 @ np.asarray(w["w_gate_up"], dtype=np.float64).T
     mm = m.ffn_dim
     a = silu(gu[:, :mm]) * gu[:, mm:]
-    return x1 + a @ np.asarray(w["w_down"], dtype=np.float64).T
+    part = a @ np.asarray(w["w_down"], dtype=np.float64).T
+    return x1 + (part if allreduce is None else allreduce(part))
 
 
 def prefill_forward(m: Model, weights: list, x: np.ndarray, seqs: list, tables: np.ndarray,

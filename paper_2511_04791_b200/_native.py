@@ -113,6 +113,9 @@ _SIGS = {
     "duet_op_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "duet_op_rmsnorm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "duet_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_int32]),
+    "duet_ctx_set_comms": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "duet_calibrate_allreduce": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -201,6 +204,13 @@ def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for duet_ctx_set_comms (duet_nccl_unique_id)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().duet_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
 class Ctx:
     """Owns a duet_ctx.  Device tensors are torch tensors (plumbing only)."""
 
@@ -280,6 +290,18 @@ class Ctx:
         _check(lib().duet_profile_read(self.h, arr))
         names = ("gemm", "prefill_attn", "decode_attn", "other")
         return {names[i]: {n: getattr(arr[i], n) for n, _ in duet_kernel_stats._fields_} for i in range(DUET_KCLASS_N)}
+
+    def set_comms(self, rank: int, id_decode: bytes, id_prefill: bytes):
+        """Tensor parallelism: collective over the tp ranks (duet_ctx_set_comms)."""
+        a = C.create_string_buffer(bytes(id_decode), 128)
+        b = C.create_string_buffer(bytes(id_prefill), 128)
+        _check(lib().duet_ctx_set_comms(self.h, int(rank), a, b))
+
+    def calibrate_allreduce(self):
+        """(alpha seconds, B_NVLink bytes/s) of the P:237 allreduce model (duet_calibrate_allreduce)."""
+        a, b = C.c_double(), C.c_double()
+        _check(lib().duet_calibrate_allreduce(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def calibrate(self, total_sms: int):
         fl = (C.c_double * (total_sms + 1))()

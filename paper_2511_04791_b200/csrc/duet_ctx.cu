@@ -11,6 +11,8 @@
 //  * Temporal mode (Alg. 1 l.4): the same kernels on one full-device stream over the
 //    concatenated rows [prefill ; decode].
 #include <cuda.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is dlopen-ed (the one torch already loaded)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -84,6 +86,43 @@ duet_status load_driver() {
   return DUET_OK;
 }
 
+// NCCL (tensor parallelism), resolved at run time from the process's libnccl.so.2 (PyTorch
+// loads one; no link-time dependency), only when a context is given communicators.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi NCCL;
+
+duet_status load_nccl() {
+  if (NCCL.ok) return DUET_OK;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) DUET_FAIL(DUET_ERR_NCCL, "libnccl.so.2 not found: %s", dlerror());
+  auto get = [&](const char* name, void** fn) -> duet_status {
+    *fn = dlsym(h, name);
+    if (!*fn) DUET_FAIL(DUET_ERR_NCCL, "NCCL symbol %s missing", name);
+    return DUET_OK;
+  };
+  DUET_TRY(get("ncclGetUniqueId", (void**)&NCCL.GetUniqueId));
+  DUET_TRY(get("ncclCommInitRank", (void**)&NCCL.CommInitRank));
+  DUET_TRY(get("ncclAllReduce", (void**)&NCCL.AllReduce));
+  DUET_TRY(get("ncclCommDestroy", (void**)&NCCL.CommDestroy));
+  DUET_TRY(get("ncclGetErrorString", (void**)&NCCL.GetErrorString));
+  NCCL.ok = true;
+  return DUET_OK;
+}
+
+#define NCCL_TRY(expr)                                                                            \
+  do {                                                                                            \
+    ncclResult_t r_ = (expr);                                                                     \
+    if (r_ != ncclSuccess) DUET_FAIL(DUET_ERR_NCCL, "%s failed: %s", #expr, NCCL.GetErrorString(r_)); \
+  } while (0)
+
 constexpr int kPageSize = 16;
 constexpr int kStageSlots = 4;
 constexpr int kMaxSplits = 32;
@@ -126,7 +165,10 @@ struct GraphEntry {
 
 struct duet_ctx {
   int device = 0;
-  duet_model_spec spec{};
+  duet_model_spec spec{};   // this rank's shard: h_q/tp, h_kv/tp, ffn_dim/tp (d_model, head_dim global)
+  duet_model_spec gspec{};  // the model as given (tp = tensor-parallel degree)
+  int tp_rank = 0;
+  ncclComm_t comm_dec = nullptr, comm_pre = nullptr;  // one communicator per side
   duet_ctx_limits lim{};
   DT dt = DT::BF16;
   int total_sms = 0;
@@ -285,6 +327,15 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
   auto gemm_by = [&](double N, double K, double Nout, bool resid) {
     return (n * K + N * K + n * Nout + (resid ? n * Nout : 0.0)) * e;
   };
+  ncclComm_t comm = (&S == &c->dec) ? c->comm_dec : c->comm_pre;
+  const bool lead = comm == nullptr || c->tp_rank == 0;
+  const ncclDataType_t nccl_dt = dt == DT::BF16 ? ncclBfloat16 : ncclFloat32;
+  // sum of the ranks' partial [n_rows][d] rows in place (2 allreduces per layer)
+  auto allreduce = [&](void* buf) -> int {
+    if (!comm) return 0;
+    const ncclResult_t r = NCCL.AllReduce(buf, buf, (size_t)n_rows * d, nccl_dt, ncclSum, comm, st);
+    return r == ncclSuccess ? 1 : -1000000;  // a negative count is reported by the check below
+  };
   auto with_ws = [&](GemmArgs& g) {
     g.ws = S.gemm_ws;
     g.ws_floats = S.gemm_ws_floats;
@@ -383,9 +434,13 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       nk += r;
     }
     // 5. x1 = x + o W_o^T
-    GemmArgs go{S.o, W.w_o, S.x1, X, nullptr, n_rows, d, hq * dh, hq * dh, hq * dh, d, d, EPI_RESIDUAL};
+    // TP: the O projection of this rank's heads is a partial sum; rank 0 adds the
+    // residual and the partials are all-reduced over the side's communicator
+    GemmArgs go{S.o, W.w_o, S.x1, lead ? X : nullptr, nullptr, n_rows, d, hq * dh, hq * dh, hq * dh, d, d,
+                lead ? EPI_RESIDUAL : EPI_STORE};
     with_ws(go);
     TIMED(DUET_KCLASS_GEMM, gemm_fl(d, hq * dh), gemm_by(d, hq * dh, d, true), launch_gemm(dt, go, num_sms, st));
+    if (comm) TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, allreduce(S.x1));
     // 6. h2 = RMSNorm(x1) g2
     TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e, launch_rmsnorm(dt, S.x1, W.g_norm2, S.h2, n_rows, d, eps, st));
     // 7. act = silu(h2 W_g^T) * (h2 W_u^T)
@@ -393,11 +448,14 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     with_ws(gg);
     TIMED(DUET_KCLASS_GEMM, gemm_fl(2.0 * m, d), gemm_by(2.0 * m, d, m, false), launch_gemm(dt, gg, num_sms, st));
     // 8. y = x1 + act W_d^T
-    GemmArgs gd{S.act, W.w_down, Y, S.x1, nullptr, n_rows, d, m, m, m, d, d, EPI_RESIDUAL};
+    GemmArgs gd{S.act, W.w_down, Y, lead ? S.x1 : nullptr, nullptr, n_rows, d, m, m, m, d, d,
+                lead ? EPI_RESIDUAL : EPI_STORE};
     with_ws(gd);
     TIMED(DUET_KCLASS_GEMM, gemm_fl(d, m), gemm_by(d, m, d, true), launch_gemm(dt, gd, num_sms, st));
+    if (comm) TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, allreduce(Y));
   }
 #undef TIMED
+  if (nk < 0) DUET_FAIL(DUET_ERR_NCCL, "ncclAllReduce failed inside the layer stack");
   DUET_TRY(check_launch("layer stack"));
   *kernels += nk;
   return DUET_OK;
@@ -431,6 +489,10 @@ extern "C" duet_status duet_ctx_create(int32_t device, const duet_model_spec* sp
     DUET_FAIL(DUET_ERR_UNSUPPORTED, "GQA group %d (kernels implement 1, 2, 4, 5, 8)", G);
   if (spec->d_model % 16 || spec->ffn_dim % 16)
     DUET_FAIL(DUET_ERR_UNSUPPORTED, "d_model and ffn_dim must be multiples of 16");
+  const int tp = spec->tp < 1 ? 1 : spec->tp;
+  if (spec->n_q_heads % tp || spec->n_kv_heads % tp || spec->ffn_dim % tp || (spec->ffn_dim / tp) % 16)
+    DUET_FAIL(DUET_ERR_CONFIG, "tp = %d must divide h_q = %d, h_kv = %d and ffn_dim = %d (ffn_dim/tp %% 16 == 0)", tp,
+              spec->n_q_heads, spec->n_kv_heads, spec->ffn_dim);
   if (lim->dtype != DUET_DTYPE_BF16 && lim->dtype != DUET_DTYPE_FP32)
     DUET_FAIL(DUET_ERR_INVALID_ARG, "dtype = %d", lim->dtype);
   if (lim->max_prefill_tokens < 0 || lim->max_decode_reqs < 0 || lim->max_k < 1 || lim->max_pages_per_seq < 1 ||
@@ -438,7 +500,12 @@ extern "C" duet_status duet_ctx_create(int32_t device, const duet_model_spec* sp
     DUET_FAIL(DUET_ERR_INVALID_ARG, "limits out of range");
   duet_ctx* c = new duet_ctx();
   c->device = device;
-  c->spec = *spec;
+  c->gspec = *spec;
+  c->spec = *spec;  // the shard this rank computes (head-sharded TP, reading #13)
+  c->spec.n_q_heads /= tp;
+  c->spec.n_kv_heads /= tp;
+  c->spec.ffn_dim /= tp;
+  c->spec.tp = tp;
   c->lim = *lim;
   c->dt = lim->dtype == DUET_DTYPE_BF16 ? DT::BF16 : DT::F32;
   auto fail = [&](duet_status s) {
@@ -531,6 +598,8 @@ extern "C" duet_status duet_ctx_create(int32_t device, const duet_model_spec* sp
 extern "C" duet_status duet_ctx_destroy(duet_ctx* c) {
   if (!c) return DUET_OK;
   cudaSetDevice(c->device);
+  if (c->comm_dec) NCCL.CommDestroy(c->comm_dec);
+  if (c->comm_pre) NCCL.CommDestroy(c->comm_pre);
   cudaDeviceSynchronize();
   for (auto& kv : c->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -905,6 +974,79 @@ extern "C" duet_status duet_last_step_times(duet_ctx* c, duet_step_times* out) {
   out->t_window = w * 1e-3;
   out->t_decode = td * 1e-3;
   out->t_prefill = tp * 1e-3;
+  return DUET_OK;
+}
+
+// ---------------------------------------------------------------------------------- tensor parallelism
+
+extern "C" duet_status duet_nccl_unique_id(void* out, int32_t len) {
+  clear_error();
+  if (!out || len < (int32_t)sizeof(ncclUniqueId))
+    DUET_FAIL(DUET_ERR_INVALID_ARG, "out must hold %d bytes", (int)sizeof(ncclUniqueId));
+  DUET_TRY(load_nccl());
+  ncclUniqueId id;
+  NCCL_TRY(NCCL.GetUniqueId(&id));
+  memcpy(out, &id, sizeof(id));
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_ctx_set_comms(duet_ctx* c, int32_t rank, const void* id_decode, const void* id_prefill) {
+  clear_error();
+  if (!c || !id_decode || !id_prefill) DUET_FAIL(DUET_ERR_INVALID_ARG, "ctx / unique ids are NULL");
+  if (rank < 0 || rank >= c->spec.tp) DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "rank %d outside [0, tp = %d)", rank, c->spec.tp);
+  if (c->comm_dec || c->comm_pre) DUET_FAIL(DUET_ERR_INVALID_ARG, "communicators already set");
+  DUET_TRY(load_nccl());
+  CUDA_TRY(cudaSetDevice(c->device));
+  ncclUniqueId a, b;
+  memcpy(&a, id_decode, sizeof(a));
+  memcpy(&b, id_prefill, sizeof(b));
+  NCCL_TRY(NCCL.CommInitRank(&c->comm_dec, c->spec.tp, a, rank));
+  NCCL_TRY(NCCL.CommInitRank(&c->comm_pre, c->spec.tp, b, rank));
+  c->tp_rank = rank;
+  c->graphs.clear();  // captured decode graphs predate the communicators
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_calibrate_allreduce(duet_ctx* c, double* alpha_s, double* bw_bytes_s) {
+  clear_error();
+  if (!c || !alpha_s || !bw_bytes_s) DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL argument");
+  if (!c->comm_pre) DUET_FAIL(DUET_ERR_INVALID_ARG, "no communicators (duet_ctx_set_comms)");
+  const int N = c->spec.tp;
+  *alpha_s = 0.0;
+  *bw_bytes_s = 0.0;
+  if (N < 2) return DUET_OK;
+  const size_t big = (size_t)64 << 20;
+  void* buf = nullptr;
+  CUDA_TRY(cudaMalloc(&buf, big));
+  CUDA_TRY(cudaMemset(buf, 0, big));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  auto time_ar = [&](size_t bytes, float* ms) -> duet_status {
+    std::vector<float> t;
+    for (int rep = 0; rep < 9; ++rep) {
+      CUDA_TRY(cudaEventRecord(e0, c->s_full));
+      NCCL_TRY(NCCL.AllReduce(buf, buf, bytes / 2, ncclBfloat16, ncclSum, c->comm_pre, c->s_full));
+      CUDA_TRY(cudaEventRecord(e1, c->s_full));
+      CUDA_TRY(cudaEventSynchronize(e1));
+      float x;
+      CUDA_TRY(cudaEventElapsedTime(&x, e0, e1));
+      if (rep >= 2) t.push_back(x);
+    }
+    std::sort(t.begin(), t.end());
+    *ms = t[t.size() / 2];
+    return DUET_OK;
+  };
+  float t_small, t_big;
+  DUET_TRY(time_ar(16, &t_small));
+  DUET_TRY(time_ar(big, &t_big));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  // P:237 ring model: t(B) = 2(N-1) alpha + 2(N-1) B / (N B_NVL)  (+ the local-reduce term, negligible)
+  *alpha_s = t_small * 1e-3 / (2.0 * (N - 1));
+  const double t_bw = std::max(t_big * 1e-3 - 2.0 * (N - 1) * *alpha_s, 1e-9);
+  *bw_bytes_s = 2.0 * (N - 1) * (double)big / (N * t_bw);
   return DUET_OK;
 }
 

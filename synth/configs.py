@@ -82,6 +82,11 @@ CONFIGS = {
                                                        k=1, tbt_slo_s=50e-3), dtype="bf16", seed=4791 + 3,
                        note="Llama-3-8B 32 layers: 8k prompt into 256 decodes at ctx 2k-6k (fits 180 GB), "
                             "TBT SLO 50 ms"),
+    # cfg5: Llama-3-70B-shaped 8-layer slice, head-sharded TP = 2/4/8 (bench.py --tp N); the TBT SLO is
+    # 50 ms scaled to the 8 of 80 layers
+    "cfg5": Config("cfg5", LLAMA3_70B_SLICE, BatchCfg(prefill=((16384, 0),), decode=(4096,) * 512, k=1,
+                                                      tbt_slo_s=50e-3 * 8 / 80), dtype="bf16", seed=4791 + 5,
+                   note="Llama-3-70B shapes, 8 layers: 16k prefill chunk + 512 decodes at ctx 4k, TP over NVLink"),
 }
 
 

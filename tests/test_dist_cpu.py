@@ -42,3 +42,61 @@ def test_replicas_max_over_ranks_gloo():
     for rank, v, tmax in res:
         assert tmax == 2.0                 # max over ranks
         assert v == pytest.approx(1000.0 * 2 / 2.0)
+
+
+def _tp_worker(rank, ws, port, q):
+    """Rank `rank` of a head-sharded TP group: its weight and KV shards (synth.tp), the
+    oracle layer with the row-parallel partial sums all-reduced over gloo."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    from dataclasses import replace
+    from oracle import layer as OL
+    from synth import configs, tp, workload
+    from tests.oracle_run import make_kv
+    cfg = configs.get_config("cfg1-gqa")
+    wl = workload.build(cfg, k=2)
+    m = cfg.model
+    full = OL.Model.from_cfg(m)
+    lq, lkv, lm = tp.shard_dims(m.n_q_heads, m.n_kv_heads, m.ffn_dim, rank, ws)
+    local = replace(full, n_q_heads=lq, n_kv_heads=lkv, ffn_dim=lm)
+    weights = [tp.shard_layer_weights(w, m.n_q_heads, m.n_kv_heads, m.head_dim, m.ffn_dim, rank, ws)
+               for w in wl.weights]
+    kv_full = make_kv(wl)
+    kv = OL.PagedKV(wl.n_layers, wl.n_pages, lkv, cfg.batch.page_size, m.head_dim)
+    kv.K = tp.shard_kv_pool(kv_full.K, m.n_kv_heads, rank, ws)
+    kv.V = tp.shard_kv_pool(kv_full.V, m.n_kv_heads, rank, ws)
+
+    def allreduce(part):
+        t = torch.from_numpy(np.ascontiguousarray(part))
+        dist.all_reduce(t)
+        return t.numpy()
+
+    pos, trows = [], []
+    for s, (qn, c) in enumerate(wl.pre_seqs):
+        pos.extend(range(c, c + qn))
+        trows.extend([wl.pre_tables[s]] * qn)
+    y_tp = OL.layer_forward(local, weights[0], 0, wl.x_pre, np.asarray(pos), trows, kv, allreduce=allreduce)
+    if rank == 0:
+        y_ref = OL.layer_forward(full, wl.weights[0], 0, wl.x_pre, np.asarray(pos), trows, kv_full)
+        q.put(float(np.max(np.abs(y_tp - y_ref)) / np.max(np.abs(y_ref))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_tp_head_sharded_oracle_equals_unsharded_gloo():
+    """The head-sharded TP recipe (synth.tp slices + allreduce after O and down) reproduces the
+    unsharded layer: SURVEY §8(c) C-8 'TP shards summed equal unsharded', at world size 2 over gloo."""
+    ws = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_tp_worker, args=(r, ws, port, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+    assert err < 1e-12, err

@@ -263,3 +263,30 @@ def test_parity_cfg2_full_layer_temporal_and_optimizer_split():
         torch.cuda.synchronize()
         _check_outputs(g, y_pre, y_dec, TOL["bf16"])
     _check_kv(g, kv_o, TOL["bf16"])
+
+
+def test_tp_allreduce_path_world1_bitwise():
+    """Head-sharded TP code path (§8 a9): a ctx with single-rank NCCL communicators runs the rank-0
+    residual + allreduce-after-O/down path (as a no-op copy) and reproduces the plain ctx bitwise,
+    in temporal and spatial mode (the decode side's allreduces are captured in its CUDA graph)."""
+    cfg = configs.get_config("cfg1-bf16")
+    wl = workload.build(cfg, k=2)
+    for split in (D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1),):
+        ref, ctx = _run_split(wl, "bf16", lambda c: split)
+        ctx.close()
+    ctx_tp = make_ctx(wl, "bf16")
+    ctx_tp.set_comms(0, D.nccl_unique_id(), D.nccl_unique_id())
+    g = GpuWorkload(wl, "bf16")
+    g.step(ctx_tp, D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1))
+    torch.cuda.synchronize()
+    assert torch.equal(g.y_pre, ref.y_pre) and torch.equal(g.y_dec[0], ref.y_dec[0])
+    parts, total = ctx_tp.partitions()
+    sp = D.split_struct(D.DUET_MODE_SPATIAL, total - parts[1], parts[1], 2)
+    ref2, ctx2 = _run_split(wl, "bf16", lambda c: sp)
+    g2 = GpuWorkload(wl, "bf16")
+    g2.step(ctx_tp, sp)
+    torch.cuda.synchronize()
+    assert torch.equal(g2.y_pre, ref2.y_pre) and torch.equal(g2.y_dec, ref2.y_dec)
+    assert ctx_tp.calibrate_allreduce() == (0.0, 0.0)
+    ctx2.close()
+    ctx_tp.close()
