@@ -328,4 +328,5 @@ def split_struct(mode, s_p, s_d, k, flags=0, t_mixed=0.0, t_p=0.0, t_d=0.0, rho=
 
 
 __all__ = [n for n in dir() if n.startswith(("duet_", "DUET_"))] + [
-    "Ctx", "HwProfile", "make_spec", "split_struct", "split_tuple", "lib", "DuetError", "EXPORTED", "LIB_PATH"]
+    "Ctx", "HwProfile", "make_spec", "split_struct", "split_tuple", "lib", "DuetError", "EXPORTED", "LIB_PATH",
+    "nccl_unique_id"]
