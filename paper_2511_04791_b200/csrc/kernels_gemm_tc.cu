@@ -155,6 +155,8 @@ struct Cfg {
 constexpr int SPLITK_TARGET_UNITS = 148;   // >= one unit per SM of the full GPU; >= 3 per CTA on a 24-SM partition
 constexpr int SPLITK_MIN_KB = 8;           // >= 512 of K per chunk
 constexpr int SPLITK_MAX = 8;              // partial bytes <= ~15% of the weight bytes at Llama-3-8B shapes
+constexpr int SPLITK_MAX_TILES = 40;       // split only tile-starved shapes (O, down: 32 tiles); with 48+
+                                           // tiles (QKV, gate-up) the reduction costs more than it balances
 
 struct Params {
   int M, N, K;        // C is M x N; N = output features (SwiGLU: width of act)
@@ -419,51 +421,83 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
   }
 }
 
-// Split-K reduction + epilogue: one CTA per (tile, 16-token slice), thread = weight row n.  Sums the
-// ksplit partials of each output in chunk order 0..ksplit-1 (a fixed order, independent of the grid
-// and of which CTA computed which chunk), then applies the fused epilogue and stores C[m][n].
+// Split-K reduction + epilogue: one CTA (256 threads) per tile.  Thread t owns 4 consecutive weight
+// rows n = 4 (t % 32) .. +3 and the token columns m = t / 32, t / 32 + 8, ...; for two columns at a
+// time it issues all ksplit float4 loads before summing them in chunk order 0..ksplit-1 (a fixed
+// order, independent of the grid and of which CTA computed which chunk), so ~16 loads per thread are
+// in flight; then applies the fused epilogue and stores 4 bf16 (8 B) per thread per column.
 template <int EPI>
-__global__ void __launch_bounds__(128) splitk_reduce_kernel(Params p, int bn, int acc_cols) {
-  const int t = blockIdx.x, r = threadIdx.x;
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(Params p, int bn, int acc_cols) {
+  const int t = blockIdx.x;
   const int mb = t % p.num_m, nb = t / p.num_m;
-  const int n = nb * BM + r;
+  const int rq = threadIdx.x & 31, cg = threadIdx.x >> 5;
+  const int n = nb * BM + 4 * rq;
   if (n >= p.N) return;
   const size_t chunk = (size_t)acc_cols * BM;
-  const float* base = p.ws + (size_t)t * p.ksplit * chunk + r;
-  float badd = 0.f;
+  const float* base = p.ws + (size_t)t * p.ksplit * chunk + 4 * rq;
+  float bias4[4] = {0.f, 0.f, 0.f, 0.f};
   if constexpr (EPI == EPI_STORE)
-    if (p.bias) badd = __bfloat162float(p.bias[n]);
-#pragma unroll 1
-  for (int j0 = 0; j0 < 16; j0 += 4) {
-    float v[4], g[4];
+    if (p.bias)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int ml = blockIdx.y * 16 + j0 + j;
-      float f[SPLITK_MAX], h[SPLITK_MAX];
+      for (int e = 0; e < 4; ++e) bias4[e] = n + e < p.N ? __bfloat162float(p.bias[n + e]) : 0.f;
+  auto sum_col = [&](int col, float (&out)[4]) {
+    float4 f[SPLITK_MAX];
 #pragma unroll
-      for (int k = 0; k < SPLITK_MAX; ++k)
-        if (k < p.ksplit) {
-          f[k] = __ldcg(base + k * chunk + (size_t)ml * BM);
-          if constexpr (EPI == EPI_SWIGLU) h[k] = __ldcg(base + k * chunk + (size_t)(bn + ml) * BM);
-        }
-      v[j] = f[0];
-      g[j] = EPI == EPI_SWIGLU ? h[0] : 0.f;
+    for (int k = 0; k < SPLITK_MAX; ++k)
+      if (k < p.ksplit) f[k] = __ldcg(reinterpret_cast<const float4*>(base + k * chunk + (size_t)col * BM));
+    float4 a = f[0];
 #pragma unroll
-      for (int k = 1; k < SPLITK_MAX; ++k)
-        if (k < p.ksplit) {
-          v[j] += f[k];
-          if constexpr (EPI == EPI_SWIGLU) g[j] += h[k];
-        }
+    for (int k = 1; k < SPLITK_MAX; ++k)
+      if (k < p.ksplit) {
+        a.x += f[k].x;
+        a.y += f[k].y;
+        a.z += f[k].z;
+        a.w += f[k].w;
+      }
+    out[0] = a.x;
+    out[1] = a.y;
+    out[2] = a.z;
+    out[3] = a.w;
+  };
+#pragma unroll 2
+  for (int ml = cg; ml < bn; ml += 8) {
+    const int m = mb * bn + ml;
+    if (m >= p.M) break;
+    float v[4];
+    sum_col(ml, v);
+    if constexpr (EPI == EPI_SWIGLU) {
+      float g[4];
+      sum_col(bn + ml, g);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = silu_f(v[e]) * g[e];
     }
+    bf16* dst = p.C + (size_t)m * p.ldc + n;
+    if (n + 4 <= p.N) {
+      if constexpr (EPI == EPI_RESIDUAL) {
+        const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(p.R + (size_t)m * p.ldr + n);
+        const float2 r0 = __bfloat1622float2(r2[0]), r1 = __bfloat1622float2(r2[1]);
+        v[0] += r0.x;
+        v[1] += r0.y;
+        v[2] += r1.x;
+        v[3] += r1.y;
+      }
+      if constexpr (EPI == EPI_STORE)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int m = mb * bn + blockIdx.y * 16 + j0 + j;
-      if (m >= p.M) continue;
-      float o = v[j];
-      if constexpr (EPI == EPI_SWIGLU) o = silu_f(o) * g[j];
-      if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)m * p.ldr + n]);
-      if constexpr (EPI == EPI_STORE) o += badd;
-      p.C[(size_t)m * p.ldc + n] = __float2bfloat16_rn(o);
+        for (int e = 0; e < 4; ++e) v[e] += bias4[e];
+      __nv_bfloat162 o0 = __floats2bfloat162_rn(v[0], v[1]), o1 = __floats2bfloat162_rn(v[2], v[3]);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&o0);
+      pk.y = *reinterpret_cast<uint32_t*>(&o1);
+      *reinterpret_cast<uint2*>(dst) = pk;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (n + e >= p.N) continue;
+        float o = v[e];
+        if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)m * p.ldr + n + e]);
+        if constexpr (EPI == EPI_STORE) o += bias4[e];
+        dst[e] = __float2bfloat16_rn(o);
+      }
     }
   }
 }
@@ -501,7 +535,7 @@ static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int l
 
 // K chunking of a split-K launch: a function of the shape only (see SPLITK_TARGET_UNITS)
 static void splitk_plan(int num_tiles, int num_k, int* ks_out, int* kb_out) {
-  int ks = (SPLITK_TARGET_UNITS + num_tiles - 1) / num_tiles;
+  int ks = num_tiles > SPLITK_MAX_TILES ? 1 : (SPLITK_TARGET_UNITS + num_tiles - 1) / num_tiles;
   ks = std::min(std::min(ks, SPLITK_MAX), num_k / SPLITK_MIN_KB);
   if (ks < 1) ks = 1;
   const int kb = (num_k + ks - 1) / ks;
@@ -560,7 +594,7 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   const int grid = p.num_units < CF::CTAS * num_sms ? p.num_units : CF::CTAS * num_sms;
   gemm_tc_kernel<BN, EPI, SWAP><<<grid, CF::THREADS, CF::SMEM, st>>>(mx, mw, p);
   if (p.ksplit > 1) {
-    splitk_reduce_kernel<EPI><<<dim3(p.num_tiles, BN / 16), 128, 0, st>>>(p, BN, CF::ACC_COLS);
+    splitk_reduce_kernel<EPI><<<p.num_tiles, 256, 0, st>>>(p, BN, CF::ACC_COLS);
     return 2;
   }
   return 1;
