@@ -1089,7 +1089,6 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
   void* buf = nullptr;
   unsigned long long* sink = nullptr;
   CUDA_TRY(cudaMalloc(&buf, n_bytes));
-  CUDA_TRY(cudaMemset(buf, 1, n_bytes));
   CUDA_TRY(cudaMalloc(&sink, 4096 * sizeof(unsigned long long)));
   // Pi_SM(S): the achievable rate of the model's largest linear operator ("gemm
   // microbenchmark"): gate-up shape, M = the prefill chunk capacity (256..8192 rows), N = 2 m, K = d
@@ -1100,8 +1099,10 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
   CUDA_TRY(cudaMalloc(&A, (size_t)GM * GK * es));
   CUDA_TRY(cudaMalloc(&B, (size_t)GN * GK * es));
   CUDA_TRY(cudaMalloc(&C, (size_t)GM * GN * es));
-  CUDA_TRY(cudaMemset(A, 0, (size_t)GM * GK * es));
-  CUDA_TRY(cudaMemset(B, 0, (size_t)GN * GK * es));
+  launch_fill_hash(c->dt, A, (size_t)GM * GK, 1u, c->s_full);
+  launch_fill_hash(c->dt, B, (size_t)GN * GK, 2u, c->s_full);
+  launch_fill_hash(DT::BF16, buf, n_bytes / 2, 3u, c->s_full);  // K/V pools of the bandwidth calibration
+  CUDA_TRY(cudaStreamSynchronize(c->s_full));
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));

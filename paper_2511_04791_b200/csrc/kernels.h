@@ -135,5 +135,7 @@ int launch_decode_advance(DT dt, const void* y, void* xin, void* y_out, int n, i
 // Streaming-read kernel for B_HBM(S) calibration: reads n_bytes, writes one word per CTA.
 int launch_stream_read(const void* buf, size_t n_bytes, unsigned long long* sink, int num_sms, cudaStream_t st);
 int launch_stream_pages(const void* buf, size_t n_bytes, unsigned long long* sink, int num_sms, cudaStream_t st);
+// hashed values in [-1, 1) (calibration operands)
+int launch_fill_hash(DT dt, void* p, size_t n_elems, uint32_t seed, cudaStream_t st);
 
 }  // namespace duet

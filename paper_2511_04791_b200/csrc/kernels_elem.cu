@@ -208,6 +208,29 @@ __global__ void __launch_bounds__(512) stream_read_kernel(const uint4* __restric
   if (acc == 0x9E3779B9u) sink[blockIdx.x] = acc;  // practically never taken; keeps the loads alive
 }
 
+// Calibration operands: hashed values in [-1, 1) (zeros would understate the tensor cores' power draw
+// and with it the clock the GPU sustains under real data)
+__global__ void fill_hash_kernel(uint16_t* p, size_t n, uint32_t seed, int is_bf16) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)i * 0x9E3779B1u ^ seed;
+    h ^= h >> 15;
+    h *= 0x85EBCA77u;
+    h ^= h >> 13;
+    const float v = (float)(h & 0xFFFF) / 32768.0f - 1.0f;
+    if (is_bf16) {
+      const bf16 b = __float2bfloat16_rn(v);
+      p[i] = *reinterpret_cast<const uint16_t*>(&b);
+    } else {
+      reinterpret_cast<float*>(p)[i] = v;
+    }
+  }
+}
+
+int launch_fill_hash(DT dt, void* p, size_t n_elems, uint32_t seed, cudaStream_t st) {
+  fill_hash_kernel<<<1184, 256, 0, st>>>((uint16_t*)p, n_elems, seed, dt == DT::BF16 ? 1 : 0);
+  return 1;
+}
+
 int launch_stream_read(const void* buf, size_t n_bytes, unsigned long long* sink, int num_sms, cudaStream_t st) {
   stream_read_kernel<<<num_sms * 4, 512, 0, st>>>((const uint4*)buf, n_bytes / 16, sink);
   return 1;
