@@ -311,9 +311,12 @@ struct AttnPlan {
   double attn_flops_pre = 0, attn_bytes_pre = 0, attn_flops_dec = 0, attn_bytes_dec = 0;
 };
 
+// x_in2 / y_final2 / row_split: rows >= row_split of the layer input / final output live in a second
+// buffer (the temporal batch [prefill ; decode] read and written in the caller's buffers, no copies)
 static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms, int n_rows, const void* x_in,
                               void* y_final, const duet_layer_weights* w, const duet_kv_pages* kv, const AttnPlan& ap,
-                              int* kernels) {
+                              int* kernels, const void* x_in2 = nullptr, void* y_final2 = nullptr,
+                              int row_split = 1 << 30) {
   const auto& sp = c->spec;
   const DT dt = c->dt;
   const size_t es = dt_size(dt);
@@ -358,7 +361,9 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     void* Y = l == sp.n_layers - 1 ? y_final : ((l & 1) ? S.xb : S.xa);
     const duet_layer_weights& W = w[l];
     // 1. h = RMSNorm(x) g1
-    TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e, launch_rmsnorm(dt, X, W.g_norm1, S.h, n_rows, d, eps, st));
+    TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e,
+          launch_rmsnorm(dt, X, W.g_norm1, S.h, n_rows, d, eps, st, l == 0 ? x_in2 : nullptr,
+                         l == 0 ? row_split : 1 << 30));
     // 2. qkv = h W_qkv^T (+ b)
     GemmArgs g{S.h, W.w_qkv, S.qkv, nullptr, W.b_qkv, n_rows, nqkv, d, d, d, nqkv, 0, EPI_STORE};
     with_ws(g);
@@ -439,6 +444,11 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     GemmArgs go{S.o, W.w_o, S.x1, lead ? X : nullptr, nullptr, n_rows, d, hq * dh, hq * dh, hq * dh, d, d,
                 lead ? EPI_RESIDUAL : EPI_STORE};
     with_ws(go);
+    if (l == 0 && row_split < n_rows) {
+      go.R2 = x_in2;
+      go.row_split = row_split;
+      go.C2 = (char*)S.x1 + (size_t)row_split * d * es;  // output stays in one buffer
+    }
     TIMED(DUET_KCLASS_GEMM, gemm_fl(d, hq * dh), gemm_by(d, hq * dh, d, true), launch_gemm(dt, go, num_sms, st));
     if (comm) TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, allreduce(S.x1));
     // 6. h2 = RMSNorm(x1) g2
@@ -451,6 +461,11 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     GemmArgs gd{S.act, W.w_down, Y, lead ? S.x1 : nullptr, nullptr, n_rows, d, m, m, m, d, d,
                 lead ? EPI_RESIDUAL : EPI_STORE};
     with_ws(gd);
+    if (l == sp.n_layers - 1 && row_split < n_rows) {
+      gd.C2 = y_final2;
+      gd.R2 = lead ? (const char*)S.x1 + (size_t)row_split * d * es : nullptr;
+      gd.row_split = row_split;
+    }
     TIMED(DUET_KCLASS_GEMM, gemm_fl(d, m), gemm_by(d, m, d, true), launch_gemm(dt, gd, num_sms, st));
     if (comm) TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, allreduce(Y));
   }
@@ -851,7 +866,23 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     CUDA_TRY(cudaEventRecord(c->ev_pre0, st));
     CUDA_TRY(cudaMemcpyAsync(c->pre.meta, img, n_int * sizeof(int), cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaEventRecord(c->stage_ev[slot], st));
-    if (n_rows > 0) {
+    // [prefill ; decode] rows straight from / into the caller's buffers when the CTA-pair GEMM runs
+    // the O and down projections (it reads the residual and writes the output per row range)
+    GemmArgs probe{};
+    probe.M = n_rows;
+    probe.N = d;
+    probe.K = d;
+    probe.lda = probe.ldb = probe.ldc = probe.ldr = d;
+    probe.epi = EPI_RESIDUAL;
+    const bool split_io = has_pre && has_dec && c->dt == DT::BF16 && gemm2_supported(probe, c->total_sms) &&
+                          c->spec.ffn_dim % 64 == 0 && (c->spec.n_q_heads * c->spec.head_dim) % 64 == 0;
+    if (n_rows > 0 && !(has_pre && has_dec)) {  // one phase only: its own buffers, whatever the GEMM path
+      DUET_TRY(run_layers(c, c->pre, st, c->total_sms, n_rows, has_pre ? pre->x : dec->x, has_pre ? pre->y : dec->y,
+                          w, kv, ap, &kernels));
+    } else if (n_rows > 0 && split_io) {
+      DUET_TRY(run_layers(c, c->pre, st, c->total_sms, n_rows, pre->x, pre->y, w, kv, ap, &kernels, dec->x, dec->y,
+                          ap.n_pre));
+    } else if (n_rows > 0) {
       if (has_pre) CUDA_TRY(cudaMemcpyAsync(c->pre.xin, pre->x, (size_t)ap.n_pre * d * es, cudaMemcpyDeviceToDevice, st));
       if (has_dec)
         CUDA_TRY(cudaMemcpyAsync((char*)c->pre.xin + (size_t)ap.n_pre * d * es, dec->x, (size_t)ap.n_dec * d * es,

@@ -31,6 +31,12 @@ struct GemmArgs {
   // A split launch is two kernels (GEMM writing partials, then an ordered reduction + epilogue).
   float* ws = nullptr;
   size_t ws_floats = 0;
+  // rows >= row_split read the residual from R2 and store to C2 (row - row_split), same pitches: the
+  // temporal batch [prefill rows ; decode rows] without copying it between the caller's buffers
+  // (CTA-pair kernel only; kernels.h gemm2_supported)
+  const void* R2 = nullptr;
+  void* C2 = nullptr;
+  int row_split = 1 << 30;
 };
 // fp32 partial floats a split-K launch of this shape needs (0 when it runs unsplit)
 size_t gemm_tc_splitk_need(int M, int N, int K, int epi);
@@ -47,7 +53,8 @@ int launch_gemm2(const GemmArgs& a, int num_sms, cudaStream_t st);
 
 // ---------------------------------------------------------------- RMSNorm
 // h[n][d] = x * rsqrt(mean(x^2) + eps) * g     (reading #1)
-int launch_rmsnorm(DT dt, const void* x, const void* g, void* h, int n, int d, float eps, cudaStream_t st);
+int launch_rmsnorm(DT dt, const void* x, const void* g, void* h, int n, int d, float eps, cudaStream_t st,
+                   const void* x2 = nullptr, int row_split = 1 << 30);  // rows >= row_split from x2
 
 // ---------------------------------------------------------------- RoPE + paged KV append
 // qkv rows [n][(hq + 2 hkv) dh]; row i at position pos[i], page-table row tok_row[i].

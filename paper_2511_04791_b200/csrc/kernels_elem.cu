@@ -10,10 +10,11 @@ namespace duet {
 // One CTA per row; 16-byte vector loads; fp32 sum of squares; h stored in T.
 template <typename T, int THREADS>
 __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const T* __restrict__ x, const T* __restrict__ g,
-                                                          T* __restrict__ h, int d, float eps) {
+                                                          T* __restrict__ h, int d, float eps, const T* __restrict__ x2,
+                                                          int row_split) {
   constexpr int E = 16 / sizeof(T);
   const int row = blockIdx.x;
-  const T* xr = x + (size_t)row * d;
+  const T* xr = row < row_split ? x + (size_t)row * d : x2 + (size_t)(row - row_split) * d;
   T* hr = h + (size_t)row * d;
   const int nv = d / E;
   float ss = 0.f;
@@ -44,12 +45,15 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const T* __restrict__ 
   }
 }
 
-int launch_rmsnorm(DT dt, const void* x, const void* g, void* h, int n, int d, float eps, cudaStream_t st) {
+int launch_rmsnorm(DT dt, const void* x, const void* g, void* h, int n, int d, float eps, cudaStream_t st,
+                   const void* x2, int row_split) {
   if (n <= 0) return 0;
   if (dt == DT::BF16)
-    rmsnorm_kernel<bf16, 256><<<n, 256, 0, st>>>((const bf16*)x, (const bf16*)g, (bf16*)h, d, eps);
+    rmsnorm_kernel<bf16, 256><<<n, 256, 0, st>>>((const bf16*)x, (const bf16*)g, (bf16*)h, d, eps, (const bf16*)x2,
+                                                 row_split);
   else
-    rmsnorm_kernel<float, 256><<<n, 256, 0, st>>>((const float*)x, (const float*)g, (float*)h, d, eps);
+    rmsnorm_kernel<float, 256><<<n, 256, 0, st>>>((const float*)x, (const float*)g, (float*)h, d, eps,
+                                                  (const float*)x2, row_split);
   return 1;
 }
 

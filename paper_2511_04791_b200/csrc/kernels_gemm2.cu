@@ -127,6 +127,9 @@ struct Params {
   const bf16* bias;
   int ldc, ldr;
   int n_up_off;  // SwiGLU: row offset of the up rows in W (= N)
+  const bf16* R2;
+  bf16* C2;
+  int row_split;  // rows >= row_split: residual from R2, output to C2 (row - row_split)
 };
 
 template <int EPI>
@@ -247,10 +250,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int e = 0; e < 32; ++e) v[e] = silu_f(v[e]) * u[e];
         }
         if (row < p.M && n0 + c < p.N) {
-          bf16* dst = p.C + (size_t)row * p.ldc + n0 + c;
+          const bool hi = row >= p.row_split;
+          const int rrow = hi ? row - p.row_split : row;
+          bf16* dst = (hi ? p.C2 : p.C) + (size_t)rrow * p.ldc + n0 + c;
+          const bf16* rbase = hi ? p.R2 : p.R;
           if (n0 + c + 32 <= p.N) {
             if constexpr (EPI == EPI_RESIDUAL) {
-              const bf16* rsrc = p.R + (size_t)row * p.ldr + n0 + c;
+              const bf16* rsrc = rbase + (size_t)rrow * p.ldr + n0 + c;
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 float rf[8];
@@ -281,7 +287,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             for (int e = 0; e < 32; ++e) {
               if (n0 + c + e >= p.N) continue;
               float o = v[e];
-              if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(p.R[(size_t)row * p.ldr + n0 + c + e]);
+              if constexpr (EPI == EPI_RESIDUAL) o += __bfloat162float(rbase[(size_t)rrow * p.ldr + n0 + c + e]);
               if constexpr (EPI == EPI_STORE)
                 if (p.bias) o += __bfloat162float(p.bias[n0 + c + e]);
               dst[e] = __float2bfloat16_rn(o);
@@ -351,6 +357,9 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   p.ldc = a.ldc;
   p.ldr = a.ldr;
   p.n_up_off = a.N;
+  p.R2 = (const bf16*)a.R2;
+  p.C2 = (bf16*)a.C2;
+  p.row_split = a.row_split;
   const int pairs = p.num_tiles < num_sms / 2 ? p.num_tiles : num_sms / 2;
   gemm2_kernel<EPI><<<2 * pairs, THREADS, SMEM, st>>>(mx, mw, p);
   return 1;
