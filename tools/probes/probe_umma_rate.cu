@@ -19,6 +19,7 @@ __global__ void k(int reps, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar2;
   const int warp = threadIdx.x / 32;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&slot)));
@@ -26,6 +27,7 @@ __global__ void k(int reps, unsigned long long* out) {
   }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar2)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -38,7 +40,19 @@ __global__ void k(int reps, unsigned long long* out) {
     constexpr uint32_t ID = MODE >= 2 ? (idesc(M, N) | (1u << 16)) : idesc(M, N);
     for (int i = 0; i < reps; ++i) {
       const uint32_t off = MODE == 0 ? (i & 3) * 32 : ((i * 7) & 7) * 1024 + (i & 3) * 32;
-      if (MODE == 3) {
+      if (MODE == 4) {  // FA-like mix: 8 SS UMMAs into D0, then 8 TS UMMAs (A = TMEM cols 384+) into D1
+        if ((i >> 3) & 1)
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 128),
+                       "r"(tmem + 384 + (i & 7) * 8), "l"(desc(b + off)), "r"(ID | (1u << 16)), "r"(i & 7));
+        else
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                       "l"(desc(a + off)), "l"(desc(b + off)), "r"(ID), "r"(i & 7));
+      } else if (MODE == 5) {  // FA-like mix with a commit after every 8 UMMAs
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + ((i >> 3) & 1) * 128),
+                     "l"(desc(a + off)), "l"(desc(b + off)), "r"(ID), "r"(i & 7));
+        if ((i & 7) == 7)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar2)) : "memory");
+      } else if (MODE == 3) {
         asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem),
                      "r"(tmem + 128 + (i & 3) * 8), "l"(desc(b + off)), "r"(ID), "r"(i & 1));
       } else {
@@ -88,5 +102,7 @@ int main() {
   run<128, 128, 2>(d);
   run<128, 128, 3>(d);
   run<128, 256, 3>(d);
+  run<128, 128, 4>(d);
+  run<128, 128, 5>(d);
   return 0;
 }
