@@ -8,6 +8,31 @@ namespace duet {
 
 using bf16 = __nv_bfloat16;
 
+// Programmatic dependent launch: hot-path kernels are launched with programmatic stream serialization
+// (launch_pdl), so a kernel's launch and set-up (barrier init, TMEM allocation, descriptor prefetch)
+// overlap the previous kernel's tail; every such kernel calls pdl_wait() before it reads anything the
+// previous kernel wrote (griddepcontrol.wait: no-op when launched without the attribute).
+// No explicit launch_dependents: the trigger is implicit at each CTA's exit, so a dependent grid's CTAs
+// never sit on SMs next to a running grid (an early trigger measured 2 % slower: waiting CTAs
+// co-resident with the persistent GEMMs).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 template <typename T> __device__ __forceinline__ float to_f(T v);
 template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
 template <> __device__ __forceinline__ float to_f<bf16>(bf16 v) { return __bfloat162float(v); }

@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(DecodeAttnArgs a, int 
 // LSE combine of the split partials: o = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
 template <typename T>
 __global__ void attn_combine_kernel(DecodeAttnArgs a, int n_splits) {
+  pdl_wait();
   const int rh = blockIdx.x;  // r * hq + head
   const size_t base = (size_t)rh * a.max_splits;
   float M = -INFINITY;
@@ -238,7 +239,7 @@ int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st) {
   }
   if (!ok) return -1;
   if (ns > 1) {
-    if (dt == DT::BF16) attn_combine_kernel<bf16><<<a.n * a.hq, 128, 0, st>>>(a, ns);
+    if (dt == DT::BF16) launch_pdl(attn_combine_kernel<bf16>, a.n * a.hq, 128, 0, st, a, ns);
     else attn_combine_kernel<float><<<a.n * a.hq, 128, 0, st>>>(a, ns);
     return 2;
   }

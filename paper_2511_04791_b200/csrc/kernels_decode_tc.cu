@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
   constexpr int WARP_BYTES = NST * STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  pdl_wait();
   const int split = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.hq / a.hkv;
@@ -387,7 +388,7 @@ static void launch_variant(const CUtensorMap& mk, const CUtensorMap& mv, const D
     attr = true;
   }
   dim3 grid(n_splits, a.hkv, a.n);
-  dtc::decode_tc_kernel<W, N, T><<<grid, 32 * W, smem, st>>>(mk, mv, a, pps, n_splits);
+  launch_pdl(dtc::decode_tc_kernel<W, N, T>, grid, 32 * W, smem, st, mk, mv, a, pps, n_splits);
 }
 
 int launch_decode_tc(const DecodeAttnArgs& a, int pps, int n_splits, cudaStream_t st) {

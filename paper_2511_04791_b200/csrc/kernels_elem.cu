@@ -13,6 +13,7 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const T* __restrict__ 
                                                           T* __restrict__ h, int d, float eps, const T* __restrict__ x2,
                                                           int row_split) {
   constexpr int E = 16 / sizeof(T);
+  pdl_wait();
   const int row = blockIdx.x;
   const T* xr = row < row_split ? x + (size_t)row * d : x2 + (size_t)(row - row_split) * d;
   T* hr = h + (size_t)row * d;
@@ -49,8 +50,8 @@ int launch_rmsnorm(DT dt, const void* x, const void* g, void* h, int n, int d, f
                    const void* x2, int row_split) {
   if (n <= 0) return 0;
   if (dt == DT::BF16)
-    rmsnorm_kernel<bf16, 256><<<n, 256, 0, st>>>((const bf16*)x, (const bf16*)g, (bf16*)h, d, eps, (const bf16*)x2,
-                                                 row_split);
+    launch_pdl(rmsnorm_kernel<bf16, 256>, n, 256, 0, st, (const bf16*)x, (const bf16*)g, (bf16*)h, d, eps,
+               (const bf16*)x2, row_split);
   else
     rmsnorm_kernel<float, 256><<<n, 256, 0, st>>>((const float*)x, (const float*)g, (float*)h, d, eps,
                                                   (const float*)x2, row_split);
@@ -110,6 +111,7 @@ __global__ void rope_kv_kernel(RopeKvArgs a) {
 // bf16, vectorized: one work item = 8 consecutive rotation pairs of one q/k head (two 16-B loads, a
 // 64-B cos/sin load, two 16-B stores) or 8 elements of one v head (one 16-B copy).
 __global__ void __launch_bounds__(256) rope_kv_vec_kernel(RopeKvArgs a) {
+  pdl_wait();
   const int row = blockIdx.x;
   const int half = a.dh / 2, hv = half / 8, vv = a.dh / 8;
   bf16* qkv = reinterpret_cast<bf16*>(a.qkv) + (size_t)row * (a.hq + 2 * a.hkv) * a.dh;
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(256) rope_kv_vec_kernel(RopeKvArgs a) {
 int launch_rope_kv(DT dt, const RopeKvArgs& a, cudaStream_t st) {
   if (a.n <= 0) return 0;
   if (dt == DT::BF16 && !a.bias && a.dh % 16 == 0)
-    rope_kv_vec_kernel<<<a.n, 256, 0, st>>>(a);
+    launch_pdl(rope_kv_vec_kernel, a.n, 256, 0, st, a);
   else if (dt == DT::BF16)
     rope_kv_kernel<bf16><<<a.n, 256, 0, st>>>(a);
   else

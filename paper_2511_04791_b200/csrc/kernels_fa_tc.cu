@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // set-up above overlaps the previous kernel's tail
   // timeline debugging (DUET_FA_TRACE=1): event e of tile j, clock() relative to kernel start
   uint32_t* trace = (uint32_t*)(smem + OFF_TRACE);
   const bool tr = (p.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
@@ -555,7 +556,7 @@ int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   // (timing experiment, garbage output); "tn" does both
   p.trace = trace ? (trace[0] == 'n' ? 2 : (trace[0] == 't' && trace[1] == 'n' ? 3 : 1)) : 0;
   dim3 grid(p.n_pairs, p.n_qtiles, a.n_seqs);
-  fatc::fa_tc_kernel<<<grid, fatc::THREADS, fatc::SMEM, st>>>(mq, p);
+  launch_pdl(fatc::fa_tc_kernel, grid, fatc::THREADS, fatc::SMEM, st, mq, p);
   return 1;
 }
 

@@ -172,6 +172,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync();  // barriers initialised and TMEM allocated in both CTAs before any remote access
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // set-up above overlaps the previous kernel's tail; its outputs are read below
 
   if (warp == 0) {
     if (lane == 0) {
@@ -361,7 +362,7 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   p.C2 = (bf16*)a.C2;
   p.row_split = a.row_split;
   const int pairs = p.num_tiles < num_sms / 2 ? p.num_tiles : num_sms / 2;
-  gemm2_kernel<EPI><<<2 * pairs, THREADS, SMEM, st>>>(mx, mw, p);
+  launch_pdl(gemm2_kernel<EPI>, 2 * pairs, THREADS, SMEM, st, mx, mw, p);
   return 1;
 }
 

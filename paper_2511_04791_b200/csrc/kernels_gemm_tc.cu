@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // set-up above overlaps the previous kernel's tail
 
   if (warp == 0 || warp >= 6) {
     if (lane == 0) {
@@ -428,6 +429,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
 // in flight; then applies the fused epilogue and stores 4 bf16 (8 B) per thread per column.
 template <int EPI>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(Params p, int bn, int acc_cols) {
+  pdl_wait();
   const int t = blockIdx.x;
   const int mb = t % p.num_m, nb = t / p.num_m;
   const int rq = threadIdx.x & 31, cg = threadIdx.x >> 5;
@@ -592,9 +594,9 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   p.ldr = a.ldr;
   p.n_up_off = a.N;
   const int grid = p.num_units < CF::CTAS * num_sms ? p.num_units : CF::CTAS * num_sms;
-  gemm_tc_kernel<BN, EPI, SWAP><<<grid, CF::THREADS, CF::SMEM, st>>>(mx, mw, p);
+  launch_pdl(gemm_tc_kernel<BN, EPI, SWAP>, grid, CF::THREADS, CF::SMEM, st, mx, mw, p);
   if (p.ksplit > 1) {
-    splitk_reduce_kernel<EPI><<<p.num_tiles, 256, 0, st>>>(p, BN, CF::ACC_COLS);
+    launch_pdl(splitk_reduce_kernel<EPI>, p.num_tiles, 256, 0, st, p, BN, (int)CF::ACC_COLS);
     return 2;
   }
   return 1;
