@@ -335,20 +335,22 @@ def main():
             return D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1)
         return D.duet_choose_split(spec, hw, batch, tau, k_max, opts)
 
-    def prefill_arg():
-        return dict(q=[q for q, _ in wl.pre_seqs], c=[c for _, c in wl.pre_seqs], table=wl.pre_tables, x=x_pre,
-                    y=y_pre)
+    def prefill_arg(bufs=None):
+        xp, yp = (x_pre, y_pre) if bufs is None else (bufs[0], bufs[2])
+        return dict(q=[q for q, _ in wl.pre_seqs], c=[c for _, c in wl.pre_seqs], table=wl.pre_tables, x=xp, y=yp)
 
-    def decode_arg(k):
-        return dict(c=wl.dec_ctx, table=wl.dec_tables, x=x_dec, y=y_dec[:k])
+    def decode_arg(k, bufs=None):
+        xd, yd = (x_dec, y_dec) if bufs is None else (bufs[1], bufs[3])
+        return dict(c=wl.dec_ctx, table=wl.dec_tables, x=xd, y=yd[:k])
 
-    def one_step(split=None):
+    def one_step(split=None, bufs=None):
+        """bufs: optional (x_pre, x_dec, y_pre, y_dec) device buffers (the e2e double buffering)."""
         s = decide() if split is None else split
         k = s.k if s.mode == D.DUET_MODE_SPATIAL else 1
         if k > 8:
             s = D.split_struct(s.mode, s.s_p, s.s_d, 8, s.flags, s.t_mixed, s.t_p, s.t_d, s.rho)
             k = 8
-        ctx.step(W, prefill_arg(), decode_arg(k), Kp, Vp, wl.n_pages, s)
+        ctx.step(W, prefill_arg(bufs), decode_arg(k, bufs), Kp, Vp, wl.n_pages, s)
         return s, k
 
     stream = torch.cuda.current_stream()
@@ -473,20 +475,45 @@ def main():
         hy_pre = torch.empty(y_pre.shape, dtype=tdt, pin_memory=True)
         hy_dec = torch.empty(y_dec.shape, dtype=tdt, pin_memory=True)
         n_e2e = max(5, args.steps // 2)
+        # The caller's view: every step's inputs come from pinned host memory and its outputs go back to
+        # it.  Two device buffer sets and a copy stream overlap step i's compute with the H2D of step
+        # i+1 and the D2H of step i-1 (PCIe is full duplex); every copy is inside the timed region.
+        bufs = [(x_pre, x_dec, y_pre, y_dec),
+                (torch.empty_like(x_pre), torch.empty_like(x_dec), torch.empty_like(y_pre), torch.empty_like(y_dec))]
+        cs = torch.cuda.Stream()    # H2D
+        cs2 = torch.cuda.Stream()   # D2H (the other PCIe direction, concurrently)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_d2h = [torch.cuda.Event() for _ in range(2)]
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tok = 0
         h2d = d2h = 0
-        a.record(stream)
-        for _ in range(n_e2e):
-            x_pre.copy_(hx_pre, non_blocking=True)
-            x_dec.copy_(hx_dec, non_blocking=True)
-            s_, k_ = one_step()
-            hy_pre.copy_(y_pre, non_blocking=True)
-            hy_dec[:k_].copy_(y_dec[:k_], non_blocking=True)
+        torch.cuda.synchronize()
+        a.record(cs)
+        for i in range(n_e2e):
+            st_ = i % 2
+            xp, xd, yp, yd = bufs[st_]
+            with torch.cuda.stream(cs):
+                if i >= 2:
+                    cs.wait_event(ev_out[st_])      # step i-2 has finished reading x of this set
+                xp.copy_(hx_pre, non_blocking=True)
+                xd.copy_(hx_dec, non_blocking=True)
+                ev_in[st_].record(cs)
+            stream.wait_event(ev_in[st_])
+            if i >= 2:
+                stream.wait_event(ev_d2h[st_])      # step i-2's outputs of this set are on the host
+            s_, k_ = one_step(bufs=bufs[st_])
+            ev_out[st_].record(stream)
+            with torch.cuda.stream(cs2):
+                cs2.wait_event(ev_out[st_])
+                hy_pre.copy_(yp, non_blocking=True)
+                hy_dec[:k_].copy_(yd[:k_], non_blocking=True)
+                ev_d2h[st_].record(cs2)
             tok += k_ * n_d + n_p
             h2d = hx_pre.numel() * hx_pre.element_size() + hx_dec.numel() * hx_dec.element_size()
             d2h = hy_pre.numel() * hy_pre.element_size() + k_ * n_d * m.d_model * hy_dec.element_size()
-        b.record(stream)
+        cs.wait_stream(cs2)
+        b.record(cs)
         torch.cuda.synchronize()
         te = max_over_ranks(a.elapsed_time(b), ws)
         e2e = {"value": tok * (1 if tp > 1 else ws) / (te * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
