@@ -207,11 +207,25 @@ typedef struct {
   void* y;
 } duet_prefill;
 
+/* Optional LM head of the decode side (P:250 t_cls, P:335 sampled tokens): after
+ * the last layer of every decode step, h = RMSNorm(y) * g_norm, logits = h . w_head^T (bf16, fp32
+ * accumulation), token = argmax (greedy; the lowest index among equal maxima), and the next step's
+ * input is embed[token] instead of y (closing the look-ahead window into an autoregressive loop).
+ *  g_norm: device [d]; w_head: device [vocab][d] (nn.Linear layout); embed: device [vocab][d];
+ *  tokens: device int32 [k][n_reqs] output.  All of the ctx dtype, vocab = spec->vocab; bf16 ctx only. */
+typedef struct {
+  const void* g_norm;
+  const void* w_head;
+  const void* embed;
+  int32_t* tokens;
+} duet_lm_head;
+
 /* Decode side (R_decode) for a look-ahead window of k steps.
  *  c: host [n_reqs] cached tokens before step 1; step j (1..k) is at position c + j - 1.
  *  page_table: host [n_reqs][max_pages]; must cover c + k tokens (look-ahead slots).
- *  x: device [n_reqs][d] step-1 input; y: device [k][n_reqs][d] per-step outputs.  Step j>1
- *  takes step j-1's last-layer output as input (reading #26). */
+ *  x: device [n_reqs][d] step-1 input; y: device [k][n_reqs][d] per-step last-layer outputs.
+ *  head == NULL: step j>1 takes step j-1's last-layer output as input (synthetic feedback,
+ *  reading #26); otherwise the greedy token's embedding (duet_lm_head). */
 typedef struct {
   int32_t n_reqs;
   const int32_t* c;
@@ -219,6 +233,7 @@ typedef struct {
   int32_t max_pages;
   const void* x;
   void* y;
+  const duet_lm_head* head;
 } duet_decode;
 
 /* Paged KV cache (vLLM-style pages).  k_pool / v_pool: host arrays of

@@ -14,7 +14,8 @@ DESIGN.md §Readings (numbered as in SURVEY.md §8(c) C-7):
   #6  q-head j reads kv-head floor(j / (h_q/h_kv));
   #7  causal with a prefix: the token at absolute position p attends to every t <= p;
   #26 decode step j>1 of a look-ahead window takes the previous step's final-layer
-      output as its input (synthetic feedback; P:335 samples tokens instead).
+      output as its input (synthetic feedback; P:335 samples tokens instead) — or, with an LM
+      head, the embedding of the previous step's greedy token.
 
 The KV cache is "concatenate then attend": every new token's (k, v)
 is appended to its page slot before any attention of the same call reads it.
@@ -221,11 +222,21 @@ def prefill_forward(m: Model, weights: list, x: np.ndarray, seqs: list, tables: 
     return h
 
 
+def lm_head_greedy(m: Model, head: dict, y: np.ndarray):
+    """Greedy next token of each row (P:250 t_cls, P:335 'sampled tokens'):
+    h = RMSNorm(y) * g_final; logits = h W_head^T; token = argmax (the lowest index among equal
+    maxima).  Returns (logits [n, vocab], tokens [n])."""
+    h = rmsnorm(np.asarray(y, dtype=np.float64), head["g_norm"], m.norm_eps)
+    logits = h @ np.asarray(head["w_head"], dtype=np.float64).T
+    return logits, np.argmax(logits, axis=1)   # numpy returns the first maximum
+
+
 def decode_window(m: Model, weights: list, x: np.ndarray, ctx: list, tables: np.ndarray,
-                  kv: PagedKV, k: int) -> np.ndarray:
+                  kv: PagedKV, k: int, head: dict | None = None, tokens_out: list | None = None) -> np.ndarray:
     """k look-ahead decode steps (P:335).  Step j (1-based) of request r is at position c_r + j - 1;
-    its input is x for j = 1 and the previous step's final-layer output otherwise (reading #26).
-    Returns y [k, n_req, d]."""
+    its input is x for j = 1; otherwise the previous step's final-layer output (synthetic feedback,
+    reading #26) or, with an LM head, the embedding of the previous step's greedy token (f1).
+    Returns y [k, n_req, d]; with a head, tokens_out receives (logits, tokens) of every step."""
     n = len(ctx)
     out = np.empty((k, n, m.d_model), dtype=np.float64)
     h_in = np.asarray(x, dtype=np.float64)
@@ -236,7 +247,13 @@ def decode_window(m: Model, weights: list, x: np.ndarray, ctx: list, tables: np.
         for l, w in enumerate(weights):
             h = layer_forward(m, w, l, h, pos, trows, kv)
         out[j - 1] = h
-        h_in = h
+        if head is None:
+            h_in = h
+        else:
+            logits, tok = lm_head_greedy(m, head, h)
+            if tokens_out is not None:
+                tokens_out.append((logits, tok))
+            h_in = np.asarray(head["embed"], dtype=np.float64)[tok]
     return out
 
 

@@ -67,9 +67,13 @@ class duet_prefill(C.Structure):
                 ("page_table", C.POINTER(C.c_int32)), ("max_pages", C.c_int32), ("x", C.c_void_p), ("y", C.c_void_p)]
 
 
+class duet_lm_head(C.Structure):
+    _fields_ = [("g_norm", C.c_void_p), ("w_head", C.c_void_p), ("embed", C.c_void_p), ("tokens", C.c_void_p)]
+
+
 class duet_decode(C.Structure):
     _fields_ = [("n_reqs", C.c_int32), ("c", C.POINTER(C.c_int32)), ("page_table", C.POINTER(C.c_int32)),
-                ("max_pages", C.c_int32), ("x", C.c_void_p), ("y", C.c_void_p)]
+                ("max_pages", C.c_int32), ("x", C.c_void_p), ("y", C.c_void_p), ("head", C.POINTER(duet_lm_head))]
 
 
 class duet_kv_pages(C.Structure):
@@ -265,7 +269,13 @@ class Ctx:
             c, cp = _i32(decode["c"])
             t, tp = _i32(decode["table"])
             keep += [c, t]
-            dec_s = duet_decode(len(c), cp, tp, t.shape[1], _ptr(decode["x"]), _ptr(decode["y"]))
+            head_p = None
+            if decode.get("head") is not None:   # dict(g_norm, w_head, embed, tokens) of device tensors (f1)
+                hd = decode["head"]
+                hs = duet_lm_head(_ptr(hd["g_norm"]), _ptr(hd["w_head"]), _ptr(hd["embed"]), _ptr(hd["tokens"]))
+                keep.append(hs)
+                head_p = C.pointer(hs)
+            dec_s = duet_decode(len(c), cp, tp, t.shape[1], _ptr(decode["x"]), _ptr(decode["y"]), head_p)
         kp = (C.c_void_p * L)(*[p.data_ptr() for p in kv_k])
         vp = (C.c_void_p * L)(*[p.data_ptr() for p in kv_v])
         kv = duet_kv_pages(kp, vp, int(n_pages), 16)

@@ -142,6 +142,7 @@ struct Side {
   int* meta = nullptr;  // [pos | tok_row | row0 | qlen | cpre | seq_row | step | table]
   float *part_o = nullptr, *part_ml = nullptr;
   int part_rows = 0;
+  void* logits = nullptr;    // LM head (f1): [decode rows][vocab]
   float* gemm_ws = nullptr;  // split-K partials of the weight-streaming GEMMs (kernels.h GemmArgs)
   size_t gemm_ws_floats = 0;
   // offsets into meta (ints)
@@ -251,6 +252,9 @@ static duet_status side_alloc(duet_ctx* c, Side& s, int cap_rows, int cap_seqs, 
     for (auto& sh : shapes) s.gemm_ws_floats = std::max(s.gemm_ws_floats, gemm_tc_splitk_need(M, sh[0], sh[1], sh[2]));
   }
   if (s.gemm_ws_floats > 0) CUDA_TRY(cudaMalloc(&s.gemm_ws, s.gemm_ws_floats * sizeof(float)));
+  // LM head logits of the decode rows (f1), bf16 contexts with a vocabulary
+  if (c->dt == DT::BF16 && sp.vocab > 0 && c->lim.max_decode_reqs > 0)
+    CUDA_TRY(cudaMalloc(&s.logits, (size_t)c->lim.max_decode_reqs * sp.vocab * es));
   size_t off = 0;
   s.o_pos = off; off += R;
   s.o_tok = off; off += R;
@@ -267,7 +271,7 @@ static duet_status side_alloc(duet_ctx* c, Side& s, int cap_rows, int cap_seqs, 
 }
 
 static void side_free(Side& s) {
-  void* ptrs[] = {s.xa, s.xb, s.h, s.x1, s.h2, s.xin, s.ylast, s.qkv, s.o, s.act, s.part_o, s.part_ml, s.meta, s.gemm_ws};
+  void* ptrs[] = {s.xa, s.xb, s.h, s.x1, s.h2, s.xin, s.ylast, s.qkv, s.o, s.act, s.part_o, s.part_ml, s.meta, s.gemm_ws, s.logits};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   s = Side{};
@@ -718,6 +722,13 @@ static duet_status validate_step(duet_ctx* c, const duet_layer_weights* w, const
     if (dec->n_reqs > c->lim.max_decode_reqs)
       DUET_FAIL(DUET_ERR_CAPACITY, "n_reqs = %d > max_decode_reqs %d", dec->n_reqs, c->lim.max_decode_reqs);
     if (!dec->c || !dec->page_table || !dec->x || !dec->y) DUET_FAIL(DUET_ERR_INVALID_ARG, "decode: a pointer is NULL");
+    if (dec->head) {
+      if (!dec->head->g_norm || !dec->head->w_head || !dec->head->embed || !dec->head->tokens)
+        DUET_FAIL(DUET_ERR_INVALID_ARG, "decode: an LM-head pointer is NULL");
+      if (c->dt != DT::BF16 || c->spec.vocab <= 0 || c->spec.vocab % 8 || !c->dec.logits)
+        DUET_FAIL(DUET_ERR_UNSUPPORTED, "the LM head needs a bf16 context with vocab %% 8 == 0 (vocab = %d)",
+                  c->spec.vocab);
+    }
     if (k > c->lim.max_k) DUET_FAIL(DUET_ERR_CAPACITY, "k = %d > max_k %d", k, c->lim.max_k);
     for (int r = 0; r < dec->n_reqs; ++r) {
       if (dec->c[r] < 1) DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "decode request %d: c = %d must be >= 1", r, dec->c[r]);
@@ -798,7 +809,8 @@ static size_t build_meta(duet_ctx* c, const Side& S, int* img, const duet_prefil
   return S.o_table + (size_t)(n_seqs + n_dec) * S.pitch;
 }
 
-static uint64_t hash_ptrs(const duet_layer_weights* w, int L, const duet_kv_pages* kv, const void* y, int maxlen_bucket) {
+static uint64_t hash_ptrs(const duet_layer_weights* w, int L, const duet_kv_pages* kv, const void* y, int maxlen_bucket,
+                          const duet_lm_head* head = nullptr) {
   uint64_t h = 1469598103934665603ull;
   auto mix = [&](const void* p) {
     h ^= (uint64_t)(uintptr_t)p;
@@ -809,20 +821,51 @@ static uint64_t hash_ptrs(const duet_layer_weights* w, int L, const duet_kv_page
     mix(w[l].g_norm1); mix(w[l].g_norm2); mix(kv->k_pool[l]); mix(kv->v_pool[l]);
   }
   mix(y);
+  if (head) {
+    mix(head->g_norm); mix(head->w_head); mix(head->embed); mix(head->tokens);
+  }
   h ^= (uint64_t)maxlen_bucket * 0x9E3779B97F4A7C15ull;
   return h;
+}
+
+// LM head over n rows y (f1, P:250 t_cls): RMSNorm with the final gain, logits = h w_head^T (the
+// weight-streaming GEMM), greedy token + embedding of the next input (x_next may be NULL).
+static duet_status lm_head(duet_ctx* c, Side& S, cudaStream_t st, int num_sms, int n, const void* y,
+                           const duet_lm_head* head, void* x_next, const int* step, int* kernels) {
+  const int d = c->spec.d_model, V = c->spec.vocab;
+  const size_t e = dt_size(c->dt);
+  int nk = 0;
+  int pi = prof_begin(c, st, DUET_KCLASS_OTHER);
+  nk += launch_rmsnorm(c->dt, y, head->g_norm, S.h, n, d, (float)c->spec.norm_eps, st);
+  prof_end(c, st, pi, DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e);
+  GemmArgs g{S.h, head->w_head, S.logits, nullptr, nullptr, n, V, d, d, d, V, 0, EPI_STORE};
+  g.ws = S.gemm_ws;
+  g.ws_floats = S.gemm_ws_floats;
+  pi = prof_begin(c, st, DUET_KCLASS_GEMM);
+  nk += launch_gemm(c->dt, g, num_sms, st);
+  prof_end(c, st, pi, DUET_KCLASS_GEMM, 2.0 * n * (double)V * d, ((double)n * d + (double)V * d + (double)n * V) * e);
+  pi = prof_begin(c, st, DUET_KCLASS_OTHER);
+  nk += launch_argmax_embed(S.logits, V, head->embed, x_next, d, head->tokens, step, n, st);
+  prof_end(c, st, pi, DUET_KCLASS_OTHER, 0.0, ((double)n * V + (x_next ? 2.0 * n * d : 0.0)) * e);
+  if (nk < 0) DUET_FAIL(DUET_ERR_CUDA, "LM head launch failed");
+  DUET_TRY(check_launch("lm head"));
+  *kernels += nk;
+  return DUET_OK;
 }
 
 // One decode step on the decode side (all layers + advance), launched on st.
 static duet_status decode_step_kernels(duet_ctx* c, cudaStream_t st, int num_sms, const duet_layer_weights* w,
                                        const duet_kv_pages* kv, const AttnPlan& meta, int max_len, void* y_out,
-                                       int* kernels) {
+                                       const duet_lm_head* head, int* kernels) {
   Side& S = c->dec;
   const int n = meta.n_dec;
   AttnPlan ap = meta;  // work counts of step 1 (timing statistics only)
   ap.max_len_dec = max_len;
   DUET_TRY(run_layers(c, S, st, num_sms, n, S.xin, S.ylast, w, kv, ap, kernels));
-  *kernels += launch_decode_advance(c->dt, S.ylast, S.xin, y_out, n, c->spec.d_model, S.pos(), S.step(), st);
+  // with an LM head the next input is the greedy token's embedding (f1), else the output (reading #26)
+  if (head) DUET_TRY(lm_head(c, S, st, num_sms, n, S.ylast, head, S.xin, S.step(), kernels));
+  *kernels += launch_decode_advance(c->dt, S.ylast, head ? nullptr : S.xin, y_out, n, c->spec.d_model, S.pos(),
+                                    S.step(), st);
   DUET_TRY(check_launch("decode advance"));
   return DUET_OK;
 }
@@ -893,6 +936,9 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
         CUDA_TRY(cudaMemcpyAsync(dec->y, (char*)c->pre.ylast + (size_t)ap.n_pre * d * es, (size_t)ap.n_dec * d * es,
                                  cudaMemcpyDeviceToDevice, st));
     }
+    // the decode rows' greedy tokens (f1; k = 1 in temporal mode): from their outputs in dec->y
+    if (has_dec && dec->head) DUET_TRY(lm_head(c, c->pre, st, c->total_sms, ap.n_dec, dec->y, dec->head, nullptr,
+                                               nullptr, &kernels));
     CUDA_TRY(cudaEventRecord(c->ev_pre1, st));
     CUDA_TRY(cudaStreamWaitEvent(ust, c->ev_pre1, 0));
     c->last_kernels = kernels;
@@ -926,9 +972,10 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     const int max_len = ((max_c + k + 1023) / 1024) * 1024;  // bucket: graphs survive context growth
     if (c->lim.flags & DUET_CTX_NO_GRAPH) {
       for (int j = 0; j < k; ++j)
-        DUET_TRY(decode_step_kernels(c, st, P->s_d, w, kv, ap, max_len, dec->y, &kernels));
+        DUET_TRY(decode_step_kernels(c, st, P->s_d, w, kv, ap, max_len, dec->y, dec->head, &kernels));
     } else {
-      auto key = std::make_tuple(P->s_d, n, c->spec.n_layers, hash_ptrs(w, c->spec.n_layers, kv, dec->y, max_len));
+      auto key = std::make_tuple(P->s_d, n, c->spec.n_layers, hash_ptrs(w, c->spec.n_layers, kv, dec->y, max_len,
+                                                                      dec->head));
       auto it = c->graphs.find(key);
       if (it == c->graphs.end()) {
         cudaStream_t cap = P->s_dec;
@@ -936,7 +983,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
         int nk = 0;
         CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         c->capturing = true;
-        duet_status s = decode_step_kernels(c, cap, P->s_d, w, kv, ap, max_len, dec->y, &nk);
+        duet_status s = decode_step_kernels(c, cap, P->s_d, w, kv, ap, max_len, dec->y, dec->head, &nk);
         c->capturing = false;
         cudaError_t e = cudaStreamEndCapture(cap, &graph);
         if (s != DUET_OK) return s;

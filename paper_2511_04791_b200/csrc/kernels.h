@@ -136,6 +136,10 @@ int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st);
 // ---------------------------------------------------------------- decode window bookkeeping
 // End of one decode step (P:335 look-ahead): y_out[step][r] = y[r]; xin[r] = y[r];
 // pos[r] += 1; step += 1.  Reads *step on device so a captured graph can be replayed k times.
+// greedy token of each row's bf16 logits [n][vocab] -> tokens[(step ? *step : 0) * n + r]; x_next[r] =
+// embed[token] (x_next may be NULL)
+int launch_argmax_embed(const void* logits, int vocab, const void* embed, void* x_next, int d, int* tokens,
+                        const int* step, int n, cudaStream_t st);
 int launch_decode_advance(DT dt, const void* y, void* xin, void* y_out, int n, int d, int* pos, int* step,
                           cudaStream_t st);
 

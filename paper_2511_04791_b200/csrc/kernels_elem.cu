@@ -174,13 +174,74 @@ __global__ void decode_advance_kernel(const T* __restrict__ y, T* __restrict__ x
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const T v = y[i];
     y_out[(size_t)s * total + i] = v;
-    xin[i] = v;
+    if (xin) xin[i] = v;  // synthetic feedback (reading #26); with an LM head the embedding is the input
   }
 }
 __global__ void decode_bump_kernel(int n, int* pos, int* step) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) pos[i] += 1;
   if (i == 0) *step += 1;
+}
+
+// ---------------------------------------------------------------- greedy token + embedding (f1)
+// One CTA per row: token = argmax over the vocab of the bf16 logits (the lowest index among equal
+// maxima), tokens[step * n + r] = token, x_next[r] = embed[token] (16-byte vector copy).
+__global__ void __launch_bounds__(1024) argmax_embed_kernel(const bf16* __restrict__ logits, int vocab,
+                                                            const bf16* __restrict__ embed, bf16* __restrict__ x_next,
+                                                            int d, int* __restrict__ tokens, const int* step, int n) {
+  pdl_wait();
+  const int r = blockIdx.x;
+  const bf16* lr = logits + (size_t)r * vocab;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+    const float v = __bfloat162float(lr[i]);
+    if (v > best) {  // ascending i per thread: the first maximum is kept
+      best = v;
+      bi = i;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  __shared__ int tok;
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = sv[0];
+    int i0 = si[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (sv[w] > b || (sv[w] == b && si[w] < i0)) {
+        b = sv[w];
+        i0 = si[w];
+      }
+    tok = i0;
+    tokens[(size_t)(step ? *step : 0) * n + r] = i0;
+  }
+  __syncthreads();
+  if (x_next) {
+    const uint4* src = reinterpret_cast<const uint4*>(embed + (size_t)tok * d);
+    uint4* dst = reinterpret_cast<uint4*>(x_next + (size_t)r * d);
+    for (int i = threadIdx.x; i < d / 8; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+int launch_argmax_embed(const void* logits, int vocab, const void* embed, void* x_next, int d, int* tokens,
+                        const int* step, int n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  launch_pdl(argmax_embed_kernel, n, 1024, 0, st, (const bf16*)logits, vocab, (const bf16*)embed, (bf16*)x_next, d,
+             tokens, step, n);
+  return 1;
 }
 
 int launch_decode_advance(DT dt, const void* y, void* xin, void* y_out, int n, int d, int* pos, int* step,

@@ -32,6 +32,7 @@ _M32 = 0xFFFFFFFF
 # stream ids (arbitrary, fixed): one per kind of tensor
 S_WQKV, S_BQKV, S_WO, S_WGU, S_WDOWN, S_G1, S_G2 = 1, 2, 3, 4, 5, 6, 7
 S_XPRE, S_XDEC, S_KHIST, S_VHIST = 11, 12, 13, 14
+S_GFINAL, S_WHEAD, S_EMBED = 21, 22, 23
 
 
 def _hash32_np(x: np.ndarray) -> np.ndarray:
@@ -123,6 +124,17 @@ def layer_weights(cfg: ModelCfg, layer: int, seed: int) -> dict:
     if cfg.qkv_bias:
         w["b_qkv"] = counter_values(seed, S_BQKV, (nqkv,), base, 6)
     return w
+
+
+def head_weights(cfg: ModelCfg, seed: int) -> dict:
+    """fp32 LM head of the decode loop: final norm gain [d], w_head [vocab][d]
+    (scaled like a layer weight), embed [vocab][d] (unscaled grid values, like the x rows)."""
+    d, v = cfg.d_model, cfg.vocab
+    return {
+        "g_norm": (1.0 + counter_values(seed, S_GFINAL, (d,), 0, 3)).astype(np.float32),
+        "w_head": counter_values(seed, S_WHEAD, (v, d), 0, pow2_scale(d)),
+        "embed": counter_values(seed, S_EMBED, (v, d), 0, 0),
+    }
 
 
 def x_rows(seed: int, stream: int, n_rows: int, d: int, row_offset: int = 0) -> np.ndarray:

@@ -52,10 +52,17 @@ class GpuWorkload:
         return dict(q=[q for q, _ in self.wl.pre_seqs], c=[c for _, c in self.wl.pre_seqs],
                     table=self.wl.pre_tables, x=self.x_pre, y=self.y_pre)
 
+    def add_head(self, head: dict, device="cuda"):
+        """LM head (f1): synth.head_weights on the GPU + a tokens [k][n_dec] output."""
+        tdt = torch_dtype(self.dtype)
+        self.head = {k: torch.from_numpy(np.ascontiguousarray(v)).to(device=device, dtype=tdt) for k, v in head.items()}
+        self.head["tokens"] = torch.full((self.wl.k, len(self.wl.dec_ctx)), -1, dtype=torch.int32, device=device)
+
     def decode_arg(self):
         if not self.wl.dec_ctx:
             return None
-        return dict(c=self.wl.dec_ctx, table=self.wl.dec_tables, x=self.x_dec, y=self.y_dec)
+        return dict(c=self.wl.dec_ctx, table=self.wl.dec_tables, x=self.x_dec, y=self.y_dec,
+                    head=getattr(self, "head", None))
 
     def step(self, ctx: D.Ctx, split, stream=None):
         ctx.step(self.W, self.prefill_arg(), self.decode_arg(), self.K, self.V, self.wl.n_pages, split, stream)

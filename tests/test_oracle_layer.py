@@ -287,3 +287,62 @@ def test_poisoned_pool_only_listed_slots_change_and_conservation():
     for p in (0, 15, 16, 33):
         assert kv.slot(trow, p) == (int(trow[p // 16]), p % 16)
     assert kv.flat_offset(3, 1, 5, 7) == ((3 * kv.h_kv + 1) * 16 + 5) * kv.d_h + 7
+
+
+# ------------------------------------------------------------------ LM head + greedy decode (f1)
+
+def test_lm_head_brute_force_and_ties():
+    """logits by explicit loops; argmax takes the lowest index among equal maxima."""
+    from oracle import layer as OL
+    rng = np.random.default_rng(7)
+    d, v = 16, 12
+    m = OL.Model(d, 32, 2, 2, 8, 1e4, 1e-5)
+    head = {"g_norm": rng.normal(size=d), "w_head": rng.normal(size=(v, d)), "embed": rng.normal(size=(v, d))}
+    y = rng.normal(size=(3, d))
+    logits, tok = OL.lm_head_greedy(m, head, y)
+    for i in range(3):
+        ms = sum(float(t) * float(t) for t in y[i]) / d
+        h = [y[i][e] / math.sqrt(ms + 1e-5) * head["g_norm"][e] for e in range(d)]
+        for t in range(v):
+            ref = sum(h[e] * head["w_head"][t][e] for e in range(d))
+            assert abs(ref - logits[i, t]) <= 1e-12 * max(1.0, abs(ref))
+        best = max(range(v), key=lambda t: (logits[i, t], -t))
+        assert tok[i] == best
+    head["g_norm"] = np.ones(d)
+    head["w_head"][5] = head["w_head"][9] = 10.0 * np.ones(d)   # two identical maxima rows
+    _, tok = OL.lm_head_greedy(m, head, np.ones((1, d)))
+    assert tok[0] == 5
+
+
+def test_lm_head_tied_embedding_recovers_token():
+    """With w_head = embed (tied) and y = embed[t], the greedy token is t: a row's dot product with
+    itself dominates in high dimension (the invariant an autoregressive loop relies on)."""
+    from oracle import layer as OL
+    rng = np.random.default_rng(3)
+    d, v = 256, 64
+    m = OL.Model(d, 32, 2, 2, 128, 1e4, 1e-5)
+    E = rng.normal(size=(v, d))
+    head = {"g_norm": np.ones(d), "w_head": E, "embed": E}
+    t = np.array([0, 17, 63, 5])
+    _, tok = OL.lm_head_greedy(m, head, E[t])
+    assert np.array_equal(tok, t)
+
+
+def test_decode_window_with_head_feeds_embedding():
+    """Step j+1's input is embed[token_j]: the window equals k single steps chained by hand."""
+    from oracle import layer as OL
+    from synth import configs, head_weights, workload
+    from tests.oracle_run import make_kv
+    cfg = configs.get_config("cfg1")
+    wl = workload.build(cfg, k=2)
+    m = OL.Model.from_cfg(cfg.model)
+    head = head_weights(cfg.model, cfg.seed)
+    toks = []
+    y = OL.decode_window(m, wl.weights, wl.x_dec, wl.dec_ctx, wl.dec_tables, make_kv(wl), 2, head, toks)
+    kv = make_kv(wl)
+    y1 = OL.decode_window(m, wl.weights, wl.x_dec, wl.dec_ctx, wl.dec_tables, kv, 1)
+    _, t1 = OL.lm_head_greedy(m, head, y1[0])
+    x2 = np.asarray(head["embed"], dtype=np.float64)[t1]
+    y2 = OL.decode_window(m, wl.weights, x2, [c + 1 for c in wl.dec_ctx], wl.dec_tables, kv, 1)
+    assert np.array_equal(toks[0][1], t1)
+    assert np.allclose(y[1], y2[0], rtol=0, atol=1e-12)
