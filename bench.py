@@ -245,6 +245,8 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="also time every SM split")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="a few steps, no extras (for ncu)")
+    ap.add_argument("--lm-head", action="store_true",
+                    help="close the decode window with the LM head + greedy tokens (f1; t_cls in the predictor)")
     ap.add_argument("--tp", type=int, default=1,
                     help="head-sharded tensor parallelism over the torchrun ranks (= WORLD_SIZE; default config "
                          "cfg5): one batch per step across all ranks, NCCL allreduce after O and down")
@@ -288,6 +290,11 @@ def main():
     else:
         W = [layer_weights_gpu(m, l, cfg.seed, dev, tdt) for l in range(m.n_layers)]
     x_pre, x_dec = inputs_gpu(wl, dev, tdt)
+    head = None
+    if args.lm_head:   # f1: LM head + embedding (vocab x d each) and a tokens [8][n_d] output
+        from synth.gpu import head_weights_gpu
+        head = head_weights_gpu(m, cfg.seed, dev, tdt)
+        head["tokens"] = torch.zeros((8, len(wl.dec_ctx)), dtype=torch.int32, device=dev)
     torch.cuda.empty_cache()  # hand the generator's temporaries back: libduet allocates with cudaMalloc
     n_p, n_d = x_pre.shape[0], x_dec.shape[0]
     y_pre = torch.empty_like(x_pre)
@@ -327,8 +334,10 @@ def main():
     log("KV ready; warm-up")
     torch.cuda.empty_cache()
     tau = args.tau if args.tau is not None else cfg.batch.tbt_slo_s
-    batch = [(q, c, 0 if c == 0 else 1, 1) for q, c in wl.pre_seqs] + [(1, c, 2, 1) for c in wl.dec_ctx]
-    opts = D.DUET_OPT_FORCE_SPATIAL if args.mode == "spatial" else 0
+    # emits_logits: the decode rows when the LM head runs (P:250 t_cls over the entries that emit logits)
+    batch = [(q, c, 0 if c == 0 else 1, 0) for q, c in wl.pre_seqs] + \
+        [(1, c, 2, 1 if head is not None else 0) for c in wl.dec_ctx]
+    opts = (D.DUET_OPT_FORCE_SPATIAL if args.mode == "spatial" else 0) | (D.DUET_OPT_INCLUDE_CLS if head is not None else 0)
 
     def decide():
         if args.mode == "temporal":
@@ -341,7 +350,7 @@ def main():
 
     def decode_arg(k, bufs=None):
         xd, yd = (x_dec, y_dec) if bufs is None else (bufs[1], bufs[3])
-        return dict(c=wl.dec_ctx, table=wl.dec_tables, x=xd, y=yd[:k])
+        return dict(c=wl.dec_ctx, table=wl.dec_tables, x=xd, y=yd[:k], head=head)
 
     def one_step(split=None, bufs=None):
         """bufs: optional (x_pre, x_dec, y_pre, y_dec) device buffers (the e2e double buffering)."""
@@ -442,7 +451,7 @@ def main():
             return tok / (a.elapsed_time(b) * 1e-3), float(np.median(wins)), float(np.median(tds))
 
         agg = timed(lambda: D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1))
-        forced = D.duet_choose_split(spec, hw, batch, tau, k_max, D.DUET_OPT_FORCE_SPATIAL)
+        forced = D.duet_choose_split(spec, hw, batch, tau, k_max, D.DUET_OPT_FORCE_SPATIAL | (opts & D.DUET_OPT_INCLUDE_CLS))
         if forced.k > 8:
             forced = D.split_struct(1, forced.s_p, forced.s_d, 8, forced.flags, forced.t_mixed, forced.t_p,
                                     forced.t_d, forced.rho)
@@ -556,7 +565,9 @@ def main():
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if tp > 1 else "weak",
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded counter generator, random weights)",
-            "config": {"workload": f"{args.config}: {cfg.note}", "mode": ["temporal", "spatial"][split.mode],
+            "config": {"workload": f"{args.config}: {cfg.note}" + (" + LM head / greedy tokens (f1)" if head is not None
+                                                                      else ""),
+                       "mode": ["temporal", "spatial"][split.mode],
                        "s_p": split.s_p, "s_d": split.s_d, "k": split.k, "flags": split.flags,
                        "tau_ms": tau * 1e3, "prefill_tokens": n_p, "decode_reqs": n_d,
                        "l2": f"inputs > L2 ({step_bytes / 1e9:.1f} GB of weights + KV read per step), no flush",

@@ -9,8 +9,18 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import (S_BQKV, S_G1, S_G2, S_KHIST, S_VHIST, S_WDOWN, S_WGU, S_WO, S_WQKV, S_XDEC, S_XPRE,
-               counter_values_torch, pow2_scale)
+from . import (S_BQKV, S_EMBED, S_G1, S_G2, S_GFINAL, S_KHIST, S_VHIST, S_WDOWN, S_WGU, S_WHEAD, S_WO, S_WQKV,
+               S_XDEC, S_XPRE, counter_values_torch, pow2_scale)
+
+
+def head_weights_gpu(cfg_model, seed: int, device, dtype) -> dict:
+    """Same values as synth.head_weights (LM head of the decode loop, f1), generated on the GPU."""
+    d, v = cfg_model.d_model, cfg_model.vocab
+    return {
+        "g_norm": (1.0 + counter_values_torch(seed, S_GFINAL, (d,), 0, 3, device=device)).to(dtype),
+        "w_head": counter_values_torch(seed, S_WHEAD, (v, d), 0, pow2_scale(d), device=device, dtype=dtype),
+        "embed": counter_values_torch(seed, S_EMBED, (v, d), 0, 0, device=device, dtype=dtype),
+    }
 
 
 def layer_weights_gpu(cfg_model, layer: int, seed: int, device, dtype) -> dict:
