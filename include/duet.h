@@ -156,6 +156,47 @@ duet_status duet_ctx_create(int32_t device, const duet_model_spec* spec,
                             const duet_ctx_limits* limits, duet_ctx** out);
 duet_status duet_ctx_destroy(duet_ctx* ctx);
 
+/* ----------------------------------------------------------------- iteration stream (§8(f) f2)
+ * Host-side batch former + KV page allocator that turns a request trace into mixed iterations
+ * (P:184 decode-first chunked prefill, P:302 R_prefill / R_decode, P:335 k-slot look-ahead; S:376
+ * KV-capacity admission).  Deterministic, pure host, thread-compatible (one sched per thread).
+ *  duet_sched_create: cfg = page size and pool size (pages), token budget per iteration (decode rows
+ *    count one token each), max decode batch, max prefill sequences per iteration, k_max (look-ahead
+ *    slots reserved per request), max pages per sequence (page-table pitch bound).
+ *  duet_sched_add: a request (id, prompt and output length in tokens, arrival time, non-decreasing).
+ *    CAPACITY if prompt + output + k_max tokens can never fit.
+ *  duet_sched_next: forms the next iteration at time now_s: admits arrived requests FIFO while the
+ *    free pages cover their whole prompt + output + k_max; every running decode (up to max_batch)
+ *    joins, then prefill chunks fill the remaining budget, the oldest prompt first.  The arrays of
+ *    *out (ids, q, c, page_table [n_prefill + n_decode][max_pages], prefill entries first) are owned by
+ *    the sched and valid until the next call; an empty iteration (n_prefill = n_decode = 0) needs
+ *    no commit — next_arrival_s says when the next request arrives (-1: none).
+ *  duet_sched_commit: the iteration ran with k_done look-ahead decode steps (1 in temporal mode):
+ *    prefill chunks advance (a completed prompt yields its first output token and joins the decodes),
+ *    decodes produce min(k_done, remaining) tokens; finished requests return their pages.
+ *    tokens_out: tokens produced (prefilled + generated); finished_out: requests completed.
+ * Errors: INVALID_ARG (order of calls, ranges), OUT_OF_RANGE, CAPACITY. */
+typedef struct {
+  int32_t page_size, n_pages, token_budget, max_batch, max_prefill_seqs, k_max, max_pages_per_seq;
+} duet_sched_cfg;
+typedef struct {
+  int32_t n_prefill, n_decode;
+  const int64_t* ids;
+  const int32_t* q;
+  const int32_t* c;
+  const int32_t* page_table;
+  int32_t max_pages;
+  double next_arrival_s;
+  int32_t n_unfinished;
+} duet_iteration;
+typedef struct duet_sched duet_sched;
+duet_status duet_sched_create(const duet_sched_cfg* cfg, duet_sched** out);
+duet_status duet_sched_destroy(duet_sched* sched);
+duet_status duet_sched_add(duet_sched* sched, int64_t id, int32_t prompt_len, int32_t output_len, double arrival_s);
+duet_status duet_sched_next(duet_sched* sched, double now_s, duet_iteration* out);
+duet_status duet_sched_commit(duet_sched* sched, int32_t k_done, int32_t* tokens_out, int32_t* finished_out);
+duet_status duet_sched_free_pages(const duet_sched* sched, int32_t* out);
+
 /* ----------------------------------------------------------------- tensor parallelism (§8 a9)
  * Head-sharded TP (reading #13).  A ctx created with spec->tp = N
  * computes the shard of rank r: h_q/N query heads, h_kv/N kv heads and ffn_dim/N FFN columns

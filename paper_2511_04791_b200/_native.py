@@ -117,6 +117,12 @@ _SIGS = {
     "duet_op_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "duet_op_rmsnorm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "duet_sched_create": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "duet_sched_destroy": (C.c_int, [C.c_void_p]),
+    "duet_sched_add": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_double]),
+    "duet_sched_next": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p]),
+    "duet_sched_commit": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "duet_sched_free_pages": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "duet_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_int32]),
     "duet_ctx_set_comms": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "duet_calibrate_allreduce": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
@@ -206,6 +212,68 @@ def _i32(a):
 
 def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class duet_sched_cfg(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("page_size", "n_pages", "token_budget", "max_batch", "max_prefill_seqs",
+                                           "k_max", "max_pages_per_seq")]
+
+
+class duet_iteration(C.Structure):
+    _fields_ = [("n_prefill", C.c_int32), ("n_decode", C.c_int32), ("ids", C.POINTER(C.c_int64)),
+                ("q", C.POINTER(C.c_int32)), ("c", C.POINTER(C.c_int32)), ("page_table", C.POINTER(C.c_int32)),
+                ("max_pages", C.c_int32), ("next_arrival_s", C.c_double), ("n_unfinished", C.c_int32)]
+
+
+class Sched:
+    """Iteration stream (duet_sched_*): decode-first chunked-prefill batch former + KV page allocator."""
+
+    def __init__(self, page_size=16, n_pages=1 << 16, token_budget=8192, max_batch=1024, max_prefill_seqs=16,
+                 k_max=8, max_pages_per_seq=4096):
+        cfg = duet_sched_cfg(page_size, n_pages, token_budget, max_batch, max_prefill_seqs, k_max, max_pages_per_seq)
+        h = C.c_void_p()
+        _check(lib().duet_sched_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.page_size = page_size
+
+    def close(self):
+        if self.h:
+            lib().duet_sched_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def add(self, rid: int, prompt: int, output: int, arrival: float):
+        _check(lib().duet_sched_add(self.h, int(rid), int(prompt), int(output), float(arrival)))
+
+    def next(self, now: float) -> dict:
+        """dict(prefill=[(id, q, c)], decode=[(id, c)], table=np.int32 [n, max_pages], next_arrival, unfinished)."""
+        import numpy as np
+        it = duet_iteration()
+        _check(lib().duet_sched_next(self.h, float(now), C.byref(it)))
+        n = it.n_prefill + it.n_decode
+        ids = [it.ids[i] for i in range(n)]
+        q = [it.q[i] for i in range(n)]
+        c = [it.c[i] for i in range(n)]
+        tab = np.ctypeslib.as_array(it.page_table, shape=(max(n, 1), max(it.max_pages, 1))).copy()[:n] if n else \
+            np.zeros((0, 1), dtype=np.int32)
+        return dict(prefill=[(ids[i], q[i], c[i]) for i in range(it.n_prefill)],
+                    decode=[(ids[i], c[i]) for i in range(it.n_prefill, n)], table=tab,
+                    next_arrival=it.next_arrival_s, unfinished=it.n_unfinished)
+
+    def commit(self, k_done: int):
+        t, f = C.c_int32(), C.c_int32()
+        _check(lib().duet_sched_commit(self.h, int(k_done), C.byref(t), C.byref(f)))
+        return t.value, f.value
+
+    def free_pages(self) -> int:
+        v = C.c_int32()
+        _check(lib().duet_sched_free_pages(self.h, C.byref(v)))
+        return v.value
 
 
 def nccl_unique_id() -> bytes:
@@ -339,4 +407,4 @@ def split_struct(mode, s_p, s_d, k, flags=0, t_mixed=0.0, t_p=0.0, t_d=0.0, rho=
 
 __all__ = [n for n in dir() if n.startswith(("duet_", "DUET_"))] + [
     "Ctx", "HwProfile", "make_spec", "split_struct", "split_tuple", "lib", "DuetError", "EXPORTED", "LIB_PATH",
-    "nccl_unique_id"]
+    "nccl_unique_id", "Sched"]

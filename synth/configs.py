@@ -68,6 +68,9 @@ CONFIGS = {
                         BatchCfg(prefill=((200, 37), (77, 0), (520, 300)), decode=(300, 17, 1029), k=3),
                         dtype="bf16",
                         seed=4791 + 2, note="Llama-3-8B layer shapes, ragged small batch (parity only)"),
+    "cfg4-mini": Config("cfg4-mini", replace(QWEN25_14B, name="qwen2.5-14b-layer", n_layers=1),
+                        BatchCfg(prefill=((300, 0), (129, 45)), decode=(700, 33, 2049, 5), k=2), dtype="bf16",
+                        seed=4791 + 4, note="Qwen2.5-14B layer shapes (GQA 5, QKV bias), ragged (parity only)"),
     "cfg2": Config("cfg2", LLAMA3_8B_LAYER, BatchCfg(prefill=((2048, 0),), decode=(4096,) * 64, k=1,
                                                      tbt_slo_s=50e-3 / 32), dtype="bf16", seed=4791 + 2,
                    note="Llama-3-8B single layer: prefill chunk 2048 + 64 decodes at ctx 4k"),

@@ -121,6 +121,27 @@ def test_parity_llama_shapes_ragged_prefix():
     _check_outputs(g, y_pre1, y_dec1, TOL["bf16"])
 
 
+def test_parity_qwen_shapes_gqa5_bias():
+    """Qwen2.5-14B layer shapes (d = 5120, h_q = 40, h_kv = 8: GQA group 5 — an odd last head per group
+    in the paired-head flash attention — QKV bias, ffn 13824) on a ragged batch, spatial k = 2 and
+    temporal, against the oracle."""
+    cfg = configs.get_config("cfg4-mini")
+    wl = workload.build(cfg)
+    y_pre, y_dec, kv_o = run(wl)
+    ctx = make_ctx(wl, "bf16")
+    parts, total = ctx.partitions()
+    g = GpuWorkload(wl, "bf16")
+    g.step(ctx, D.split_struct(D.DUET_MODE_SPATIAL, total - parts[1], parts[1], wl.k))
+    torch.cuda.synchronize()
+    _check_outputs(g, y_pre, y_dec, TOL["bf16"])
+    _check_kv(g, kv_o, TOL["bf16"])
+    g = GpuWorkload(wl, "bf16")   # temporal runs k = 1: step 1 of the same oracle window
+    g.step(ctx, D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1))
+    torch.cuda.synchronize()
+    assert rel_err(g.y_pre.float().cpu().numpy(), y_pre) <= TOL["bf16"]
+    assert rel_err(g.y_dec[0].float().cpu().numpy(), y_dec[0]) <= TOL["bf16"]
+
+
 def test_parity_large_activations_running_max_rebase():
     """Inputs scaled x16 (still exact in bf16): attention scores grow along the sequence, so rows re-base
     their running max at different key tiles (warp-divergent rescale decisions in the flash kernel)."""
