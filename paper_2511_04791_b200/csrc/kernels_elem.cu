@@ -13,17 +13,32 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const T* __restrict__ 
                                                           T* __restrict__ h, int d, float eps, const T* __restrict__ x2,
                                                           int row_split) {
   constexpr int E = 16 / sizeof(T);
+  constexpr int VPT = 4;  // rows of up to THREADS * VPT vectors stay in registers: x is read once
   pdl_wait();
   const int row = blockIdx.x;
   const T* xr = row < row_split ? x + (size_t)row * d : x2 + (size_t)(row - row_split) * d;
   T* hr = h + (size_t)row * d;
   const int nv = d / E;
+  const bool cached = nv <= THREADS * VPT;
+  float f[VPT][E];
   float ss = 0.f;
-  for (int v = threadIdx.x; v < nv; v += THREADS) {
-    float f[E];
-    load16<T>(xr + v * E, f);
+  if (cached) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) ss += f[e] * f[e];
+    for (int k = 0; k < VPT; ++k) {
+      const int v = threadIdx.x + k * THREADS;
+      if (v < nv) {
+        load16<T>(xr + v * E, f[k]);
+#pragma unroll
+        for (int e = 0; e < E; ++e) ss += f[k][e] * f[k][e];
+      }
+    }
+  } else {
+    for (int v = threadIdx.x; v < nv; v += THREADS) {
+      float t[E];
+      load16<T>(xr + v * E, t);
+#pragma unroll
+      for (int e = 0; e < E; ++e) ss += t[e] * t[e];
+    }
   }
   __shared__ float red[THREADS / 32];
   ss = warp_sum(ss);
@@ -36,13 +51,27 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const T* __restrict__ 
   }
   __syncthreads();
   const float r = rsqrtf(red[0] / (float)d + eps);
-  for (int v = threadIdx.x; v < nv; v += THREADS) {
-    float f[E], gg[E];
-    load16<T>(xr + v * E, f);
-    load16<T>(g + v * E, gg);
+  if (cached) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) f[e] = f[e] * r * gg[e];
-    store16<T>(hr + v * E, f);
+    for (int k = 0; k < VPT; ++k) {
+      const int v = threadIdx.x + k * THREADS;
+      if (v < nv) {
+        float gg[E];
+        load16<T>(g + v * E, gg);
+#pragma unroll
+        for (int e = 0; e < E; ++e) f[k][e] = f[k][e] * r * gg[e];
+        store16<T>(hr + v * E, f[k]);
+      }
+    }
+  } else {
+    for (int v = threadIdx.x; v < nv; v += THREADS) {
+      float t[E], gg[E];
+      load16<T>(xr + v * E, t);
+      load16<T>(g + v * E, gg);
+#pragma unroll
+      for (int e = 0; e < E; ++e) t[e] = t[e] * r * gg[e];
+      store16<T>(hr + v * E, t);
+    }
   }
 }
 
