@@ -57,6 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 "--expt-relaxed-constexpr", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}",
                 "-Xptxas", "-warn-spills"]
     stamp = os.path.join(BUILD, "libduet.stamp")
+    flags_cu += os.environ.get("DUET_NVCC_EXTRA", "").split()   # A/B builds (e.g. -DDUET_NO_PDL_TRIGGER)
     dig = _digest(cpp + cu + hdr, " ".join(flags_cpp + flags_cu))
     if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == dig:
         return LIB

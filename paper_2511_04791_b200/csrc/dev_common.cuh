@@ -16,6 +16,13 @@ using bf16 = __nv_bfloat16;
 // never sit on SMs next to a running grid (an early trigger measured 2 % slower: waiting CTAs
 // co-resident with the persistent GEMMs).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Late trigger: issued when a CTA has no main-loop work left (its last tile's epilogue), so the next
+// kernel's CTAs launch into the SMs this grid is about to leave and overlap their set-up with its tail.
+__device__ __forceinline__ void pdl_trigger() {
+#ifndef DUET_NO_PDL_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
     l[h] += __shfl_xor_sync(0xffffffffu, l[h], 16);
   }
   __syncthreads();
+  pdl_trigger();  // only the merge is left
   // merge the warps (heads h < G); the rings are no longer needed
   float* sm_o = reinterpret_cast<float*>(smem);  // [WARPS][8 heads][DH]
   float* sm_ml = sm_o + WARPS * 8 * DH;          // [WARPS][8][2]

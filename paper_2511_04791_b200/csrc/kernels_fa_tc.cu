@@ -467,6 +467,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
         if (warp == 2) stamp(6, j);
         if (warp == 6) stamp(9, j);
       }
+      pdl_trigger();  // only the epilogue is left
       // epilogue: O / l -> bf16 -> global
       mbar_wait(&o_done[h], 0);
       tc_after();

@@ -236,6 +236,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const int acc = i & 1;
       const int mp = t % p.num_m2, nb = t / p.num_m2;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
+      if (t + n_pairs >= p.num_tiles) pdl_trigger();  // last tile: only the epilogue is left
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN_PAIR;
       const int row = mp * PAIR_M + (int)rank * BM + lane_row;

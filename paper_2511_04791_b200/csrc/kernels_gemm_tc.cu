@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
       const uint32_t aph = (i >> 1) & 1;
       const int mb = t % p.num_m, nb = t / p.num_m;
       mbar_wait(&tfull[acc], aph);
+      if (u + (int)gridDim.x >= p.num_units) pdl_trigger();  // last unit: only the epilogue is left
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * CF::ACC_COLS;
       if constexpr (!SWAP) {
