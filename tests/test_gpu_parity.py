@@ -12,7 +12,8 @@ import torch
 
 import paper_2511_04791_b200 as D
 from synth import configs, workload
-from tests.gpu_helpers import GpuWorkload, make_ctx
+from synth import layer_weights as synth_layer_weights
+from tests.gpu_helpers import GpuWorkload, make_ctx, spec_of
 from tests.oracle_run import rel_err, run
 
 pytestmark = pytest.mark.gpu
@@ -357,3 +358,76 @@ def test_lm_head_greedy_window_vs_oracle(mode):
         alive &= tok_gpu[j] == t_ref
     assert checked >= len(wl.dec_ctx) // 2  # the comparison is not vacuous
     ctx.close()
+
+
+def test_iteration_stream_served_trace_vs_oracle():
+    """f2 end to end: duet_sched forms the iterations of a small bursty trace on the tiny model; every
+    iteration runs through duet_step (alternating temporal and spatial with k = 2) and through the
+    oracle on the same rows, the same page tables and a KV pool that both sides fill iteration after
+    iteration (pages are reused once requests finish).  Outputs must agree every iteration."""
+    from oracle import layer as OL
+    from synth import configs, counter_values
+    cfg = configs.get_config("cfg1-bf16")
+    m = cfg.model
+    M = OL.Model.from_cfg(m)
+    d, P = m.d_model, 16
+    weights = [synth_layer_weights(m, 0, cfg.seed)]
+    n_pages = 40
+    sched = D.Sched(page_size=P, n_pages=n_pages, token_budget=96, max_batch=8, max_prefill_seqs=4, k_max=2,
+                    max_pages_per_seq=16)
+    trace = [(0, 70, 4, 0.0), (1, 30, 3, 0.0), (2, 120, 2, 0.0), (3, 45, 5, 0.001), (4, 20, 3, 0.002)]
+    for r in trace:
+        sched.add(*r)
+    tdt = torch.bfloat16
+    W = [{k: torch.from_numpy(np.ascontiguousarray(v)).to("cuda", tdt) for k, v in weights[0].items() if v is not None}]
+    Kg = [torch.zeros((n_pages, m.n_kv_heads, P, m.head_dim), dtype=tdt, device="cuda")]
+    Vg = [torch.zeros_like(Kg[0])]
+    kv_o = OL.PagedKV(1, n_pages, m.n_kv_heads, P, m.head_dim)
+    ctx = D.Ctx(spec_of(m, "bf16"), 96, 4, 8, 2, 16, 256, D.DUET_DTYPE_BF16)
+    parts, total = ctx.partitions()
+
+    def rows(rid, p0, n):   # input row of (request, position): exact bf16 grid values
+        return counter_values(cfg.seed, 31, (n, d), (rid * 4096 + p0) * d)
+
+    it_no, now = 0, 0.0
+    while True:
+        it = sched.next(now)
+        if not it["prefill"] and not it["decode"]:
+            if it["unfinished"] == 0:
+                break
+            now = it["next_arrival"]
+            continue
+        n_pre, n_dec = len(it["prefill"]), len(it["decode"])
+        tab = it["table"]
+        spatial = it_no % 2 == 1 and n_pre > 0 and n_dec > 0
+        k = 2 if spatial else 1
+        x_pre = np.concatenate([rows(rid, c, q) for rid, q, c in it["prefill"]]) if n_pre else np.zeros((0, d))
+        x_dec = np.concatenate([rows(rid, c, 1) for rid, c in it["decode"]]) if n_dec else np.zeros((0, d))
+        # oracle: the prefill chunks then the k-step decode window, on the shared paged pool
+        y_pre_o = OL.prefill_forward(M, weights, x_pre, [(q, c) for _, q, c in it["prefill"]], tab[:n_pre], kv_o) \
+            if n_pre else None
+        y_dec_o = OL.decode_window(M, weights, x_dec, [c for _, c in it["decode"]], tab[n_pre:], kv_o, k) \
+            if n_dec else None
+        xp = torch.from_numpy(x_pre).to("cuda", tdt)
+        xd = torch.from_numpy(x_dec).to("cuda", tdt)
+        yp = torch.empty_like(xp)
+        yd = torch.empty((k,) + tuple(xd.shape), dtype=tdt, device="cuda")
+        pre = dict(q=[q for _, q, _ in it["prefill"]], c=[c for _, _, c in it["prefill"]],
+                   table=np.ascontiguousarray(tab[:n_pre]), x=xp, y=yp) if n_pre else None
+        dec = dict(c=[c for _, c in it["decode"]], table=np.ascontiguousarray(tab[n_pre:]), x=xd, y=yd) \
+            if n_dec else None
+        split = D.split_struct(D.DUET_MODE_SPATIAL, total - parts[0], parts[0], k) if spatial else \
+            D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1)
+        ctx.step(W, pre, dec, Kg, Vg, n_pages, split)
+        torch.cuda.synchronize()
+        if n_pre:
+            assert rel_err(yp.float().cpu().numpy(), y_pre_o) <= TOL["bf16"], it_no
+        if n_dec:
+            for j in range(k):
+                assert rel_err(yd[j].float().cpu().numpy(), y_dec_o[j]) <= TOL["bf16"], (it_no, j)
+        sched.commit(k)
+        it_no += 1
+        now += 1e-3
+    assert it_no >= 6 and sched.free_pages() == n_pages
+    ctx.close()
+    sched.close()
