@@ -368,15 +368,22 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e,
           launch_rmsnorm(dt, X, W.g_norm1, S.h, n_rows, d, eps, st, l == 0 ? x_in2 : nullptr,
                          l == 0 ? row_split : 1 << 30));
-    // 2. qkv = h W_qkv^T (+ b)
-    GemmArgs g{S.h, W.w_qkv, S.qkv, nullptr, W.b_qkv, n_rows, nqkv, d, d, d, nqkv, 0, EPI_STORE};
-    with_ws(g);
-    TIMED(DUET_KCLASS_GEMM, gemm_fl(nqkv, d), gemm_by(nqkv, d, nqkv, false), launch_gemm(dt, g, num_sms, st));
-    // 3. RoPE + paged KV append (before attention)
+    // 2. qkv = h W_qkv^T (+ b);  3. RoPE + paged KV append (before attention) — fused into the
+    // CTA-pair GEMM's epilogue when it runs (k and v never round-trip through the qkv buffer)
     RopeKvArgs ra{S.qkv, nullptr, n_rows, hq, hkv, dh, S.pos(), S.tok(), S.table(), S.pitch, kPageSize,
                   kv->k_pool[l], kv->v_pool[l], c->rope};
-    TIMED(DUET_KCLASS_OTHER, 6.0 * n * (hq + hkv) * dh, n * (nqkv + (hq + 2.0 * hkv) * dh) * e,
-          launch_rope_kv(dt, ra, st));
+    GemmArgs g{S.h, W.w_qkv, S.qkv, nullptr, W.b_qkv, n_rows, nqkv, d, d, d, nqkv, 0, EPI_STORE};
+    with_ws(g);
+    static const bool fuse_env = !getenv("DUET_FUSE_ROPE") || atoi(getenv("DUET_FUSE_ROPE")) != 0;
+    const bool fuse_rope = fuse_env && dt == DT::BF16 && dh == 128 && kPageSize == 16 && gemm2_supported(g, num_sms);
+    if (fuse_rope) {
+      g.epi = EPI_QKV_ROPE;
+      g.rope = &ra;
+    }
+    TIMED(DUET_KCLASS_GEMM, gemm_fl(nqkv, d), gemm_by(nqkv, d, nqkv, false), launch_gemm(dt, g, num_sms, st));
+    if (!fuse_rope)
+      TIMED(DUET_KCLASS_OTHER, 6.0 * n * (hq + hkv) * dh, n * (nqkv + (hq + 2.0 * hkv) * dh) * e,
+            launch_rope_kv(dt, ra, st));
     // 4. attention
     if (ap.n_pre > 0) {
       PrefillAttnArgs pa{};

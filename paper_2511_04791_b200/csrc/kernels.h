@@ -16,7 +16,9 @@ inline size_t dt_size(DT t) { return t == DT::BF16 ? 2 : 4; }
 //  EPI_RESIDUAL: C = R[m][n] (ldr) + acc
 //  EPI_SWIGLU:   B has rows [gate(N) ; up(N)] (gate row j at j, up row j at N + j);
 //                C[m][j] = silu(acc_gate) * acc_up
-enum { EPI_STORE = 0, EPI_RESIDUAL = 1, EPI_SWIGLU = 2 };
+//  EPI_QKV_ROPE: C = acc (+ bias) for the q heads after RoPE; k heads (RoPE) and v heads are written to
+//                their paged KV slots instead (QKV GEMM + RoPE + KV append fused; CTA-pair kernel only)
+enum { EPI_STORE = 0, EPI_RESIDUAL = 1, EPI_SWIGLU = 2, EPI_QKV_ROPE = 3 };
 
 struct GemmArgs {
   const void* A;
@@ -37,6 +39,8 @@ struct GemmArgs {
   const void* R2 = nullptr;
   void* C2 = nullptr;
   int row_split = 1 << 30;
+  // EPI_QKV_ROPE: the RoPE / KV-append operands (kernels.h RopeKvArgs; head_dim 128, page size 16)
+  const struct RopeKvArgs* rope = nullptr;
 };
 // fp32 partial floats a split-K launch of this shape needs (0 when it runs unsplit)
 size_t gemm_tc_splitk_need(int M, int N, int K, int epi);

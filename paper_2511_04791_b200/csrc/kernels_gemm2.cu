@@ -130,6 +130,14 @@ struct Params {
   const bf16* R2;
   bf16* C2;
   int row_split;  // rows >= row_split: residual from R2, output to C2 (row - row_split)
+  // EPI_QKV_ROPE (RoPE, reading #5; paged KV append before attention; C-3 slots)
+  const int* pos;
+  const int* tok_row;
+  const int* table;
+  int max_pages, hq, hkv;
+  bf16* k_pool;
+  bf16* v_pool;
+  const float2* rope;
 };
 
 template <int EPI>
@@ -241,6 +249,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN_PAIR;
       const int row = mp * PAIR_M + (int)rank * BM + lane_row;
       const int n0 = nb * OUT_COLS;
+      if constexpr (EPI == EPI_QKV_ROPE) {
+        // the tile's 256 columns are two whole heads (d_h = 128): rotate (i, i + 64) pairs of q and k
+        // heads at this row's position; q stays in C, k and v go to their KV slots
+        {  // tcgen05.ld is warp-collective: every lane loads, only rows < M store
+          const bool row_ok = row < p.M;
+          const int pos = row_ok ? p.pos[row] : 0;
+          const int page = row_ok ? p.table[(size_t)p.tok_row[row] * p.max_pages + (pos >> 4)] : 0;
+          const int slot = pos & 15;
+          const float2* cs = p.rope + (size_t)pos * 64;
+#pragma unroll 1
+          for (int hh = 0; hh < 2; ++hh) {
+            const int head = (n0 >> 7) + hh;
+            if (head * 128 >= p.N) break;
+            const bool is_q = head < p.hq, is_k = !is_q && head < p.hq + p.hkv;
+            bf16* dst = is_q ? p.C + (size_t)row * p.ldc + head * 128
+                             : (is_k ? p.k_pool : p.v_pool) +
+                                   (((size_t)page * p.hkv + (head - p.hq - (is_k ? 0 : p.hkv))) * 16 + slot) * 128;
+#pragma unroll 1
+            for (int c = 0; c < 64; c += 32) {
+              float x0[32], x1[32];
+              tmem_ld32(tbase + hh * 128 + c, x0);
+              tmem_ld32(tbase + hh * 128 + 64 + c, x1);
+              if (p.bias) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  float b0[8], b1[8];
+                  load16<bf16>(p.bias + head * 128 + c + q * 8, b0);
+                  load16<bf16>(p.bias + head * 128 + 64 + c + q * 8, b1);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    x0[q * 8 + e] += b0[e];
+                    x1[q * 8 + e] += b1[e];
+                  }
+                }
+              }
+              if (head < p.hq + p.hkv) {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                  const float2 r = cs[c + e];
+                  const float a = x0[e], b = x1[e];
+                  x0[e] = a * r.x - b * r.y;
+                  x1[e] = b * r.x + a * r.y;
+                }
+              }
+              if (row_ok) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  float o0[8], o1[8];
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    o0[e] = x0[q * 8 + e];
+                    o1[e] = x1[q * 8 + e];
+                  }
+                  store16<bf16>(dst + c + q * 8, o0);
+                  store16<bf16>(dst + 64 + c + q * 8, o1);
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_tempty0 + acc * 8);
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < OUT_COLS; c += 32) {
         float v[32];
@@ -362,6 +435,17 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   p.R2 = (const bf16*)a.R2;
   p.C2 = (bf16*)a.C2;
   p.row_split = a.row_split;
+  if constexpr (EPI == EPI_QKV_ROPE) {
+    p.pos = a.rope->pos;
+    p.tok_row = a.rope->tok_row;
+    p.table = a.rope->table;
+    p.max_pages = a.rope->max_pages;
+    p.hq = a.rope->hq;
+    p.hkv = a.rope->hkv;
+    p.k_pool = (bf16*)a.rope->k_pool;
+    p.v_pool = (bf16*)a.rope->v_pool;
+    p.rope = a.rope->rope;
+  }
   const int pairs = p.num_tiles < num_sms / 2 ? p.num_tiles : num_sms / 2;
   launch_pdl(gemm2_kernel<EPI>, 2 * pairs, THREADS, SMEM, st, mx, mw, p);
   return 1;
@@ -376,6 +460,7 @@ bool gemm2_supported(const GemmArgs& a, int num_sms) {
 }
 
 int launch_gemm2(const GemmArgs& a, int num_sms, cudaStream_t st) {
+  if (a.epi == EPI_QKV_ROPE) return a.rope ? tc2::launch<EPI_QKV_ROPE>(a, num_sms, st) : -1;
   if (a.epi == EPI_SWIGLU) return tc2::launch<EPI_SWIGLU>(a, num_sms, st);
   if (a.epi == EPI_RESIDUAL) return tc2::launch<EPI_RESIDUAL>(a, num_sms, st);
   return tc2::launch<EPI_STORE>(a, num_sms, st);
