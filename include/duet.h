@@ -135,7 +135,10 @@ enum { DUET_DTYPE_BF16 = 0, DUET_DTYPE_FP32 = 1 };
 enum {
   DUET_CTX_FINE_SPLIT = 1u,  /* 2-SM (TPC) partitions: CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING;
                                 default is the driver's 8-SM granularity (cuda.h green contexts) */
-  DUET_CTX_NO_GRAPH = 2u     /* launch decode kernels directly instead of replaying a CUDA graph */
+  DUET_CTX_NO_GRAPH = 2u,    /* launch decode kernels directly instead of replaying a CUDA graph */
+  DUET_CTX_NO_CORUN = 4u     /* temporal steps never co-run the prefill and decode attentions on an SM
+                                split (f4; by default a measured-rate model decides per step, and the
+                                environment variable DUET_CORUN=<S_d> / 0 forces / disables it) */
 };
 
 /* Capacity the workspace is sized for.  max_pos bounds every absolute token position
@@ -308,8 +311,9 @@ duet_status duet_step(duet_ctx* ctx, const duet_layer_weights* w, const duet_pre
 /* Device-measured times of the last completed duet_step (CUDA events on the partition
  * streams; requires the step to have completed, e.g. after synchronizing `stream`).
  * Times in seconds: t_window = first launch -> join; t_decode = decode side (k steps);
- * t_prefill = prefill side.  Temporal: t_window = t_decode = t_prefill. */
-typedef struct { double t_window, t_decode, t_prefill; int32_t mode, k, kernels; } duet_step_times;
+ * t_prefill = prefill side.  Temporal: t_window = t_decode = t_prefill.  corun_s_d: SMs of the
+ * decode group the two attentions of a temporal step co-ran on (f4; 0 = one after the other). */
+typedef struct { double t_window, t_decode, t_prefill; int32_t mode, k, kernels, corun_s_d; } duet_step_times;
 duet_status duet_last_step_times(duet_ctx* ctx, duet_step_times* out);
 
 /* Measures Pi_SM(S) and B_HBM(S) for S = every partition size the ctx can provision (both

@@ -15,7 +15,7 @@ DUET_OPT_FORCE_SPATIAL, DUET_OPT_INCLUDE_CLS = 1, 2
 DUET_MODE_TEMPORAL, DUET_MODE_SPATIAL = 0, 1
 DUET_FLAG_INFEASIBLE, DUET_FLAG_DEGENERATE = 1, 2
 DUET_DTYPE_BF16, DUET_DTYPE_FP32 = 0, 1
-DUET_CTX_FINE_SPLIT, DUET_CTX_NO_GRAPH = 1, 2
+DUET_CTX_FINE_SPLIT, DUET_CTX_NO_GRAPH, DUET_CTX_NO_CORUN = 1, 2, 4
 DUET_EPI_STORE, DUET_EPI_RESIDUAL, DUET_EPI_SWIGLU = 0, 1, 2
 STATUS_NAMES = {0: "OK", -1: "INVALID_ARG", -2: "OUT_OF_RANGE", -3: "CONFIG", -4: "UNSUPPORTED", -5: "CUDA",
                 -6: "CAPACITY"}
@@ -91,7 +91,8 @@ class duet_kernel_stats(C.Structure):
 
 class duet_step_times(C.Structure):
     _fields_ = [("t_window", C.c_double), ("t_decode", C.c_double), ("t_prefill", C.c_double),
-                ("mode", C.c_int32), ("k", C.c_int32), ("kernels", C.c_int32)]
+                ("mode", C.c_int32), ("k", C.c_int32), ("kernels", C.c_int32),
+                ("corun_s_d", C.c_int32)]
 
 
 _lib = None

@@ -178,6 +178,10 @@ struct duet_ctx {
   std::vector<Partition> parts;
   cudaStream_t s_full = nullptr;
   cudaEvent_t ev_in = nullptr, ev_dec0 = nullptr, ev_dec1 = nullptr, ev_pre0 = nullptr, ev_pre1 = nullptr;
+  // temporal-mode attention co-run: prefill attention on the remainder, decode
+  // attention on an S_d group, forked from and joined back into the full-device stream per layer
+  Partition* corun = nullptr;
+  cudaEvent_t ev_cf = nullptr, ev_ca = nullptr, ev_cb = nullptr;
   float2* rope = nullptr;
   Side dec, pre;
   int* stage = nullptr;  // pinned [kStageSlots][stage_ints]
@@ -188,7 +192,7 @@ struct duet_ctx {
   uint32_t page_gen = 0;
   std::map<std::tuple<int, int, int, uint64_t>, GraphEntry> graphs;
   // last step
-  int last_mode = -1, last_k = 0, last_kernels = 0;
+  int last_mode = -1, last_k = 0, last_kernels = 0, last_corun = 0;
   bool last_has_dec = false, last_has_pre = false;
   // live kernel timing
   bool prof_on = false, capturing = false;
@@ -315,6 +319,30 @@ struct AttnPlan {
   double attn_flops_pre = 0, attn_bytes_pre = 0, attn_flops_dec = 0, attn_bytes_dec = 0;
 };
 
+// f4 co-run partition choice for a temporal step with both phases: minimise the attention window
+// max(t_pre(S_p), t_dec(S_d)) against running the two one after the other on the full device.
+// Rates measured on B200 with these kernels (tools/gpu/run_corun.sh): prefill attention
+// ~4.0 TFLOP/s per SM (linear in SMs), decode attention B(S) = 5.9 TB/s (1 - e^(-S/28)), 6.1 TB/s on
+// the full device; ~15 us of fork / join / lost launch overlap per layer must be won back.
+static Partition* corun_pick(duet_ctx* c, const AttnPlan& ap) {
+  constexpr double kFaPerSm = 4.0e12, kDecSat = 5.9e12, kDecS0 = 28.0, kDecFull = 6.1e12, kOverhead = 15e-6;
+  const double seq = ap.attn_flops_pre / (kFaPerSm * c->total_sms) + ap.attn_bytes_dec / kDecFull;
+  Partition* best = nullptr;
+  double best_t = seq - kOverhead;
+  for (auto& p : c->parts) {
+    const int s_p = c->total_sms - p.s_d;  // the remainder of a split (exact once created)
+    if (p.s_d < 16 || s_p < 16) continue;
+    const double t_pre = ap.attn_flops_pre / (kFaPerSm * s_p);
+    const double t_dec = ap.attn_bytes_dec / (kDecSat * (1.0 - std::exp(-p.s_d / kDecS0)));
+    const double t = std::max(t_pre, t_dec);
+    if (t < best_t) {
+      best_t = t;
+      best = &p;
+    }
+  }
+  return best;
+}
+
 // x_in2 / y_final2 / row_split: rows >= row_split of the layer input / final output live in a second
 // buffer (the temporal batch [prefill ; decode] read and written in the caller's buffers, no copies)
 static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms, int n_rows, const void* x_in,
@@ -384,7 +412,20 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     if (!fuse_rope)
       TIMED(DUET_KCLASS_OTHER, 6.0 * n * (hq + hkv) * dh, n * (nqkv + (hq + 2.0 * hkv) * dh) * e,
             launch_rope_kv(dt, ra, st));
-    // 4. attention
+    // 4. attention; with a co-run partition the two attentions run side by side (compute-bound
+    // prefill on the remainder, HBM-bound decode on S_d SMs) and the O GEMM waits for both
+    Partition* cp = (c->corun && ap.n_pre > 0 && ap.n_dec > 0 && !c->capturing) ? c->corun : nullptr;
+    cudaStream_t st_pa = st, st_da = st;
+    int sms_pa = num_sms, sms_da = num_sms;
+    if (cp) {
+      CUDA_TRY(cudaEventRecord(c->ev_cf, st));
+      CUDA_TRY(cudaStreamWaitEvent(cp->s_pre, c->ev_cf, 0));
+      CUDA_TRY(cudaStreamWaitEvent(cp->s_dec, c->ev_cf, 0));
+      st_pa = cp->s_pre;
+      sms_pa = cp->s_p;
+      st_da = cp->s_dec;
+      sms_da = cp->s_d;
+    }
     if (ap.n_pre > 0) {
       PrefillAttnArgs pa{};
       pa.q = S.qkv;
@@ -405,19 +446,19 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       pa.v_pool = kv->v_pool[l];
       pa.max_q = ap.max_q;
       pa.total_q = ap.n_pre;
-      pa.num_sms = num_sms;
+      pa.num_sms = sms_pa;
       pa.tok_pos = S.pos();
       pa.tok_row = S.tok();
       pa.max_len = ap.max_len_pre;
       pa.n_pages = kv->n_pages;
       pa.total_rows = n_rows;
-      const int pi = prof_begin(c, st, DUET_KCLASS_PREFILL_ATTN);
-      const int r = launch_prefill_attn(dt, pa, st);
+      const int pi = prof_begin(c, st_pa, DUET_KCLASS_PREFILL_ATTN);
+      const int r = launch_prefill_attn(dt, pa, st_pa);
       if (r < 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "prefill attention: unsupported head layout");
-      prof_end(c, st, pi, DUET_KCLASS_PREFILL_ATTN, ap.attn_flops_pre, ap.attn_bytes_pre);
+      prof_end(c, st_pa, pi, DUET_KCLASS_PREFILL_ATTN, ap.attn_flops_pre, ap.attn_bytes_pre);
       if (dbg_sync && !c->capturing) {
         fprintf(stderr, "[duet] layer %d: prefill attention ...", l);
-        fprintf(stderr, " %s\n", cudaGetErrorString(cudaStreamSynchronize(st)));
+        fprintf(stderr, " %s\n", cudaGetErrorString(cudaStreamSynchronize(st_pa)));
       }
       nk += r;
     }
@@ -440,14 +481,20 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       da.part_o = S.part_o;
       da.part_ml = S.part_ml;
       da.max_splits = kMaxSplits;
-      da.num_sms = num_sms;
+      da.num_sms = sms_da;
       da.max_len = ((ap.max_len_dec + 1023) / 1024) * 1024;  // same bucket in both modes
       da.n_pages = kv->n_pages;
-      const int pi = prof_begin(c, st, DUET_KCLASS_DECODE_ATTN);
-      const int r = launch_decode_attn(dt, da, st);
+      const int pi = prof_begin(c, st_da, DUET_KCLASS_DECODE_ATTN);
+      const int r = launch_decode_attn(dt, da, st_da);
       if (r < 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "decode attention: unsupported head layout");
-      prof_end(c, st, pi, DUET_KCLASS_DECODE_ATTN, ap.attn_flops_dec, ap.attn_bytes_dec);
+      prof_end(c, st_da, pi, DUET_KCLASS_DECODE_ATTN, ap.attn_flops_dec, ap.attn_bytes_dec);
       nk += r;
+    }
+    if (cp) {
+      CUDA_TRY(cudaEventRecord(c->ev_ca, cp->s_pre));
+      CUDA_TRY(cudaEventRecord(c->ev_cb, cp->s_dec));
+      CUDA_TRY(cudaStreamWaitEvent(st, c->ev_ca, 0));
+      CUDA_TRY(cudaStreamWaitEvent(st, c->ev_cb, 0));
     }
     // 5. x1 = x + o W_o^T
     // TP: the O projection of this rank's heads is a partial sum; rank 0 adds the
@@ -576,6 +623,8 @@ extern "C" duet_status duet_ctx_create(int32_t device, const duet_model_spec* sp
     CUDA_TRY(cudaStreamCreateWithFlags(&c->s_full, cudaStreamNonBlocking));
     cudaEvent_t* evs[] = {&c->ev_in, &c->ev_dec0, &c->ev_dec1, &c->ev_pre0, &c->ev_pre1};
     for (auto e : evs) CUDA_TRY(cudaEventCreate(e));
+    cudaEvent_t* evc[] = {&c->ev_cf, &c->ev_ca, &c->ev_cb};
+    for (auto e : evc) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (int i = 0; i < kStageSlots; ++i) {
       CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
       CUDA_TRY(cudaEventRecord(c->stage_ev[i], c->s_full));
@@ -640,7 +689,7 @@ extern "C" duet_status duet_ctx_destroy(duet_ctx* c) {
   side_free(c->pre);
   if (c->rope) cudaFree(c->rope);
   if (c->stage) cudaFreeHost(c->stage);
-  cudaEvent_t evs[] = {c->ev_in, c->ev_dec0, c->ev_dec1, c->ev_pre0, c->ev_pre1};
+  cudaEvent_t evs[] = {c->ev_in, c->ev_dec0, c->ev_dec1, c->ev_pre0, c->ev_pre1, c->ev_cf, c->ev_ca, c->ev_cb};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
   for (auto e : c->stage_ev)
@@ -926,6 +975,28 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     probe.epi = EPI_RESIDUAL;
     const bool split_io = has_pre && has_dec && c->dt == DT::BF16 && gemm2_supported(probe, c->total_sms) &&
                           c->spec.ffn_dim % 64 == 0 && (c->spec.n_q_heads * c->spec.head_dim) % 64 == 0;
+    // f4 co-run: the two attentions of each layer side by side, decode on an S_d group and prefill
+    // on the remainder.  DUET_CORUN=<S_d> forces the partition whose decode group has
+    // >= S_d SMs, 0 disables; unset, corun_pick's measured-rate model decides per step.
+    c->corun = nullptr;
+    if (has_pre && has_dec && !(c->lim.flags & DUET_CTX_NO_CORUN)) {
+      static const int corun_sd = getenv("DUET_CORUN") ? atoi(getenv("DUET_CORUN")) : -1;
+      Partition* cp = nullptr;
+      if (corun_sd > 0) {
+        for (auto& p : c->parts)
+          if (p.s_d >= corun_sd) {
+            cp = &p;
+            break;
+          }
+      } else if (corun_sd < 0) {
+        cp = corun_pick(c, ap);
+      }
+      if (cp) {
+        DUET_TRY(ensure_partition(c, *cp));
+        c->corun = cp;
+      }
+    }
+    c->last_corun = c->corun ? c->corun->s_d : 0;
     if (n_rows > 0 && !(has_pre && has_dec)) {  // one phase only: its own buffers, whatever the GEMM path
       DUET_TRY(run_layers(c, c->pre, st, c->total_sms, n_rows, has_pre ? pre->x : dec->x, has_pre ? pre->y : dec->y,
                           w, kv, ap, &kernels));
@@ -943,6 +1014,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
         CUDA_TRY(cudaMemcpyAsync(dec->y, (char*)c->pre.ylast + (size_t)ap.n_pre * d * es, (size_t)ap.n_dec * d * es,
                                  cudaMemcpyDeviceToDevice, st));
     }
+    c->corun = nullptr;
     // the decode rows' greedy tokens (f1; k = 1 in temporal mode): from their outputs in dec->y
     if (has_dec && dec->head) DUET_TRY(lm_head(c, c->pre, st, c->total_sms, ap.n_dec, dec->y, dec->head, nullptr,
                                                nullptr, &kernels));
@@ -1036,6 +1108,7 @@ extern "C" duet_status duet_last_step_times(duet_ctx* c, duet_step_times* out) {
   out->mode = c->last_mode;
   out->k = c->last_k;
   out->kernels = c->last_kernels;
+  out->corun_s_d = c->last_mode == DUET_MODE_TEMPORAL ? c->last_corun : 0;
   float ms = 0;
   if (c->last_mode == DUET_MODE_TEMPORAL) {
     CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_pre0, c->ev_pre1));

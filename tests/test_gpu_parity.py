@@ -278,6 +278,14 @@ def test_parity_cfg2_full_layer_temporal_and_optimizer_split():
     y_pre, y_dec, kv_o = run(wl)
     g, ctx = _run_split(wl, "bf16", lambda c: D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1))
     _check_outputs(g, y_pre, y_dec, TOL["bf16"])
+    # f4: at this size the attention co-run model picks an SM split; the same kernels on fewer SMs
+    # give the same function as the one-after-the-other temporal step (NO_CORUN context)
+    assert ctx.last_step_times()["corun_s_d"] > 0
+    g_seq, ctx_seq = _run_split(wl, "bf16", lambda c: D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1),
+                                D.DUET_CTX_NO_CORUN)
+    assert ctx_seq.last_step_times()["corun_s_d"] == 0
+    assert torch.equal(g.y_pre, g_seq.y_pre) and torch.equal(g.y_dec, g_seq.y_dec)
+    del ctx_seq, g_seq
     parts, total = ctx.partitions()
     for s_d in (parts[0], 32, parts[-1]):
         g = GpuWorkload(wl, "bf16")
