@@ -184,7 +184,8 @@ struct duet_ctx {
   cudaEvent_t ev_cf = nullptr, ev_ca = nullptr, ev_cb = nullptr;
   float2* rope = nullptr;
   Side dec, pre;
-  int* stage = nullptr;  // pinned [kStageSlots][stage_ints]
+  int* stage = nullptr;  // pinned, mapped [kStageSlots][stage_ints]
+  int* stage_dev = nullptr;  // its device address (read zero-copy by launch_copy_bytes)
   size_t stage_ints = 0;
   cudaEvent_t stage_ev[kStageSlots] = {};
   int stage_next = 0;
@@ -535,6 +536,9 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
 }
 
 // Pinned staging slot (ring of kStageSlots; waits only if the host runs kStageSlots steps ahead).
+// device address of a staging-ring pointer (mapped pinned memory)
+static const int* stage_dev_ptr(const duet_ctx* c, const int* img) { return c->stage_dev + (img - c->stage); }
+
 static duet_status stage_slot(duet_ctx* c, int** out, int* slot) {
   const int s = c->stage_next;
   c->stage_next = (s + 1) % kStageSlots;
@@ -647,9 +651,10 @@ extern "C" duet_status duet_ctx_create(int32_t device, const duet_model_spec* sp
   STEP(side_alloc(c, c->dec, nd, 0, nd, nd));
   STEP(side_alloc(c, c->pre, np + nd, ns, ns + nd, nd));
   // pinned staging ring: large enough for the bigger side's metadata
-  c->stage_ints = std::max(c->dec.n_meta, c->pre.n_meta) * 2;
-  if (cudaMallocHost(&c->stage, kStageSlots * c->stage_ints * sizeof(int)) != cudaSuccess) {
-    set_error("cudaMallocHost of the staging ring failed");
+  c->stage_ints = (std::max(c->dec.n_meta, c->pre.n_meta) * 2 + 3) / 4 * 4;  // 16-B aligned slots
+  if (cudaHostAlloc(&c->stage, kStageSlots * c->stage_ints * sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&c->stage_dev, c->stage, 0) != cudaSuccess) {
+    set_error("cudaHostAlloc of the staging ring failed");
     return fail(DUET_ERR_CUDA);
   }
   // decode rows use identity page-table rows (row r of the decode table)
@@ -963,7 +968,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     CUDA_TRY(cudaEventRecord(c->ev_in, ust));
     CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in, 0));
     CUDA_TRY(cudaEventRecord(c->ev_pre0, st));
-    CUDA_TRY(cudaMemcpyAsync(c->pre.meta, img, n_int * sizeof(int), cudaMemcpyHostToDevice, st));
+    kernels += launch_copy_bytes(c->pre.meta, stage_dev_ptr(c, img), n_int * sizeof(int), c->total_sms, st);
     CUDA_TRY(cudaEventRecord(c->stage_ev[slot], st));
     // [prefill ; decode] rows straight from / into the caller's buffers when the CTA-pair GEMM runs
     // the O and down projections (it reads the residual and writes the output per row range)
@@ -1004,15 +1009,15 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
       DUET_TRY(run_layers(c, c->pre, st, c->total_sms, n_rows, pre->x, pre->y, w, kv, ap, &kernels, dec->x, dec->y,
                           ap.n_pre));
     } else if (n_rows > 0) {
-      if (has_pre) CUDA_TRY(cudaMemcpyAsync(c->pre.xin, pre->x, (size_t)ap.n_pre * d * es, cudaMemcpyDeviceToDevice, st));
+      if (has_pre) kernels += launch_copy_bytes(c->pre.xin, pre->x, (size_t)ap.n_pre * d * es, c->total_sms, st);
       if (has_dec)
-        CUDA_TRY(cudaMemcpyAsync((char*)c->pre.xin + (size_t)ap.n_pre * d * es, dec->x, (size_t)ap.n_dec * d * es,
-                                 cudaMemcpyDeviceToDevice, st));
+        kernels += launch_copy_bytes((char*)c->pre.xin + (size_t)ap.n_pre * d * es, dec->x, (size_t)ap.n_dec * d * es,
+                                     c->total_sms, st);
       DUET_TRY(run_layers(c, c->pre, st, c->total_sms, n_rows, c->pre.xin, c->pre.ylast, w, kv, ap, &kernels));
-      if (has_pre) CUDA_TRY(cudaMemcpyAsync(pre->y, c->pre.ylast, (size_t)ap.n_pre * d * es, cudaMemcpyDeviceToDevice, st));
+      if (has_pre) kernels += launch_copy_bytes(pre->y, c->pre.ylast, (size_t)ap.n_pre * d * es, c->total_sms, st);
       if (has_dec)
-        CUDA_TRY(cudaMemcpyAsync(dec->y, (char*)c->pre.ylast + (size_t)ap.n_pre * d * es, (size_t)ap.n_dec * d * es,
-                                 cudaMemcpyDeviceToDevice, st));
+        kernels += launch_copy_bytes(dec->y, (char*)c->pre.ylast + (size_t)ap.n_pre * d * es, (size_t)ap.n_dec * d * es,
+                                     c->total_sms, st);
     }
     c->corun = nullptr;
     // the decode rows' greedy tokens (f1; k = 1 in temporal mode): from their outputs in dec->y
@@ -1042,10 +1047,10 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     cudaStream_t st = P->s_dec;
     CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in, 0));
     CUDA_TRY(cudaEventRecord(c->ev_dec0, st));
-    CUDA_TRY(cudaMemcpyAsync(c->dec.meta, img, n_int * sizeof(int), cudaMemcpyHostToDevice, st));
+    kernels += launch_copy_bytes(c->dec.meta, stage_dev_ptr(c, img), n_int * sizeof(int), P->s_d, st);
     CUDA_TRY(cudaEventRecord(c->stage_ev[slot], st));
     const int n = ap.n_dec;
-    CUDA_TRY(cudaMemcpyAsync(c->dec.xin, dec->x, (size_t)n * d * es, cudaMemcpyDeviceToDevice, st));
+    kernels += launch_copy_bytes(c->dec.xin, dec->x, (size_t)n * d * es, P->s_d, st);
     int max_c = 0;
     for (int r = 0; r < n; ++r) max_c = std::max(max_c, dec->c[r]);
     const int max_len = ((max_c + k + 1023) / 1024) * 1024;  // bucket: graphs survive context growth
@@ -1088,7 +1093,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     cudaStream_t st = P->s_pre;
     CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in, 0));
     CUDA_TRY(cudaEventRecord(c->ev_pre0, st));
-    CUDA_TRY(cudaMemcpyAsync(c->pre.meta, img, n_int * sizeof(int), cudaMemcpyHostToDevice, st));
+    kernels += launch_copy_bytes(c->pre.meta, stage_dev_ptr(c, img), n_int * sizeof(int), P->s_p, st);
     CUDA_TRY(cudaEventRecord(c->stage_ev[slot], st));
     DUET_TRY(run_layers(c, c->pre, st, P->s_p, ap.n_pre, pre->x, pre->y, w, kv, ap, &kernels));
     CUDA_TRY(cudaEventRecord(c->ev_pre1, st));

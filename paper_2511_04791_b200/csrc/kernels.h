@@ -152,5 +152,7 @@ int launch_stream_read(const void* buf, size_t n_bytes, unsigned long long* sink
 int launch_stream_pages(const void* buf, size_t n_bytes, unsigned long long* sink, int num_sms, cudaStream_t st);
 // hashed values in [-1, 1) (calibration operands)
 int launch_fill_hash(DT dt, void* p, size_t n_elems, uint32_t seed, cudaStream_t st);
+// dst <- src on the SMs (src may be mapped pinned host memory: zero-copy over PCIe); no copy engine
+int launch_copy_bytes(void* dst, const void* src, size_t bytes, int num_sms, cudaStream_t st);
 
 }  // namespace duet

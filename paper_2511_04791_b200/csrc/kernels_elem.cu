@@ -381,4 +381,29 @@ int launch_stream_pages(const void* buf, size_t n_bytes, unsigned long long* sin
   return 1;
 }
 
+// ---------------------------------------------------------------- copies on the SMs
+// The per-step metadata (from the pinned staging ring, read zero-copy over PCIe) and the activation
+// copies of the non-fused paths.  Not cudaMemcpyAsync: a copy-engine transfer queues behind whatever
+// bulk H2D / D2H the caller has in flight on the same engine (the caller's next-step inputs), which
+// would stall the step's first kernel by a whole PCIe transfer.
+__global__ void __launch_bounds__(256) copy_bytes_kernel(char* __restrict__ dst, const char* __restrict__ src,
+                                                          size_t n16, size_t bytes) {
+  pdl_wait();
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (size_t i = t; i < n16; i += stride)
+    reinterpret_cast<uint4*>(dst)[i] = __ldcv(reinterpret_cast<const uint4*>(src) + i);
+  for (size_t i = n16 * 16 + t; i < bytes; i += stride) dst[i] = src[i];
+}
+
+int launch_copy_bytes(void* dst, const void* src, size_t bytes, int num_sms, cudaStream_t st) {
+  if (bytes == 0) return 0;
+  const bool al = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  const size_t n16 = al ? bytes / 16 : 0;
+  const size_t work = al ? n16 : bytes;
+  const int grid = (int)std::max<size_t>(1, std::min<size_t>((work + 255) / 256, (size_t)num_sms * 4));
+  launch_pdl(copy_bytes_kernel, grid, 256, 0, st, (char*)dst, (const char*)src, n16, bytes);
+  return 1;
+}
+
 }  // namespace duet
