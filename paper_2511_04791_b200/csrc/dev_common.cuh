@@ -1,5 +1,6 @@
 // Device helpers shared by the kernels: element conversions, vector loads, warp reductions.
 #pragma once
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -24,6 +25,12 @@ __device__ __forceinline__ void pdl_trigger() {
 #endif
 }
 
+// DUET_PDL=0: plain stream-ordered launches (A/B and triage)
+inline bool pdl_enabled() {
+  static const bool on = !getenv("DUET_PDL") || atoi(getenv("DUET_PDL")) != 0;
+  return on;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args... args) {
@@ -36,7 +43,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 

@@ -188,6 +188,10 @@ struct duet_ctx {
   int* stage_dev = nullptr;  // its device address (read zero-copy by launch_copy_bytes)
   size_t stage_ints = 0;
   cudaEvent_t stage_ev[kStageSlots] = {};
+  // metadata prefetch (§5.3): device copy of the ring, filled on s_up as soon as duet_step is called
+  int* stage_d = nullptr;
+  cudaStream_t s_up = nullptr;
+  cudaEvent_t up_ev[kStageSlots] = {}, use_ev[kStageSlots] = {};
   int stage_next = 0;
   std::vector<uint32_t> page_mark;
   uint32_t page_gen = 0;
@@ -536,8 +540,28 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
 }
 
 // Pinned staging slot (ring of kStageSlots; waits only if the host runs kStageSlots steps ahead).
-// device address of a staging-ring pointer (mapped pinned memory)
-static const int* stage_dev_ptr(const duet_ctx* c, const int* img) { return c->stage_dev + (img - c->stage); }
+// Side metadata <- staging slot, on stream st ahead of the step's kernels.  Default: the slot is
+// uploaded right away on s_up (an early copy-engine H2D into a device ring, off the step's critical
+// path) and copied device-to-device on st; DUET_META=0: st reads the mapped slot zero-copy.
+static duet_status upload_meta(duet_ctx* c, Side& S, const int* img, int slot, size_t n_int, int num_sms,
+                               cudaStream_t st, int* kernels) {
+  static const bool prefetch = !getenv("DUET_META") || atoi(getenv("DUET_META")) != 0;
+  const size_t bytes = n_int * sizeof(int);
+  if (prefetch) {
+    int* ring = c->stage_d + (size_t)slot * c->stage_ints;
+    CUDA_TRY(cudaStreamWaitEvent(c->s_up, c->use_ev[slot], 0));  // the slot's previous reader is done
+    CUDA_TRY(cudaMemcpyAsync(ring, img, bytes, cudaMemcpyHostToDevice, c->s_up));
+    CUDA_TRY(cudaEventRecord(c->up_ev[slot], c->s_up));
+    CUDA_TRY(cudaEventRecord(c->stage_ev[slot], c->s_up));  // host slot reusable once uploaded
+    CUDA_TRY(cudaStreamWaitEvent(st, c->up_ev[slot], 0));
+    *kernels += launch_copy_bytes(S.meta, ring, bytes, num_sms, st);
+    CUDA_TRY(cudaEventRecord(c->use_ev[slot], st));
+  } else {
+    *kernels += launch_copy_bytes(S.meta, c->stage_dev + (img - c->stage), bytes, num_sms, st);
+    CUDA_TRY(cudaEventRecord(c->stage_ev[slot], st));
+  }
+  return DUET_OK;
+}
 
 static duet_status stage_slot(duet_ctx* c, int** out, int* slot) {
   const int s = c->stage_next;
@@ -629,9 +653,13 @@ extern "C" duet_status duet_ctx_create(int32_t device, const duet_model_spec* sp
     for (auto e : evs) CUDA_TRY(cudaEventCreate(e));
     cudaEvent_t* evc[] = {&c->ev_cf, &c->ev_ca, &c->ev_cb};
     for (auto e : evc) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->s_up, cudaStreamNonBlocking));
     for (int i = 0; i < kStageSlots; ++i) {
       CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
       CUDA_TRY(cudaEventRecord(c->stage_ev[i], c->s_full));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->up_ev[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->use_ev[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(c->use_ev[i], c->s_full));
     }
     // RoPE table (reading #5): theta_i = theta^(-2i/d_h), phi = p theta_i, computed in double
     const int half = spec->head_dim / 2;
@@ -653,7 +681,8 @@ extern "C" duet_status duet_ctx_create(int32_t device, const duet_model_spec* sp
   // pinned staging ring: large enough for the bigger side's metadata
   c->stage_ints = (std::max(c->dec.n_meta, c->pre.n_meta) * 2 + 3) / 4 * 4;  // 16-B aligned slots
   if (cudaHostAlloc(&c->stage, kStageSlots * c->stage_ints * sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
-      cudaHostGetDevicePointer(&c->stage_dev, c->stage, 0) != cudaSuccess) {
+      cudaHostGetDevicePointer(&c->stage_dev, c->stage, 0) != cudaSuccess ||
+      cudaMalloc(&c->stage_d, kStageSlots * c->stage_ints * sizeof(int)) != cudaSuccess) {
     set_error("cudaHostAlloc of the staging ring failed");
     return fail(DUET_ERR_CUDA);
   }
@@ -694,6 +723,12 @@ extern "C" duet_status duet_ctx_destroy(duet_ctx* c) {
   side_free(c->pre);
   if (c->rope) cudaFree(c->rope);
   if (c->stage) cudaFreeHost(c->stage);
+  if (c->stage_d) cudaFree(c->stage_d);
+  if (c->s_up) cudaStreamDestroy(c->s_up);
+  for (int i = 0; i < kStageSlots; ++i) {
+    if (c->up_ev[i]) cudaEventDestroy(c->up_ev[i]);
+    if (c->use_ev[i]) cudaEventDestroy(c->use_ev[i]);
+  }
   cudaEvent_t evs[] = {c->ev_in, c->ev_dec0, c->ev_dec1, c->ev_pre0, c->ev_pre1, c->ev_cf, c->ev_ca, c->ev_cb};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
@@ -968,8 +1003,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     CUDA_TRY(cudaEventRecord(c->ev_in, ust));
     CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in, 0));
     CUDA_TRY(cudaEventRecord(c->ev_pre0, st));
-    kernels += launch_copy_bytes(c->pre.meta, stage_dev_ptr(c, img), n_int * sizeof(int), c->total_sms, st);
-    CUDA_TRY(cudaEventRecord(c->stage_ev[slot], st));
+    DUET_TRY(upload_meta(c, c->pre, img, slot, n_int, c->total_sms, st, &kernels));
     // [prefill ; decode] rows straight from / into the caller's buffers when the CTA-pair GEMM runs
     // the O and down projections (it reads the residual and writes the output per row range)
     GemmArgs probe{};
@@ -1047,8 +1081,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     cudaStream_t st = P->s_dec;
     CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in, 0));
     CUDA_TRY(cudaEventRecord(c->ev_dec0, st));
-    kernels += launch_copy_bytes(c->dec.meta, stage_dev_ptr(c, img), n_int * sizeof(int), P->s_d, st);
-    CUDA_TRY(cudaEventRecord(c->stage_ev[slot], st));
+    DUET_TRY(upload_meta(c, c->dec, img, slot, n_int, P->s_d, st, &kernels));
     const int n = ap.n_dec;
     kernels += launch_copy_bytes(c->dec.xin, dec->x, (size_t)n * d * es, P->s_d, st);
     int max_c = 0;
@@ -1093,8 +1126,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     cudaStream_t st = P->s_pre;
     CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in, 0));
     CUDA_TRY(cudaEventRecord(c->ev_pre0, st));
-    kernels += launch_copy_bytes(c->pre.meta, stage_dev_ptr(c, img), n_int * sizeof(int), P->s_p, st);
-    CUDA_TRY(cudaEventRecord(c->stage_ev[slot], st));
+    DUET_TRY(upload_meta(c, c->pre, img, slot, n_int, P->s_p, st, &kernels));
     DUET_TRY(run_layers(c, c->pre, st, P->s_p, ap.n_pre, pre->x, pre->y, w, kv, ap, &kernels));
     CUDA_TRY(cudaEventRecord(c->ev_pre1, st));
   }
