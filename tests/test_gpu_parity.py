@@ -439,3 +439,18 @@ def test_iteration_stream_served_trace_vs_oracle():
     assert it_no >= 6 and sched.free_pages() == n_pages
     ctx.close()
     sched.close()
+
+
+@pytest.mark.skipif(bool(__import__("os").environ.get("DUET_CORUN")), reason="already the forced co-run run")
+def test_forced_attention_corun_parity_subprocess():
+    """f4 co-run forced onto small ragged batches (a fresh process: the switch is read once per process):
+    the Llama ragged-prefix, Qwen GQA-5 + bias and running-max re-base cases pass against the oracle with
+    the two attentions of every temporal step on a 16-SM decode group and the remainder."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DUET_CORUN="16")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        "-k", "llama_shapes or qwen or running_max"], env=env, capture_output=True, text=True,
+                       timeout=900, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "3 passed" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
