@@ -620,6 +620,7 @@ def main():
                                                                       else ""),
                        "mode": ["temporal", "spatial"][split.mode],
                        "s_p": split.s_p, "s_d": split.s_d, "k": split.k, "flags": split.flags,
+                       "attention_corun_s_d": times["corun_s_d"],
                        "tau_ms": tau * 1e3, "prefill_tokens": n_p, "decode_reqs": n_d,
                        "l2": f"inputs > L2 ({step_bytes / 1e9:.1f} GB of weights + KV read per step), no flush",
                        "parallelism": f"tp{tp} (head-sharded, NCCL allreduce after O and down)" if tp > 1
