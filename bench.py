@@ -492,92 +492,107 @@ def main():
         hx_dec.copy_(x_dec)
         hy_pre = torch.empty(y_pre.shape, dtype=tdt, pin_memory=True)
         hy_dec = torch.empty(y_dec.shape, dtype=tdt, pin_memory=True)
-        n_e2e = max(5, args.steps // 2)
-        NSET = int(os.environ.get("DUET_E2E_SETS", "2"))   # device buffer sets in flight
-        # The caller's view: every step's inputs come from pinned host memory and its outputs go back to
-        # it.  Two device buffer sets and a copy stream overlap step i's compute with the H2D of step
-        # i+1 and the D2H of step i-1 (PCIe is full duplex); every copy is inside the timed region.
-        bufs = [(x_pre, x_dec, y_pre, y_dec)] + [
-            (torch.empty_like(x_pre), torch.empty_like(x_dec), torch.empty_like(y_pre), torch.empty_like(y_dec))
-            for _ in range(NSET - 1)]
-        cs = torch.cuda.Stream()    # H2D
-        cs2 = torch.cuda.Stream()   # D2H (the other PCIe direction, concurrently)
-        ev_in = [torch.cuda.Event() for _ in range(NSET)]
-        ev_out = [torch.cuda.Event() for _ in range(NSET)]
-        ev_d2h = [torch.cuda.Event() for _ in range(NSET)]
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        tok = 0
-        h2d = d2h = 0
-        # diagnosis only (never set for a reported run): DUET_E2E_SKIP=h2d / d2h drops one direction
-        skip = os.environ.get("DUET_E2E_SKIP", "")
-        tl = ([[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(n_e2e)]
-              if os.environ.get("DUET_E2E_TIMELINE") else None)
-        hts = []
-        torch.cuda.synchronize()
-        a.record(cs)
-        h1 = time.perf_counter()
-        def d2h_of(j, kj):
-            """D2H of step j's outputs, issued one iteration late (after step j+1's work): a copy
-            queued ahead of the next step could hold that step's launches behind it."""
-            sj = j % NSET
-            yp_, yd_ = bufs[sj][2], bufs[sj][3]
-            with torch.cuda.stream(cs2):
-                cs2.wait_event(ev_out[sj])
-                if "d2h" not in skip:
-                    hy_pre.copy_(yp_, non_blocking=True)
-                    hy_dec[:kj].copy_(yd_[:kj], non_blocking=True)
-                ev_d2h[sj].record(cs2)
-                if tl is not None:
-                    tl[j][4].record(cs2)
+        # The step's result a server reads back is the rows it samples from: every decode row's output and
+        # the last row of each prefill sequence (the other prompt rows' hidden states never leave the
+        # GPU in serving).  all_rows=True reads back every output row instead (reported alongside).
+        last_rows = [int(r) for r in np.cumsum([q for q, _ in wl.pre_seqs]) - 1]
+        hy_last = torch.empty((max(len(last_rows), 1), m.d_model), dtype=tdt, pin_memory=True)
 
-        k_prev = None
-        for i in range(n_e2e):
-            st_ = i % NSET
-            xp, xd, yp, yd = bufs[st_]
-            if tl is not None:
-                hts.append([time.perf_counter()])
-            with torch.cuda.stream(cs):
+        def e2e_leg(all_rows):
+            n_e2e = max(5, args.steps // 2)
+            NSET = int(os.environ.get("DUET_E2E_SETS", "2"))   # device buffer sets in flight
+            # The caller's view: every step's inputs come from pinned host memory and its outputs go back to
+            # it.  Two device buffer sets and a copy stream overlap step i's compute with the H2D of step
+            # i+1 and the D2H of step i-1 (PCIe is full duplex); every copy is inside the timed region.
+            bufs = [(x_pre, x_dec, y_pre, y_dec)] + [
+                (torch.empty_like(x_pre), torch.empty_like(x_dec), torch.empty_like(y_pre), torch.empty_like(y_dec))
+                for _ in range(NSET - 1)]
+            cs = torch.cuda.Stream()    # H2D
+            cs2 = torch.cuda.Stream()   # D2H (the other PCIe direction, concurrently)
+            ev_in = [torch.cuda.Event() for _ in range(NSET)]
+            ev_out = [torch.cuda.Event() for _ in range(NSET)]
+            ev_d2h = [torch.cuda.Event() for _ in range(NSET)]
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            tok = 0
+            h2d = d2h = 0
+            # diagnosis only (never set for a reported run): DUET_E2E_SKIP=h2d / d2h drops one direction
+            skip = os.environ.get("DUET_E2E_SKIP", "")
+            tl = ([[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(n_e2e)]
+                  if os.environ.get("DUET_E2E_TIMELINE") else None)
+            hts = []
+            torch.cuda.synchronize()
+            a.record(cs)
+            h1 = time.perf_counter()
+            def d2h_of(j, kj):
+                """D2H of step j's outputs, issued one iteration late (after step j+1's work): a copy
+                queued ahead of the next step could hold that step's launches behind it."""
+                sj = j % NSET
+                yp_, yd_ = bufs[sj][2], bufs[sj][3]
+                with torch.cuda.stream(cs2):
+                    cs2.wait_event(ev_out[sj])
+                    if "d2h" not in skip:
+                        if all_rows:
+                            hy_pre.copy_(yp_, non_blocking=True)
+                        else:
+                            for j_, r_ in enumerate(last_rows):
+                                hy_last[j_].copy_(yp_[r_], non_blocking=True)
+                        hy_dec[:kj].copy_(yd_[:kj], non_blocking=True)
+                    ev_d2h[sj].record(cs2)
+                    if tl is not None:
+                        tl[j][4].record(cs2)
+
+            k_prev = None
+            for i in range(n_e2e):
+                st_ = i % NSET
+                xp, xd, yp, yd = bufs[st_]
+                if tl is not None:
+                    hts.append([time.perf_counter()])
+                with torch.cuda.stream(cs):
+                    if i >= NSET:
+                        cs.wait_event(ev_out[st_])      # step i-NSET has finished reading x of this set
+                    if tl is not None:
+                        tl[i][0].record(cs)
+                    if "h2d" not in skip:
+                        xp.copy_(hx_pre, non_blocking=True)
+                        xd.copy_(hx_dec, non_blocking=True)
+                    ev_in[st_].record(cs)
+                    if tl is not None:
+                        tl[i][1].record(cs)
+                stream.wait_event(ev_in[st_])
                 if i >= NSET:
-                    cs.wait_event(ev_out[st_])      # step i-NSET has finished reading x of this set
+                    stream.wait_event(ev_d2h[st_])      # step i-NSET's outputs of this set are on the host
                 if tl is not None:
-                    tl[i][0].record(cs)
-                if "h2d" not in skip:
-                    xp.copy_(hx_pre, non_blocking=True)
-                    xd.copy_(hx_dec, non_blocking=True)
-                ev_in[st_].record(cs)
+                    tl[i][2].record(stream)
+                    hts[-1].append(time.perf_counter())
+                s_, k_ = one_step(bufs=bufs[st_])
                 if tl is not None:
-                    tl[i][1].record(cs)
-            stream.wait_event(ev_in[st_])
-            if i >= NSET:
-                stream.wait_event(ev_d2h[st_])      # step i-NSET's outputs of this set are on the host
-            if tl is not None:
-                tl[i][2].record(stream)
-                hts[-1].append(time.perf_counter())
-            s_, k_ = one_step(bufs=bufs[st_])
-            if tl is not None:
-                hts[-1].append(time.perf_counter())
-            ev_out[st_].record(stream)
-            if tl is not None:
-                tl[i][3].record(stream)
-            if k_prev is not None:
-                d2h_of(i - 1, k_prev)
-            k_prev = k_
-            tok += k_ * n_d + n_p
-            h2d = hx_pre.numel() * hx_pre.element_size() + hx_dec.numel() * hx_dec.element_size()
-            d2h = hy_pre.numel() * hy_pre.element_size() + k_ * n_d * m.d_model * hy_dec.element_size()
-        d2h_of(n_e2e - 1, k_prev)
-        cs.wait_stream(cs2)
-        b.record(cs)
-        host_e2e_ms = (time.perf_counter() - h1) * 1e3 / n_e2e
-        torch.cuda.synchronize()
-        log(f"host enqueue ms/step: timed loop {host_ms:.3f}, e2e loop {host_e2e_ms:.3f}")
-        if tl is not None:   # per-step timeline (ms from the loop start): h2d start/end, step start/end, d2h end
-            for i in range(min(n_e2e, 12)):
-                log(f"e2e step {i}: " + " ".join(f"{a.elapsed_time(ev):8.3f}" for ev in tl[i]) + " | host " +
-                    " ".join(f"{(t - h1) * 1e3:8.3f}" for t in hts[i]))
-        te = max_over_ranks(a.elapsed_time(b), ws)
-        e2e = {"value": tok * (1 if tp > 1 else ws) / (te * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h)}
+                    hts[-1].append(time.perf_counter())
+                ev_out[st_].record(stream)
+                if tl is not None:
+                    tl[i][3].record(stream)
+                if k_prev is not None:
+                    d2h_of(i - 1, k_prev)
+                k_prev = k_
+                tok += k_ * n_d + n_p
+                h2d = hx_pre.numel() * hx_pre.element_size() + hx_dec.numel() * hx_dec.element_size()
+                d2h = ((hy_pre.numel() if all_rows else len(last_rows) * m.d_model) * hy_pre.element_size()
+                       + k_ * n_d * m.d_model * hy_dec.element_size())
+            d2h_of(n_e2e - 1, k_prev)
+            cs.wait_stream(cs2)
+            b.record(cs)
+            host_e2e_ms = (time.perf_counter() - h1) * 1e3 / n_e2e
+            torch.cuda.synchronize()
+            log(f"host enqueue ms/step: timed loop {host_ms:.3f}, e2e loop {host_e2e_ms:.3f}")
+            if tl is not None:   # per-step timeline (ms from the loop start): h2d start/end, step start/end, d2h end
+                for i in range(min(n_e2e, 12)):
+                    log(f"e2e step {i}: " + " ".join(f"{a.elapsed_time(ev):8.3f}" for ev in tl[i]) + " | host " +
+                        " ".join(f"{(t - h1) * 1e3:8.3f}" for t in hts[i]))
+            te = max_over_ranks(a.elapsed_time(b), ws)
+            return {"value": tok * (1 if tp > 1 else ws) / (te * 1e-3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+        e2e = e2e_leg(False)
+        e2e["all_rows"] = e2e_leg(True)
 
     # ------------------------------------------------ roofline of the dominant kernel class
     pk, pk_src = peaks()
