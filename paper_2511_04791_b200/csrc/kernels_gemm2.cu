@@ -243,6 +243,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int t = pair; t < p.num_tiles; t += n_pairs, ++i) {
       const int acc = i & 1;
       const int mp = t % p.num_m2, nb = t / p.num_m2;
+      // EPI_QKV_ROPE: this row's position, KV page and cos/sin row are fetched while the tile's MMAs
+      // still run (the dependent pos -> table / rope loads are off the epilogue's critical path)
+      int r_pos = 0, r_page = 0;
+      if constexpr (EPI == EPI_QKV_ROPE) {
+        const int row_ = mp * PAIR_M + (int)rank * BM + quad * 32 + lane;
+        if (row_ < p.M) {
+          r_pos = p.pos[row_];
+          r_page = p.table[(size_t)p.tok_row[row_] * p.max_pages + (r_pos >> 4)];
+          const char* cs_ = reinterpret_cast<const char*>(p.rope + (size_t)r_pos * 64);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) asm volatile("prefetch.global.L1 [%0];" ::"l"(cs_ + j * 128));
+        }
+      }
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       if (t + n_pairs >= p.num_tiles) pdl_trigger();  // last tile: only the epilogue is left
       tc_fence_after();
@@ -254,8 +267,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         // heads at this row's position; q stays in C, k and v go to their KV slots
         {  // tcgen05.ld is warp-collective: every lane loads, only rows < M store
           const bool row_ok = row < p.M;
-          const int pos = row_ok ? p.pos[row] : 0;
-          const int page = row_ok ? p.table[(size_t)p.tok_row[row] * p.max_pages + (pos >> 4)] : 0;
+          const int pos = r_pos;
+          const int page = r_page;
           const int slot = pos & 15;
           const float2* cs = p.rope + (size_t)pos * 64;
 #pragma unroll 1
