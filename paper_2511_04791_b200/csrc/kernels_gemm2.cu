@@ -180,25 +180,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync();  // barriers initialised and TMEM allocated in both CTAs before any remote access
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();  // set-up above overlaps the previous kernel's tail; its outputs are read below
+  // set-up above overlaps the previous kernel's tail; its outputs are read below.  The producer waits
+  // later: the weights (never written by an earlier kernel) of its first stages are requested first.
+  if (warp != 0) pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs): own X rows and own W rows; leader's `full` counts both
       asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+      auto w_row = [&](int nb) {
+        return EPI == EPI_SWIGLU ? (rank ? p.n_up_off : 0) + nb * 128 : nb * BN_PAIR + (int)rank * 128;
+      };
+      int pre = 0;
+#ifndef DUET_NO_WPREFETCH
+      if (pair < p.num_tiles) {  // fresh ring: the first STAGES stages are free
+        pre = num_k < STAGES ? num_k : STAGES;
+        const int row_w0 = w_row(pair / p.num_m2);
+        for (int kb = 0; kb < pre; ++kb) {
+          if (leader) mbar_expect_tx(&full[kb], 2 * STAGE_BYTES);
+          tma_load_2cta(&map_w, mapa(smem_u32(&full[kb]), 0), sB + kb * B_BYTES, kb * BK, row_w0);
+        }
+      }
+#endif
+      pdl_wait();
       int s = 0;
       uint32_t ph = 0;
       for (int t = pair; t < p.num_tiles; t += n_pairs) {
         const int mp = t % p.num_m2, nb = t / p.num_m2;
         const int row_x = mp * PAIR_M + (int)rank * BM;
-        const int row_w = EPI == EPI_SWIGLU ? (rank ? p.n_up_off : 0) + nb * 128 : nb * BN_PAIR + (int)rank * 128;
+        const int row_w = w_row(nb);
         for (int kb = 0; kb < num_k; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
           const uint32_t lbar = mapa(smem_u32(&full[s]), 0);
-          if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
-          tma_load_2cta(&map_x, lbar, sA + s * A_BYTES, kb * BK, row_x);
-          tma_load_2cta(&map_w, lbar, sB + s * B_BYTES, kb * BK, row_w);
+          if (t == pair && kb < pre) {  // weights already requested before pdl_wait
+            tma_load_2cta(&map_x, lbar, sA + s * A_BYTES, kb * BK, row_x);
+          } else {
+            mbar_wait(&empty[s], ph ^ 1);
+            if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+            tma_load_2cta(&map_x, lbar, sA + s * A_BYTES, kb * BK, row_x);
+            tma_load_2cta(&map_w, lbar, sB + s * B_BYTES, kb * BK, row_w);
+          }
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
