@@ -235,7 +235,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();  // set-up above overlaps the previous kernel's tail
+  // set-up above overlaps the previous kernel's tail.  Producers wait later: the weight tiles of their
+  // first ring pass (never written by an earlier kernel) are requested before the wait.
+  if (!(warp == 0 || warp >= 6)) pdl_wait();
 
   if (warp == 0 || warp >= 6) {
     if (lane == 0) {
@@ -244,6 +246,43 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
       uint64_t pol_w = 0;
       if constexpr (SWAP)  // weights are streamed once per step: evict-first keeps split-K partials in L2
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
+      auto load_w = [&](int s, int kb, int nb) {
+        if constexpr (SWAP) {
+          uint8_t* a_dst = sA + s * CF::A_BYTES;
+          const int j0 = nb * BM;
+          tma_load_2d_hint(&map_w, &full[s], a_dst, kb * BK, j0, pol_w);
+          if constexpr (EPI == EPI_SWIGLU)
+            tma_load_2d_hint(&map_w, &full[s], a_dst + BM * BK * 2, kb * BK, p.n_up_off + j0, pol_w);
+        } else {
+          uint8_t* b_dst = sB + s * CF::B_BYTES;
+          if constexpr (EPI == EPI_SWIGLU) {
+            const int j0 = nb * (BN / 2);
+            tma_load_2d(&map_w, &full[s], b_dst, kb * BK, j0);
+            tma_load_2d(&map_w, &full[s], b_dst + (BN / 2) * BK * 2, kb * BK, p.n_up_off + j0);
+          } else {
+            tma_load_2d(&map_w, &full[s], b_dst, kb * BK, nb * BN);
+          }
+        }
+      };
+      auto load_x = [&](int s, int kb, int mb) {
+        if constexpr (SWAP)
+          tma_load_2d(&map_x, &full[s], sB + s * CF::B_BYTES, kb * BK, mb * BN);
+        else
+          tma_load_2d(&map_x, &full[s], sA + s * CF::A_BYTES, kb * BK, mb * BM);
+      };
+      int pre = 0;
+#ifndef DUET_NO_WPREFETCH
+      if ((int)blockIdx.x < p.num_units) {  // fresh ring: the first S stages are free
+        int t, kb0, kb1;
+        unit_k(blockIdx.x, t, kb0, kb1);
+        pre = kb1 - kb0 < S ? kb1 - kb0 : S;
+        for (int it = pr; it < pre; it += CF::NPROD) {
+          mbar_expect_tx(&full[it], CF::STAGE_BYTES);
+          load_w(it, kb0 + it, t / p.num_m);
+        }
+      }
+#endif
+      pdl_wait();
       int it = 0;
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
         int t, kb0, kb1;
@@ -252,26 +291,14 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, SWAP>::THREADS, Cfg<BN, EPI, SWAP
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           if (it % CF::NPROD != pr) continue;
           const int s = it % S;
+          if (it < pre) {  // weights already requested before pdl_wait
+            load_x(s, kb, mb);
+            continue;
+          }
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           mbar_expect_tx(&full[s], CF::STAGE_BYTES);
-          uint8_t* a_dst = sA + s * CF::A_BYTES;
-          uint8_t* b_dst = sB + s * CF::B_BYTES;
-          if constexpr (SWAP) {
-            const int j0 = nb * BM;
-            tma_load_2d_hint(&map_w, &full[s], a_dst, kb * BK, j0, pol_w);
-            if constexpr (EPI == EPI_SWIGLU)
-              tma_load_2d_hint(&map_w, &full[s], a_dst + BM * BK * 2, kb * BK, p.n_up_off + j0, pol_w);
-            tma_load_2d(&map_x, &full[s], b_dst, kb * BK, mb * BN);
-          } else {
-            tma_load_2d(&map_x, &full[s], a_dst, kb * BK, mb * BM);
-            if constexpr (EPI == EPI_SWIGLU) {
-              const int j0 = nb * (BN / 2);
-              tma_load_2d(&map_w, &full[s], b_dst, kb * BK, j0);
-              tma_load_2d(&map_w, &full[s], b_dst + (BN / 2) * BK * 2, kb * BK, p.n_up_off + j0);
-            } else {
-              tma_load_2d(&map_w, &full[s], b_dst, kb * BK, nb * BN);
-            }
-          }
+          load_w(s, kb, nb);
+          load_x(s, kb, mb);
         }
       }
     }
