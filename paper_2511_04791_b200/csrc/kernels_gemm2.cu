@@ -320,11 +320,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               }
               if (head < p.hq + p.hkv) {
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                  const float2 r = cs[c + e];
-                  const float a = x0[e], b = x1[e];
-                  x0[e] = a * r.x - b * r.y;
-                  x1[e] = b * r.x + a * r.y;
+                for (int e = 0; e < 32; e += 2) {  // two (cos, sin) pairs per 16-B load
+                  const float4 r = __ldg(reinterpret_cast<const float4*>(cs + c + e));
+                  const float a0 = x0[e], b0 = x1[e], a1 = x0[e + 1], b1 = x1[e + 1];
+                  x0[e] = a0 * r.x - b0 * r.y;
+                  x1[e] = b0 * r.x + a0 * r.y;
+                  x0[e + 1] = a1 * r.z - b1 * r.w;
+                  x1[e + 1] = b1 * r.z + a1 * r.w;
                 }
               }
               if (row_ok) {
