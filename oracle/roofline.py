@@ -15,7 +15,9 @@ F = 5nd, B = 2nds; act F = 2nm', B = 3nm's (plain: 2nm's), #12 t_cls over entrie
 that emit logits, #13 TP shards h_q, h_kv, m by N, #14 allreduce third term
 verbatim, #16 S_d enumerated over the launcher's achievable list excluding
 S_d = S, #17 k clamped to [1, k_max], #18 strict ">" (first found wins),
-#19 temporal at equality, #20 infeasible fallback = argmin t_d, #21 a batch
+#19 temporal at equality, #20 infeasible fallback = argmin t_d, #20b the
+infeasible spatial fallback is kept only when its rho is not below the temporal
+rho (both violate tau; the paper's objective, throughput, decides), #21 a batch
 missing one phase runs temporally, #25 T_pre = sum q over prefill entries,
 T_dec = number of decode entries.
 """
@@ -25,7 +27,7 @@ import math
 from dataclasses import dataclass
 
 PHASE_PREFILL_FULL, PHASE_PREFILL_CHUNK, PHASE_DECODE = 0, 1, 2
-OPT_FORCE_SPATIAL, OPT_INCLUDE_CLS = 1, 2
+OPT_FORCE_SPATIAL, OPT_INCLUDE_CLS, OPT_VERBATIM_INFEASIBLE = 1, 2, 4
 FLAG_INFEASIBLE, FLAG_DEGENERATE = 1, 2
 MODE_TEMPORAL, MODE_SPATIAL = 0, 1
 
@@ -308,6 +310,11 @@ def _choose(sp: Spec, prof: Profile, batch: list, tau: float, k_max: int, opts: 
     if best is None:
         rho, best = infeasible_fallback(S, prof.cand_sd_sms, k_max, t_d_of, t_p_of, T_dec, T_pre)
         flags = FLAG_INFEASIBLE
+        # reading #20b: no split meets tau, so both modes miss the SLO; keep the spatial fallback only
+        # if its throughput rho is not below the temporal mixed batch's (the objective of Alg. 1)
+        rho_t = float(T_dec + T_pre) / t_mixed if t_mixed > 0 else 0.0
+        if rho < rho_t and not (opts & OPT_VERBATIM_INFEASIBLE) and not (opts & OPT_FORCE_SPATIAL):
+            return _temporal(batch, t_mixed, FLAG_INFEASIBLE, S)
     S_p, S_d, k, t_p, t_d = best
     return Split(MODE_SPATIAL, S_p, S_d, k, flags, t_mixed, t_p, t_d, rho)
 

@@ -173,7 +173,7 @@ def test_alg1_equals_exhaustive_1200_instances():
         sp = R.Spec(rnd.choice([1, 4, 32]), 4096, 14336, 32, 8, 128, 128256, 2)
         tau = 10 ** rnd.uniform(-5, -0.5)
         k_max = rnd.choice([1, 4, 32, 64])
-        opts = rnd.choice([0, R.OPT_FORCE_SPATIAL])
+        opts = rnd.choice([0, R.OPT_FORCE_SPATIAL, R.OPT_VERBATIM_INFEASIBLE])
         a = R.choose_split(sp, prof, batch, tau, k_max, opts)
         b = R.choose_split_exhaustive(sp, prof, batch, tau, k_max, opts)
         assert a == b, (i, a, b)
@@ -201,6 +201,41 @@ def test_gate_equality_and_degenerate_and_infeasible():
     s = R.choose_split(sp, prof, batch, 1e-15)                               # infeasible
     assert s.flags == R.FLAG_INFEASIBLE and s.mode == R.MODE_SPATIAL
     assert s.s_d == 1                                                         # flat profile: first argmin
+
+
+def test_infeasible_guard_reading_20b():
+    """Reading #20b.  When no S_d meets tau both modes miss the SLO; the argmin-t_d spatial fallback
+     is kept only if its throughput rho is not below the temporal batch's sum(q) / t_mixed.
+    (1) A Llama-3-70B-shaped layer stack at TP = 1 (a 16k prefill + 512 decodes at 4k, tau = 5 ms) on a
+    profile linear in FLOPs and saturating in bandwidth: every S_d misses tau, the verbatim fallback is
+    the largest decode group with a sliver of SMs for the prefill, whose window is dominated by the
+    starved prefill (the 16x loss measured in round 1) -> temporal, flagged.  (2) On the flat profile
+    the fallback keeps its rho advantage -> spatial, flagged."""
+    sp = R.Spec(8, 8192, 28672, 64, 8, 128, 128256, 2)
+    S = 148
+    prof = R.Profile(S, tuple(range(8, S, 8)), tuple([0.0] + [1.6e15 * i / S for i in range(1, S + 1)]),
+                     tuple([0.0] + [6.5e12 * min(1.0, i / 40) for i in range(1, S + 1)]))
+    batch = [R.Req(16384, 0, R.PHASE_PREFILL_FULL)] + [R.Req(1, 4096, R.PHASE_DECODE)] * 512
+    verb = R.choose_split(sp, prof, batch, 5e-3, 32, R.OPT_VERBATIM_INFEASIBLE)
+    assert verb.mode == R.MODE_SPATIAL and verb.flags == R.FLAG_INFEASIBLE
+    # argmin t_d: the decode side's weight reads saturate the bandwidth at S_d >= 40, the remaining
+    # compute terms keep falling with S_d, so the fallback is the largest candidate (144 of 148 SMs)
+    assert verb.s_d == 144 and verb.s_p == 4
+    rho_t = (512 + 16384) / verb.t_mixed
+    assert verb.rho < rho_t / 4                    # the starved-prefill window: far worse throughput
+    g = R.choose_split(sp, prof, batch, 5e-3, 32, 0)
+    assert (g.mode, g.flags, g.s_p, g.s_d, g.k) == (R.MODE_TEMPORAL, R.FLAG_INFEASIBLE, S, 0, 1)
+    assert g.rho == rho_t and g.t_mixed == verb.t_mixed
+    assert R.choose_split_exhaustive(sp, prof, batch, 5e-3, 32, 0) == g
+    # FORCE_SPATIAL still returns the (flagged) spatial fallback: forcing is the caller's explicit request
+    assert R.choose_split(sp, prof, batch, 5e-3, 32, R.OPT_FORCE_SPATIAL).mode == R.MODE_SPATIAL
+    # (2) flat profile: both sides run at the full rate concurrently, the fallback's rho wins
+    prof2 = _flat_profile()
+    sp2 = R.Spec(1, 64, 96, 4, 2, 16, 100, 2)
+    b2 = [R.Req(50, 0, 0), R.Req(1, 100, 2)]
+    s2 = R.choose_split(sp2, prof2, b2, 1e-15)
+    assert s2.mode == R.MODE_SPATIAL and s2.flags == R.FLAG_INFEASIBLE
+    assert s2.rho >= 51 / s2.t_mixed
 
 
 def test_paper_qualitative_anchors():
