@@ -6,8 +6,10 @@ A step = one pass of the whole hot path over one mixed batch:
          duet_calibrate at start-up),
   a3-a7  duet_step: metadata staging, partition binding, k decode steps (CUDA-graph replays on the
          S_d partition) concurrently with the prefill chunk (S_p partition), join.
-Workload (N=1): cfg2 of BASELINE.json — Llama-3-8B layer shapes, bf16, prefill chunk 2048 + 64
-decodes at ctx 4096, TBT SLO 50 ms / 32 layers = 1.5625 ms per layer.  Synthetic seeded inputs
+Workload (N=1): cfg3 of BASELINE.json, the largest single-GPU configuration — Llama-3-8B, 32 layers,
+bf16: an 8k-token prompt arriving into 256 in-flight decodes at ctx 2k-8k, TBT SLO 50 ms (cfg3-fit, the
+2k-6k ramp, when the full ramp's KV does not fit next to the weights).  `--config cfg2` runs the
+single-layer configuration (prefill 2048 + 64 decodes at 4k, tau = 50/32 ms).  Synthetic seeded inputs
 (synth/), random weights of that architecture.
 
 metric: tokens/s per mixed iteration = (k T_dec + T_pre) / window, summed over ranks (each rank
@@ -152,9 +154,11 @@ def barrier(ws):
 # ----------------------------------------------------------------------------- oracle arm
 
 class OracleSample:
-    """The CPU oracle on a bounded sample of the workload: the first n_pre tokens of the prompt (exact,
-    by causality) and n_dec of the decode requests, one layer.  Inputs are prepared once (not timed);
-    run() times one oracle mixed iteration and returns (tokens, seconds)."""
+    """The CPU oracle on a bounded sample of the workload, one layer: two prefill chunks of n_pre/2 rows
+    each — the first rows of the prompt (c = 0) and its last rows (c = prompt - n_pre/2, the prefix given
+    as KV history) — so the sample's mean attention cost per row is the prompt's (causal cost is linear
+    in the position), plus n_dec decode requests spread evenly over the batch's context ramp.  Inputs
+    are prepared once (not timed); run() times one oracle mixed iteration, returns (tokens, seconds)."""
 
     def __init__(self, cfg_name: str, n_pre: int, n_dec: int):
         import numpy as np
@@ -164,16 +168,20 @@ class OracleSample:
         cfg = configs.get_config(cfg_name)
         # one layer of the configuration; deeper models are extrapolated per layer
         self.layers_total = cfg.model.n_layers
-        wl = workload.build(cfg, pre_seqs=[(n_pre, 0)], dec_ctx=list(cfg.batch.decode)[:n_dec], k=1, n_layers=1)
+        n_full = sum(q for q, _ in cfg.batch.prefill)
+        h = max(1, min(n_pre // 2, n_full // 2))
+        dec_all = list(cfg.batch.decode)
+        pick = [dec_all[int(i * (len(dec_all) - 1) / max(1, n_dec - 1))] for i in range(n_dec)] if n_dec else []
+        wl = workload.build(cfg, pre_seqs=[(h, 0), (h, n_full - h)], dec_ctx=pick, k=1, n_layers=1)
         wl.weights = [{k_: (None if v is None else np.asarray(v, dtype=np.float64)) for k_, v in w.items()}
                       for w in wl.weights]
         self.wl, self.kv, self.OL = wl, make_kv(wl), OL
         self.mdl = OL.Model.from_cfg(wl.cfg.model)
         # tokens per second of the whole model = tokens / (time of one layer x layers)
-        self.tokens = (n_pre + n_dec) / self.layers_total
-        n_full = sum(q for q, _ in cfg.batch.prefill)
-        self.desc = (f"oracle (numpy float64) on {cfg_name}: prompt rows 0..{n_pre - 1} of the {n_full}-token "
-                     f"chunk (exact by causality) + {n_dec} of the {len(cfg.batch.decode)} decodes, one layer"
+        self.tokens = (2 * h + n_dec) / self.layers_total
+        self.desc = (f"oracle (numpy float64) on {cfg_name}: prompt rows 0..{h - 1} and {n_full - h}..{n_full - 1} "
+                     f"of the {n_full}-token chunk (the tail with its prefix as KV history) + {n_dec} of the "
+                     f"{len(dec_all)} decodes spread over the context ramp, one layer"
                      + (f", extrapolated x{self.layers_total} layers" if self.layers_total > 1 else ""))
 
     def run(self):
@@ -185,8 +193,8 @@ class OracleSample:
 
 
 def oracle_baseline(cfg_name: str, budget_s: float = 12.0):
-    """cpu_baseline: repeat the (256 prompt rows + 8 decodes) sample for about budget_s seconds."""
-    smp = OracleSample(cfg_name, 256, 8)
+    """cpu_baseline: repeat the (2 x 64 prompt rows + 4 decodes) sample for about budget_s seconds."""
+    smp = OracleSample(cfg_name, 128, 4)
     tok = sec = 0.0
     n = 0
     while sec < budget_s or n < 2:
@@ -198,12 +206,17 @@ def oracle_baseline(cfg_name: str, budget_s: float = 12.0):
 
 
 def oracle_cores():
+    """Threads the oracle's BLAS actually uses (numpy matmuls are its only parallel part)."""
     try:
         from threadpoolctl import threadpool_info
         th = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
     except Exception:
         th = os.cpu_count()
     return int(th)
+
+
+def host_cores():
+    return {"nproc": os.cpu_count(), "blas_threads": oracle_cores()}
 
 
 def run_reference(args, ws, rank):
@@ -226,7 +239,7 @@ def run_reference(args, ws, rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "sample": desc},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": oracle_cores(), "kind": "oracle",
-                             "sample": desc},
+                             "sample": desc, "host": host_cores()},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -239,10 +252,12 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="duet", choices=["duet", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg3",
+                    help="cfg3 (the largest single-GPU config; cfg3-fit when the full ramp does not fit) or cfg2")
     ap.add_argument("--mode", default="auto", choices=["auto", "temporal", "spatial"])
     ap.add_argument("--tau", type=float, default=None, help="TBT SLO per iteration, seconds")
-    ap.add_argument("--sweep", action="store_true", help="also time every SM split")
+    ap.add_argument("--sweep", action="store_true",
+                    help="also time every SM split at its Alg. 1 k, measured vs predicted (Fig. 7/8 table)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="a few steps, no extras (for ncu)")
     ap.add_argument("--lm-head", action="store_true",
@@ -271,7 +286,7 @@ def main():
     tp = args.tp
     if tp > 1 and tp != ws:
         raise SystemExit(f"--tp {tp} needs WORLD_SIZE = {tp} (torchrun --nproc-per-node {tp})")
-    if tp > 1 and args.config == "cfg2":
+    if tp > 1 and args.config in ("cfg2", "cfg3", "cfg3-fit"):
         args.config = "cfg5"
     cfg = configs.get_config(args.config)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -323,6 +338,9 @@ def main():
     else:
         fl, bw = ctx.calibrate(total)
     t_cal = time.perf_counter() - t0
+    # the hardware read-stream ceiling per partition size (decode-side roofline denominator), before the
+    # KV pools take the memory
+    stream_bw = ctx.calibrate_stream(total) if not args.profile_only else None
     hw = D.HwProfile(total, parts, fl, bw, nvlink_bw=nvl_bw, allreduce_alpha=ar_alpha)
     log(f"calibrated in {t_cal:.1f}s; generating the KV history")
     Kp, Vp = kv_pools_gpu(wl, dev, tdt)   # after calibration: the pools take most of HBM at cfg3
@@ -344,22 +362,24 @@ def main():
             return D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1)
         return D.duet_choose_split(spec, hw, batch, tau, k_max, opts)
 
-    def prefill_arg(bufs=None):
+    def prefill_arg(bufs=None, chunk=None):
         xp, yp = (x_pre, y_pre) if bufs is None else (bufs[0], bufs[2])
+        if chunk is not None:   # the first `chunk` tokens of the (single) prompt: a smaller chunked-prefill step
+            return dict(q=[chunk], c=[0], table=wl.pre_tables[:1], x=xp[:chunk], y=yp[:chunk])
         return dict(q=[q for q, _ in wl.pre_seqs], c=[c for _, c in wl.pre_seqs], table=wl.pre_tables, x=xp, y=yp)
 
     def decode_arg(k, bufs=None):
         xd, yd = (x_dec, y_dec) if bufs is None else (bufs[1], bufs[3])
         return dict(c=wl.dec_ctx, table=wl.dec_tables, x=xd, y=yd[:k], head=head)
 
-    def one_step(split=None, bufs=None):
+    def one_step(split=None, bufs=None, chunk=None):
         """bufs: optional (x_pre, x_dec, y_pre, y_dec) device buffers (the e2e double buffering)."""
         s = decide() if split is None else split
         k = s.k if s.mode == D.DUET_MODE_SPATIAL else 1
         if k > 8:
             s = D.split_struct(s.mode, s.s_p, s.s_d, 8, s.flags, s.t_mixed, s.t_p, s.t_d, s.rho)
             k = 8
-        ctx.step(W, prefill_arg(bufs), decode_arg(k, bufs), Kp, Vp, wl.n_pages, s)
+        ctx.step(W, prefill_arg(bufs, chunk), decode_arg(k, bufs), Kp, Vp, wl.n_pages, s)
         return s, k
 
     # every step runs on a dedicated non-blocking stream: the legacy default stream would serialise
@@ -424,63 +444,168 @@ def main():
     ms_per_step = t_max_s * 1e3 / args.steps
     split = s
 
-    # ------------------------------------------------ per-side times & predictor error (one step)
-    one_step(split)
-    torch.cuda.synchronize()
-    side = ctx.last_step_times()
-    if split.mode == D.DUET_MODE_SPATIAL:
-        t_pred = max(split.k * split.t_d, split.t_p)
-    else:
-        t_pred = split.t_mixed
-    pred_err = abs(t_pred - side["t_window"]) / side["t_window"]
+    # ------------------------------------------------ per-side times & predictor error (synced steps)
+    def side_times(split, n=3, **kw):
+        """Median of n synced steps of each duet_last_step_times field (t_window, t_decode, t_prefill)."""
+        rows = []
+        for _ in range(n):
+            one_step(split, **kw)
+            torch.cuda.synchronize()
+            rows.append(ctx.last_step_times())
+        return {key: float(np.median([r[key] for r in rows])) for key in ("t_window", "t_decode", "t_prefill")}
+
+    def pred_errors(sp_, st_):
+        """|t_pred - t_meas| / t_meas per side and for the window (Alg. 1's t_d, t_p)."""
+        k_ = sp_.k if sp_.mode == D.DUET_MODE_SPATIAL else 1
+        if sp_.mode == D.DUET_MODE_SPATIAL:
+            w_pred = max(k_ * sp_.t_d, sp_.t_p)
+            td_meas = st_["t_decode"] / k_
+            return {"window": abs(w_pred - st_["t_window"]) / st_["t_window"],
+                    "decode": abs(sp_.t_d - td_meas) / td_meas if td_meas > 0 else None,
+                    "prefill": abs(sp_.t_p - st_["t_prefill"]) / st_["t_prefill"] if st_["t_prefill"] > 0 else None,
+                    "t_pred_window_ms": w_pred * 1e3, "t_pred_d_ms": sp_.t_d * 1e3, "t_pred_p_ms": sp_.t_p * 1e3}
+        return {"window": abs(sp_.t_mixed - st_["t_window"]) / st_["t_window"], "t_pred_window_ms": sp_.t_mixed * 1e3}
+
+    side = side_times(split)
+    pe = pred_errors(split, side)
+    t_pred = pe["t_pred_window_ms"] * 1e-3
+    pred_err = pe["window"]
+
+    # algorithmic work of one window per side (DESIGN.md §5; SURVEY §8(d) per-unit figures)
+    es_b = 2 if cfg.dtype == "bf16" else 4
+    d_, hq_, hkv_, dh_, f_ = m.d_model, m.n_q_heads, m.n_kv_heads, m.head_dim, m.ffn_dim
+    w_elems = nqkv * d_ + d_ * hq_ * dh_ + 2 * f_ * d_ + f_ * d_          # per layer
+
+    def prefill_flops(seqs):
+        g = 2.0 * sum(q for q, _ in seqs) * w_elems
+        a = sum(4.0 * hq_ * dh_ * (q * c + q * (q + 1) / 2) for q, c in seqs)
+        return m.n_layers * (g + a)
+
+    def decode_step_bytes(ctxs):
+        n = len(ctxs)
+        act = n * (d_ + nqkv + hq_ * dh_ + d_ + d_ + 2 * f_ + f_ + d_ + d_)   # GEMM inputs + outputs
+        kv = sum(2 * hkv_ * dh_ * (c + 1) for c in ctxs)
+        return m.n_layers * (w_elems + act + kv) * es_b
+
+    F_pre = prefill_flops(wl.pre_seqs)
+    B_dec = decode_step_bytes(wl.dec_ctx)
+    pk, pk_src = peaks()
+
+    def partition_roofline(sp_, st_):
+        """Per-partition roofline (BASELINE north_star; SURVEY §8(d) 'which roofline bounds each side')."""
+        if sp_.mode != D.DUET_MODE_SPATIAL:
+            return None
+        k_ = sp_.k
+        ach_t = F_pre / st_["t_prefill"] / 1e12
+        peak_p = float(pk["bf16_tflops_sustained"]) * sp_.s_p / total
+        ach_b = k_ * B_dec / st_["t_decode"] / 1e9
+        out = {"prefill": {"s_p": sp_.s_p, "achieved_tflops": ach_t, "peak_tflops": peak_p, "frac": ach_t / peak_p,
+                           "peak_note": "sustained bf16 peak x S_p/148 (MEASURED_PEAKS.json)"},
+               "decode": {"s_d": sp_.s_d, "achieved_gbs": ach_b, "frac_of_hbm_peak": ach_b / float(pk["hbm_gbs"]),
+                          "hbm_peak_gbs": float(pk["hbm_gbs"])}}
+        if stream_bw is not None and stream_bw[sp_.s_d] > 0:
+            out["decode"]["stream_ceiling_gbs"] = stream_bw[sp_.s_d] / 1e9
+            out["decode"]["frac_of_stream_ceiling"] = ach_b * 1e9 / stream_bw[sp_.s_d]
+            # per-operator roofline at S_d with the stream ceiling as B(S): sum_op max(F/Pi(S_d), B/B_stream(S_d))
+            hw_s = D.HwProfile(total, parts, fl, [b if b > 0 else bw[i] for i, b in enumerate(stream_bw)],
+                               nvlink_bw=nvl_bw, allreduce_alpha=ar_alpha)
+            t_op = D.duet_predict_latency(spec, hw_s, [e for e in batch if e[2] == 2], sp_.s_d,
+                                          opts & D.DUET_OPT_INCLUDE_CLS)["t_total"]
+            out["decode"]["per_operator_roofline_ms"] = t_op * 1e3
+            out["decode"]["frac_of_per_operator_roofline"] = t_op / (st_["t_decode"] / k_)
+        return out
 
     log(f"timed: {ms_per_step:.3f} ms/step; comparisons")
     # ------------------------------------------------ aggregated vs partitioned (same kernels, same batch)
-    comp = {}
-    if not args.profile_only:
-        def timed(split_fn, n=max(5, args.steps // 2)):
-            for _ in range(2):
-                one_step(split_fn())
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            tok = 0
-            wins, tds = [], []
-            a.record(stream)
-            for _ in range(n):
-                s_, k_ = one_step(split_fn())
-                tok += k_ * n_d + n_p
-            b.record(stream)
-            torch.cuda.synchronize()
-            for _ in range(3):
-                one_step(split_fn())
-                torch.cuda.synchronize()
-                st = ctx.last_step_times()
-                wins.append(st["t_window"])
-                tds.append(st["t_decode"] / max(1, st["k"]))
-            return tok / (a.elapsed_time(b) * 1e-3), float(np.median(wins)), float(np.median(tds))
+    def tbt_stats(ts, k_):
+        """Inter-token gaps (ms) from the device token-time ring: every gap, and the window-boundary ones."""
+        g = np.diff(np.asarray(ts, dtype=np.float64)) * 1e-6
+        if g.size == 0:
+            return {}
+        bnd = g[[j for j in range(g.size) if (j + 1) % k_ == 0]]
+        return {"tbt_max_ms": float(g.max()), "tbt_median_ms": float(np.median(g)), "tbt_p90_ms": float(np.percentile(g, 90)),
+                "boundary_gap_max_ms": float(bnd.max()) if bnd.size else None,
+                "boundary_gap_median_ms": float(np.median(bnd)) if bnd.size else None, "gaps": int(g.size)}
 
-        agg = timed(lambda: D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1))
+    def timed(split_fn, n=max(5, min(args.steps, 20)), chunk=None):
+        """tokens/s over n back-to-back windows (CUDA events), TBT from the token-time ring of the same
+        windows, per-side times of synced steps."""
+        for _ in range(2):
+            one_step(split_fn(), chunk=chunk)
+        torch.cuda.synchronize()
+        ctx.token_times_reset()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tok = 0
+        n_p_ = chunk if chunk is not None else n_p
+        a.record(stream)
+        for _ in range(n):
+            s_, k_ = one_step(split_fn(), chunk=chunk)
+            tok += k_ * n_d + n_p_
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts = ctx.token_times(reset=True)
+        sp_ = split_fn()
+        st_ = side_times(sp_, chunk=chunk)
+        k_ = sp_.k if sp_.mode == D.DUET_MODE_SPATIAL else 1
+        r = {"tok_s": tok / (a.elapsed_time(b) * 1e-3), "window_ms": st_["t_window"] * 1e3,
+             "t_decode_ms": st_["t_decode"] * 1e3, "t_prefill_ms": st_["t_prefill"] * 1e3, "k": k_}
+        r.update(tbt_stats(ts, k_))
+        return r, st_
+
+    comp, part_roof = {}, None
+    if not args.profile_only:
+        temporal = lambda: D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1)
+        agg, _ = timed(temporal)
+        agg["t_pred_ms"] = split.t_mixed * 1e3
+        # aggregated at the SLO: conventional chunked prefill (P:59, P:184) with the chunk cut to the largest
+        # multiple of 256 tokens for which the predicted mixed iteration meets tau — what a temporal-only
+        # server must do to hold the TBT SLO
+        q_slo = 0
+        for q_ in range(n_p // 256 * 256, 0, -256):
+            b_ = [(q_, 0, 0, 0)] + [e for e in batch if e[2] == 2]
+            if D.duet_predict_latency(spec, hw, b_, total, opts & D.DUET_OPT_INCLUDE_CLS)["t_total"] <= tau:
+                q_slo = q_
+                break
+        agg_slo = None
+        if 0 < q_slo < n_p:
+            agg_slo, _ = timed(temporal, chunk=q_slo)
+            agg_slo["prefill_chunk"] = q_slo
         forced = D.duet_choose_split(spec, hw, batch, tau, k_max, D.DUET_OPT_FORCE_SPATIAL | (opts & D.DUET_OPT_INCLUDE_CLS))
         if forced.k > 8:
             forced = D.split_struct(1, forced.s_p, forced.s_d, 8, forced.flags, forced.t_mixed, forced.t_p,
                                     forced.t_d, forced.rho)
-        spa = timed(lambda: forced)
-        comp = {
-            "aggregated": {"tok_s": agg[0], "tbt_ms": agg[2] * 1e3, "window_ms": agg[1] * 1e3,
-                           "t_pred_ms": forced.t_mixed * 1e3},
-            "partitioned_optimizer": {"s_d": forced.s_d, "s_p": forced.s_p, "k": forced.k, "tok_s": spa[0],
-                                      "tbt_ms": spa[2] * 1e3, "window_ms": spa[1] * 1e3,
-                                      "t_pred_window_ms": max(forced.k * forced.t_d, forced.t_p) * 1e3,
-                                      "t_pred_d_ms": forced.t_d * 1e3, "t_pred_p_ms": forced.t_p * 1e3},
-            "tau_ms": tau * 1e3,
-        }
+        spa, spa_side = timed(lambda: forced)
+        spa.update({"s_d": forced.s_d, "s_p": forced.s_p, "k": forced.k, "flags": forced.flags})
+        spa["predictor_error"] = pred_errors(forced, spa_side)
+        part_roof = partition_roofline(forced, spa_side)
+        comp = {"aggregated": agg, "aggregated_chunked_at_slo": agg_slo, "partitioned_optimizer": spa,
+                "tau_ms": tau * 1e3,
+                "north_star": {"partitioned_tbt_max_ms": spa.get("tbt_max_ms"),
+                               "partitioned_meets_slo": (spa.get("tbt_max_ms") or 1e9) <= tau * 1e3,
+                               "partitioned_over_aggregated": spa["tok_s"] / agg["tok_s"],
+                               "partitioned_over_aggregated_at_slo":
+                                   spa["tok_s"] / agg_slo["tok_s"] if agg_slo else None}}
         if args.sweep:
             rows = []
+            P_b = [e for e in batch if e[2] != 2]
+            D_b = [e for e in batch if e[2] == 2]
             for sd in parts:
-                sp_ = D.split_struct(1, total - sd, sd, 1)
-                r = timed(lambda: sp_, n=3)
-                rows.append({"s_d": sd, "tok_s": r[0], "window_ms": r[1] * 1e3, "tbt_ms": r[2] * 1e3})
-            comp["sweep_k1"] = rows
+                td = D.duet_predict_latency(spec, hw, D_b, sd, opts & D.DUET_OPT_INCLUDE_CLS)["t_total"]
+                tp = D.duet_predict_latency(spec, hw, P_b, total - sd, opts & D.DUET_OPT_INCLUDE_CLS)["t_total"]
+                r_ = int(np.floor(tp / td))
+                ks = [min(max(x, 1), 8) for x in (r_, r_ + 1)]
+                rhos = [(kk * len(D_b) + sum(e[0] for e in P_b)) / max(kk * td, tp) for kk in ks]
+                kk = ks[int(np.argmax(rhos))]
+                sp_ = D.split_struct(1, total - sd, sd, kk, 0, split.t_mixed, tp, td, max(rhos))
+                r, st_ = timed(lambda: sp_, n=4)
+                r.update({"s_d": sd, "s_p": total - sd, "t_pred_d_ms": td * 1e3, "t_pred_p_ms": tp * 1e3,
+                          "t_pred_window_ms": max(kk * td, tp) * 1e3, "predicted_tok_s": max(rhos),
+                          "optimizer_pick": sd == forced.s_d, "meets_slo_pred": td <= tau,
+                          "meets_slo_meas": (r.get("tbt_max_ms") or 1e9) <= tau * 1e3})
+                rows.append(r)
+                log(f"sweep S_d={sd}: k={kk} {r['tok_s']:.0f} tok/s window {r['window_ms']:.2f} ms "
+                    f"(pred {max(kk * td, tp) * 1e3:.2f}) TBT max {r.get('tbt_max_ms', 0):.2f} ms")
+            comp["sweep"] = rows
 
     log("e2e")
     # ------------------------------------------------ e2e through the C ABI with host buffers
@@ -605,10 +730,15 @@ def main():
     if st_["launches"] and st_["seconds"] > 0:
         if tensor_bound:
             ach = st_["flops"] / st_["seconds"] / 1e12
-            peak = float(pk["bf16_tflops"])
+            # the burst figure for a short timed region, the sustained one for a region of seconds
+            # (the GPU settles at its power cap, B200_PROFILING.md)
+            sustained = t_ms > 1000.0
+            peak = float(pk["bf16_tflops_sustained" if sustained else "bf16_tflops"])
             roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                     "traffic": traffic, "kernel": dom, "launches": st_["launches"],
-                    "avg_launch_us": st_["seconds"] / st_["launches"] * 1e6, "peak_source": pk_src + " burst bf16"}
+                    "avg_launch_us": st_["seconds"] / st_["launches"] * 1e6,
+                    "peak_source": pk_src + (" sustained bf16 (timed region %.1f s)" % (t_ms / 1e3) if sustained
+                                             else " burst bf16")}
         else:
             ach = st_["bytes"] / st_["seconds"] / 1e9
             peak = float(pk["hbm_gbs"])
@@ -624,7 +754,21 @@ def main():
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile_only:
         v_c, desc_c = oracle_baseline(args.config)
-        cpu = {"value": v_c, "unit": "tokens/s", "cores": oracle_cores(), "kind": "oracle", "sample": desc_c}
+        cpu = {"value": v_c, "unit": "tokens/s", "cores": oracle_cores(), "kind": "oracle", "sample": desc_c,
+               "host": host_cores()}
+        # Alg. 1 on the host ("< 1 ms"): the library's C++ and the oracle's Python on this batch
+        import oracle.roofline as R
+        t0_ = time.perf_counter()
+        for _ in range(20):
+            D.duet_choose_split(spec, hw, batch, tau, k_max, opts)
+        cpu["optimizer_ms"] = (time.perf_counter() - t0_) / 20 * 1e3
+        prof_o = R.Profile(total, tuple(parts), tuple(fl), tuple(bw), nvl_bw, ar_alpha)
+        spec_o = R.Spec(m.n_layers, m.d_model, m.ffn_dim, m.n_q_heads, m.n_kv_heads, m.head_dim, m.vocab,
+                        2 if cfg.dtype == "bf16" else 4, True, tp)
+        reqs_o = [R.Req(e[0], e[1], e[2], e[3]) for e in batch]
+        t0_ = time.perf_counter()
+        R.choose_split(spec_o, prof_o, reqs_o, tau, k_max, opts)
+        cpu["oracle_optimizer_ms"] = (time.perf_counter() - t0_) * 1e3
 
     if rank == 0:
         line = {
@@ -641,8 +785,11 @@ def main():
                        "parallelism": f"tp{tp} (head-sharded, NCCL allreduce after O and down)" if tp > 1
                        else f"dp{ws} (independent replicas)", "calibration_s": round(t_cal, 2)},
             "predictor": {"t_pred_ms": t_pred * 1e3, "t_meas_ms": side["t_window"] * 1e3, "err": pred_err,
-                          "t_meas_decode_ms": side["t_decode"] * 1e3, "t_meas_prefill_ms": side["t_prefill"] * 1e3},
+                          "t_meas_decode_ms": side["t_decode"] * 1e3, "t_meas_prefill_ms": side["t_prefill"] * 1e3,
+                          "per_side": pe,
+                          "partitioned_optimizer_split": comp.get("partitioned_optimizer", {}).get("predictor_error")},
             "comparison": comp,
+            "partition_roofline": part_roof,
             "roofline": roof,
             "kernel_seconds_per_step": share,
             "kernel_timing": f"CUDA events on the launching stream: the {dom} launches inside the timed region "

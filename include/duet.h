@@ -88,7 +88,7 @@ typedef struct {
   double t_linear, t_norm_act, t_attn, t_allreduce, t_block, t_cls, t_total;
 } duet_latency;
 
-enum { DUET_OPT_FORCE_SPATIAL = 1u, DUET_OPT_INCLUDE_CLS = 2u };
+enum { DUET_OPT_FORCE_SPATIAL = 1u, DUET_OPT_INCLUDE_CLS = 2u, DUET_OPT_VERBATIM_INFEASIBLE = 4u };
 
 /* f_roofline(batch, Pi_SM(sms), B_HBM(sms)) — the attention-aware roofline model of §4.1
  * (P:194-250): token-level operators max(F/Pi, B/B) with F_lin = 2 n d_i d_o,
@@ -121,11 +121,33 @@ typedef struct {
  * > tau; t_p(S - S_d); k in {floor(t_p/t_d), floor(t_p/t_d)+1} clamped to [1, k_max]
  * (reading #17); rho = (k T_dec + T_pre) / max(k t_d, t_p); strict ">" keeps the
  * first maximum (reading #18).  Fallbacks are flagged, never silent: DEGENERATE
- * (one phase absent -> temporal), INFEASIBLE (no S_d meets tau -> argmin t_d).
+ * (one phase absent -> temporal), INFEASIBLE (no S_d meets tau -> argmin t_d; reading #20b: that
+ * spatial split is kept only if its rho >= the temporal rho sum(q)/t_mixed, else the batch runs
+ * temporally with the INFEASIBLE flag — VERBATIM_INFEASIBLE or FORCE_SPATIAL keep it spatial).
  * Errors: as duet_predict_latency, plus CONFIG for tbt_slo_s <= 0 or k_max < 1. */
 duet_status duet_choose_split(const duet_model_spec* spec, const duet_hw_profile* hw,
                               const duet_req* batch, int32_t n, double tbt_slo_s, int32_t k_max,
                               uint32_t opts, duet_split* out);
+
+/* f4 attention co-run choice of a temporal step (POD-Attention's overlap): the
+ * prefill attention (F causal FLOPs) and the decode attention (B bytes) of one layer run either one
+ * after the other on the full device, t_seq = F / fa(S) + B / bw(S), or side by side on the partition
+ * (S - S_d, S_d), t = max(F / fa(S - S_d), B / bw(S_d)).  *s_d_out = the first candidate (ascending,
+ * both sides >= min_sms) with the smallest t if that t < t_seq - overhead_s, else 0 (no co-run);
+ * *t_out (nullable) = that t or t_seq.  fa_flops_at_sms / dec_bw_at_sms: [total_sms + 1] rates of the
+ * library's prefill- and decode-attention kernels per partition size (duet_calibrate measures them
+ * for the ctx; entries <= 0 are skipped).  Pure host function.
+ * Errors: INVALID_ARG, CONFIG (full-device rate <= 0). */
+typedef struct {
+  int32_t total_sms, n_cand;
+  const int32_t* cand_sd_sms;
+  const double* fa_flops_at_sms;
+  const double* dec_bw_at_sms;
+  int32_t min_sms;
+  double overhead_s;
+} duet_corun_profile;
+duet_status duet_corun_choose(const duet_corun_profile* p, double attn_flops_pre, double attn_bytes_dec,
+                              int32_t* s_d_out, double* t_out);
 
 /* ----------------------------------------------------------------- execution context */
 
@@ -169,8 +191,9 @@ duet_status duet_ctx_destroy(duet_ctx* ctx);
  *  duet_sched_add: a request (id, prompt and output length in tokens, arrival time, non-decreasing).
  *    CAPACITY if prompt + output + k_max tokens can never fit.
  *  duet_sched_next: forms the next iteration at time now_s: admits arrived requests FIFO while the
- *    free pages cover their whole prompt + output + k_max; every running decode (up to max_batch)
- *    joins, then prefill chunks fill the remaining budget, the oldest prompt first.  The arrays of
+ *    free pages cover their whole prompt + output + k_max and the admitted, unfinished requests number
+ *    fewer than max_batch; every running decode joins (so none is ever skipped), then prefill chunks
+ *    fill the remaining budget, the oldest prompt first.  The arrays of
  *    *out (ids, q, c, page_table [n_prefill + n_decode][max_pages], prefill entries first) are owned by
  *    the sched and valid until the next call; an empty iteration (n_prefill = n_decode = 0) needs
  *    no commit — next_arrival_s says when the next request arrives (-1: none).
@@ -214,8 +237,13 @@ duet_status duet_sched_free_pages(const duet_sched* sched, int32_t* out);
  * duet_nccl_unique_id: an ncclUniqueId (128 bytes) into out (len >= 128); rank 0 creates two (one
  *   per side) and broadcasts them (e.g. with torch.distributed).
  * duet_ctx_set_comms: collective over the N ranks (each calls it with its rank and the same two
- *   ids): creates the ctx's decode-side and prefill-side communicators (ncclCommInitRank).  With
- *   spec->tp = 1 it creates single-rank communicators (the allreduce path, as a no-op copy).
+ *   ids): creates the ctx's decode-side and prefill-side communicators (ncclCommInitRankConfig with
+ *   maxCTAs / nvlsCTAs capped — 4 on the decode side, 16 on the prefill side; env DUET_NCCL_MAXCTAS_DEC,
+ *   DUET_NCCL_MAXCTAS_PRE, DUET_NCCL_NVLSCTAS — so a side's collectives stay a small share of its
+ *   partition).  With spec->tp = 1 it creates single-rank communicators (the allreduce
+ *   path, as a no-op copy).
+ * duet_ctx_check_comms: polls ncclCommGetAsyncError on both communicators (NCCL if either reports an
+ *   error; OK without communicators); duet_step does the same before it enqueues work on a TP ctx.
  * duet_calibrate_allreduce: alpha (s) and B_NVLink (B/s) of the P:237 ring model from timed
  *   allreduces of 16 B and 64 MiB on the prefill communicator (0, 0 when tp = 1).
  * libnccl.so.2 is resolved at run time (the one PyTorch loads).  Errors: INVALID_ARG,
@@ -223,6 +251,7 @@ duet_status duet_sched_free_pages(const duet_sched* sched, int32_t* out);
 duet_status duet_nccl_unique_id(void* out, int32_t len);
 duet_status duet_ctx_set_comms(duet_ctx* ctx, int32_t rank, const void* id_decode, const void* id_prefill);
 duet_status duet_calibrate_allreduce(duet_ctx* ctx, double* alpha_s, double* bw_bytes_s);
+duet_status duet_ctx_check_comms(duet_ctx* ctx);
 
 /* The achievable decode-partition sizes, ascending (host array of capacity *n on input;
  * *n is set to the count).  total_sms: SMs of the device. */
@@ -327,6 +356,13 @@ duet_status duet_last_step_times(duet_ctx* ctx, duet_step_times* out);
  * Errors: INVALID_ARG, CUDA. */
 duet_status duet_calibrate(duet_ctx* ctx, double* flops_at_sms, double* bw_at_sms, int32_t len);
 
+/* The hardware read-stream ceiling per partition size — the roofline denominator of a decode
+ * partition, SURVEY §8(d) (not a predictor input): plain 16-byte LDG streaming of a >= 256 MiB buffer
+ * from 2048 threads per SM on S SMs (median of 5), for S = every achievable partition side and the
+ * full device; other entries 0.  bw_stream: host array of len >= total_sms + 1 doubles (B/s).
+ * Errors: INVALID_ARG, CAPACITY, CUDA. */
+duet_status duet_calibrate_stream(duet_ctx* ctx, double* bw_stream, int32_t len);
+
 /* Live kernel timing (measurement, §8(d)): while enabled, duet_step records CUDA events on the
  * launching stream around every kernel it launches outside CUDA graphs (the prefill side of a
  * spatial step and every kernel of a temporal step), per kernel class, together with the
@@ -357,6 +393,42 @@ duet_status duet_op_gemm(duet_ctx* ctx, const void* A, const void* B, void* C, c
 /* h[n][d] = x * (mean(x^2) + eps)^(-1/2) * g   (reading #1). */
 duet_status duet_op_rmsnorm(duet_ctx* ctx, const void* x, const void* g, void* h, int32_t n,
                             void* stream);
+
+/* Paged decode attention alone (a5.4: split-K over pages + log-sum-exp combine, exactly the launch
+ * duet_step makes), for parity checks at full size and partition microbenchmarks.
+ *  q: device [n] rows of row stride q_stride elements (>= h_q d_h), head j at column j d_h, already
+ *  rotated; o: device [n][h_q d_h].  Row r attends to positions 0..pos[r] of page-table row r
+ *  (readings #2, #6, #7); their K/V must already be in the pools (no append).
+ *  pos: host int32 [n]; page_table: host int32 [n][max_pages], covering pos + 1 tokens, pages distinct.
+ *  k_pool / v_pool: device [n_pages][h_kv][16][d_h] of one layer.  s_d: 0 = full device on `stream`,
+ *  else the decode group of the partition with s_d SMs (duet_ctx_partitions), ordered after and
+ *  joined back into `stream`.  n <= max_decode_reqs, pos < max_pos.
+ * Errors: INVALID_ARG, OUT_OF_RANGE (pages, positions, s_d), CAPACITY, UNSUPPORTED, CUDA. */
+duet_status duet_op_decode_attn(duet_ctx* ctx, const void* q, int32_t q_stride, void* o, int32_t n,
+                                const int32_t* pos, const int32_t* page_table, int32_t max_pages,
+                                const void* k_pool, const void* v_pool, int32_t n_pages, int32_t s_d,
+                                void* stream);
+
+/* Causal prefill attention alone (a6.4, the launch of duet_step): n_seqs sequences, sequence s has
+ * q_len[s] query rows (rows grouped by sequence in order) at positions c[s] .. c[s] + q_len[s] - 1 and
+ * attends to every position <= its own (the prefix fully, reading #7); K/V of all those positions
+ * must already be in the pools.  q: device [sum q_len] rows of stride q_stride; o: device
+ * [sum q_len][h_q d_h].  q_len, c: host int32 [n_seqs]; page_table: host [n_seqs][max_pages].
+ *  s_p: 0 = full device, else the prefill side (remainder) of the partition with that many SMs.
+ * Errors: as duet_op_decode_attn. */
+duet_status duet_op_prefill_attn(duet_ctx* ctx, const void* q, int32_t q_stride, void* o, int32_t n_seqs,
+                                 const int32_t* q_len, const int32_t* c, const int32_t* page_table,
+                                 int32_t max_pages, const void* k_pool, const void* v_pool, int32_t n_pages,
+                                 int32_t s_p, void* stream);
+
+/* Token times (TBT per decode step, the window-boundary gap): every decode step of a
+ * spatial window, and the decode rows of a temporal step, write %globaltimer (ns, one device-wide
+ * clock) into a 4096-slot device ring when that step's tokens are complete, in stream order.
+ * duet_token_times synchronizes the device, returns the number of stamps written since the last reset
+ * in *n and copies the first min(*n, cap) of them to out_ns (both nullable), then clears the ring
+ * when reset != 0.  Consecutive stamps of one decode batch are its inter-token gaps, including the
+ * gap across a window boundary.  Errors: INVALID_ARG, CAPACITY (> 4096 stamps since the reset), CUDA. */
+duet_status duet_token_times(duet_ctx* ctx, int32_t reset, uint64_t* out_ns, int32_t cap, int32_t* n);
 
 #ifdef __cplusplus
 }

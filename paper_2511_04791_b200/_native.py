@@ -11,14 +11,14 @@ LIB_PATH = os.path.join(_HERE, "libduet.so")
 
 DUET_OK = 0
 DUET_PHASE_PREFILL_FULL, DUET_PHASE_PREFILL_CHUNK, DUET_PHASE_DECODE = 0, 1, 2
-DUET_OPT_FORCE_SPATIAL, DUET_OPT_INCLUDE_CLS = 1, 2
+DUET_OPT_FORCE_SPATIAL, DUET_OPT_INCLUDE_CLS, DUET_OPT_VERBATIM_INFEASIBLE = 1, 2, 4
 DUET_MODE_TEMPORAL, DUET_MODE_SPATIAL = 0, 1
 DUET_FLAG_INFEASIBLE, DUET_FLAG_DEGENERATE = 1, 2
 DUET_DTYPE_BF16, DUET_DTYPE_FP32 = 0, 1
 DUET_CTX_FINE_SPLIT, DUET_CTX_NO_GRAPH, DUET_CTX_NO_CORUN = 1, 2, 4
 DUET_EPI_STORE, DUET_EPI_RESIDUAL, DUET_EPI_SWIGLU = 0, 1, 2
 STATUS_NAMES = {0: "OK", -1: "INVALID_ARG", -2: "OUT_OF_RANGE", -3: "CONFIG", -4: "UNSUPPORTED", -5: "CUDA",
-                -6: "CAPACITY"}
+                -6: "CAPACITY", -7: "NCCL"}
 
 
 class DuetError(RuntimeError):
@@ -85,6 +85,12 @@ DUET_KCLASS_N = 4
 DUET_PROFILE_ALL = 0xF
 
 
+class duet_corun_profile(C.Structure):
+    _fields_ = [("total_sms", C.c_int32), ("n_cand", C.c_int32), ("cand_sd_sms", C.POINTER(C.c_int32)),
+                ("fa_flops_at_sms", C.POINTER(C.c_double)), ("dec_bw_at_sms", C.POINTER(C.c_double)),
+                ("min_sms", C.c_int32), ("overhead_s", C.c_double)]
+
+
 class duet_kernel_stats(C.Structure):
     _fields_ = [("launches", C.c_int32), ("seconds", C.c_double), ("flops", C.c_double), ("bytes", C.c_double)]
 
@@ -127,6 +133,18 @@ _SIGS = {
     "duet_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_int32]),
     "duet_ctx_set_comms": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "duet_calibrate_allreduce": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "duet_ctx_check_comms": (C.c_int, [C.c_void_p]),
+    "duet_op_decode_attn": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32, C.c_void_p, C.c_void_p,
+                                      C.c_int32, C.c_int32, C.c_void_p]),
+    "duet_op_prefill_attn": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32,
+                                       C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "duet_corun_choose": (C.c_int, [C.POINTER(duet_corun_profile), C.c_double, C.c_double, C.POINTER(C.c_int32),
+                                    C.POINTER(C.c_double)]),
+    "duet_calibrate_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int32]),
+    "duet_token_times": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.c_int32,
+                                   C.POINTER(C.c_int32)]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -197,6 +215,18 @@ def duet_choose_split(spec: duet_model_spec, hw: HwProfile, batch, tbt_slo_s: fl
     _check(lib().duet_choose_split(C.byref(spec), C.byref(hw.struct), _reqs(batch), len(batch), float(tbt_slo_s),
                                    int(k_max), int(opts), C.byref(out)))
     return out
+
+
+def duet_corun_choose(total_sms, cand_sd_sms, fa_flops_at_sms, dec_bw_at_sms, attn_flops_pre, attn_bytes_dec,
+                      min_sms=16, overhead_s=15e-6):
+    """(s_d, t): the f4 attention co-run split of a temporal step (0 = one after the other)."""
+    cand = (C.c_int32 * max(1, len(cand_sd_sms)))(*cand_sd_sms)
+    fa = (C.c_double * (total_sms + 1))(*fa_flops_at_sms)
+    bw = (C.c_double * (total_sms + 1))(*dec_bw_at_sms)
+    p = duet_corun_profile(total_sms, len(cand_sd_sms), cand, fa, bw, min_sms, overhead_s)
+    sd, t = C.c_int32(), C.c_double()
+    _check(lib().duet_corun_choose(C.byref(p), float(attn_flops_pre), float(attn_bytes_dec), C.byref(sd), C.byref(t)))
+    return sd.value, t.value
 
 
 def split_tuple(s: duet_split):
@@ -376,6 +406,10 @@ class Ctx:
         b = C.create_string_buffer(bytes(id_prefill), 128)
         _check(lib().duet_ctx_set_comms(self.h, int(rank), a, b))
 
+    def check_comms(self):
+        """Raises DuetError(NCCL) when a communicator reports an asynchronous error (duet_ctx_check_comms)."""
+        _check(lib().duet_ctx_check_comms(self.h))
+
     def calibrate_allreduce(self):
         """(alpha seconds, B_NVLink bytes/s) of the P:237 allreduce model (duet_calibrate_allreduce)."""
         a, b = C.c_double(), C.c_double()
@@ -387,6 +421,12 @@ class Ctx:
         bw = (C.c_double * (total_sms + 1))()
         _check(lib().duet_calibrate(self.h, fl, bw, total_sms + 1))
         return list(fl), list(bw)
+
+    def calibrate_stream(self, total_sms: int):
+        """LDG stream ceiling (B/s) per achievable partition size (duet_calibrate_stream); 0 elsewhere."""
+        bw = (C.c_double * (total_sms + 1))()
+        _check(lib().duet_calibrate_stream(self.h, bw, total_sms + 1))
+        return list(bw)
 
     def op_gemm(self, A, B, Cout, R=None, bias=None, epi=DUET_EPI_STORE, stream=None):
         M, K = A.shape
@@ -400,6 +440,37 @@ class Ctx:
         if stream is None:
             stream = torch.cuda.current_stream().cuda_stream
         _check(lib().duet_op_rmsnorm(self.h, _ptr(x), _ptr(g), _ptr(h), x.shape[0], C.c_void_p(stream)))
+
+
+    def op_decode_attn(self, q, o, pos, table, k_pool, v_pool, n_pages, s_d=0, stream=None):
+        """q: [n][>= h_q d_h] device rows (stride q.stride(0)); pos: host [n]; table: host [n][max_pages]."""
+        p, pp = _i32(pos)
+        t, tp = _i32(table)
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        _check(lib().duet_op_decode_attn(self.h, _ptr(q), q.stride(0), _ptr(o), len(p), pp, tp, t.shape[1],
+                                         _ptr(k_pool), _ptr(v_pool), int(n_pages), int(s_d), C.c_void_p(stream)))
+
+    def op_prefill_attn(self, q, o, q_len, c, table, k_pool, v_pool, n_pages, s_p=0, stream=None):
+        """q: [sum q_len][>= h_q d_h] device rows; q_len, c: host [n_seqs]; table: host [n_seqs][max_pages]."""
+        ql, qlp = _i32(q_len)
+        cc, cp = _i32(c)
+        t, tp = _i32(table)
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        _check(lib().duet_op_prefill_attn(self.h, _ptr(q), q.stride(0), _ptr(o), len(ql), qlp, cp, tp, t.shape[1],
+                                          _ptr(k_pool), _ptr(v_pool), int(n_pages), int(s_p), C.c_void_p(stream)))
+
+    def token_times_reset(self):
+        _check(lib().duet_token_times(self.h, 1, None, 0, None))
+
+    def token_times(self, reset=True):
+        """%globaltimer stamps (ns) of the decode steps since the last reset (duet_token_times)."""
+        n = C.c_int32(0)
+        _check(lib().duet_token_times(self.h, 0, None, 0, C.byref(n)))
+        arr = (C.c_uint64 * max(1, n.value))()
+        _check(lib().duet_token_times(self.h, int(bool(reset)), arr, n.value, C.byref(n)))
+        return list(arr[:n.value])
 
 
 def split_struct(mode, s_p, s_d, k, flags=0, t_mixed=0.0, t_p=0.0, t_d=0.0, rho=0.0) -> duet_split:

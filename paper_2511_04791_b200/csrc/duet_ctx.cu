@@ -92,6 +92,8 @@ struct NcclApi {
   bool ok = false;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, ncclConfig_t*) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -110,6 +112,8 @@ duet_status load_nccl() {
   };
   DUET_TRY(get("ncclGetUniqueId", (void**)&NCCL.GetUniqueId));
   DUET_TRY(get("ncclCommInitRank", (void**)&NCCL.CommInitRank));
+  DUET_TRY(get("ncclCommInitRankConfig", (void**)&NCCL.CommInitRankConfig));
+  DUET_TRY(get("ncclCommGetAsyncError", (void**)&NCCL.CommGetAsyncError));
   DUET_TRY(get("ncclAllReduce", (void**)&NCCL.AllReduce));
   DUET_TRY(get("ncclCommDestroy", (void**)&NCCL.CommDestroy));
   DUET_TRY(get("ncclGetErrorString", (void**)&NCCL.GetErrorString));
@@ -160,7 +164,11 @@ struct Side {
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   int kernels = 0;
+  uint64_t last_use = 0;
 };
+// decode graphs kept per ctx (key: partition, batch size, layers, pointer hash, context bucket); the
+// least recently used one is destroyed beyond this many (a serving loop changes the batch size often)
+constexpr size_t kGraphCap = 48;
 
 }  // namespace
 
@@ -196,6 +204,7 @@ struct duet_ctx {
   std::vector<uint32_t> page_mark;
   uint32_t page_gen = 0;
   std::map<std::tuple<int, int, int, uint64_t>, GraphEntry> graphs;
+  uint64_t graph_clock = 0;
   // last step
   int last_mode = -1, last_k = 0, last_kernels = 0, last_corun = 0;
   bool last_has_dec = false, last_has_pre = false;
@@ -210,7 +219,14 @@ struct duet_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_pool;
   size_t prof_used = 0;
   duet_kernel_stats prof_acc[DUET_KCLASS_N] = {};
+  // f4 co-run rates per partition size (duet_corun_choose): prefill-attention FLOP/s, decode-attention B/s
+  std::vector<double> cal_fa, cal_bw;
+  // token-time ring (SURVEY §8(d) TBT per decode step): %globaltimer when each step's tokens are done
+  unsigned long long* tok_ts = nullptr;
+  int* tok_cnt = nullptr;
 };
+
+static duet_status comms_healthy(duet_ctx* c);
 
 static int prof_begin(duet_ctx* c, cudaStream_t st, int cls) {
   if (!c->prof_on || c->capturing || !(c->prof_mask & (1 << cls))) return -1;
@@ -324,28 +340,85 @@ struct AttnPlan {
   double attn_flops_pre = 0, attn_bytes_pre = 0, attn_flops_dec = 0, attn_bytes_dec = 0;
 };
 
-// f4 co-run partition choice for a temporal step with both phases: minimise the attention window
-// max(t_pre(S_p), t_dec(S_d)) against running the two one after the other on the full device.
-// Rates measured on B200 with these kernels (tools/gpu/run_corun.sh): prefill attention
-// ~4.0 TFLOP/s per SM (linear in SMs), decode attention B(S) = 5.9 TB/s (1 - e^(-S/28)), 6.1 TB/s on
-// the full device; ~15 us of fork / join / lost launch overlap per layer must be won back.
+// f4 co-run partition choice for a temporal step with both phases: duet_corun_choose on
+// the ctx's per-size attention rates — measured by duet_calibrate (prefill attention FLOP/s, decode
+// attention B/s on every partition side), until then the prior fitted on B200 in round 1
+// (tools/gpu/run_corun.sh): ~4.0 TFLOP/s per SM, B(S) = 5.9 TB/s (1 - e^(-S/28)), 6.1 TB/s full device.
 static Partition* corun_pick(duet_ctx* c, const AttnPlan& ap) {
-  constexpr double kFaPerSm = 4.0e12, kDecSat = 5.9e12, kDecS0 = 28.0, kDecFull = 6.1e12, kOverhead = 15e-6;
-  const double seq = ap.attn_flops_pre / (kFaPerSm * c->total_sms) + ap.attn_bytes_dec / kDecFull;
-  Partition* best = nullptr;
-  double best_t = seq - kOverhead;
-  for (auto& p : c->parts) {
-    const int s_p = c->total_sms - p.s_d;  // the remainder of a split (exact once created)
-    if (p.s_d < 16 || s_p < 16) continue;
-    const double t_pre = ap.attn_flops_pre / (kFaPerSm * s_p);
-    const double t_dec = ap.attn_bytes_dec / (kDecSat * (1.0 - std::exp(-p.s_d / kDecS0)));
-    const double t = std::max(t_pre, t_dec);
-    if (t < best_t) {
-      best_t = t;
-      best = &p;
-    }
-  }
-  return best;
+  constexpr double kOverhead = 15e-6;  // fork / join / lost launch overlap per layer
+  std::vector<int32_t> cand;
+  for (auto& p : c->parts) cand.push_back(p.s_d);
+  duet_corun_profile prof{c->total_sms, (int32_t)cand.size(), cand.data(), c->cal_fa.data(), c->cal_bw.data(), 16,
+                          kOverhead};
+  int32_t sd = 0;
+  if (duet_corun_choose(&prof, ap.attn_flops_pre, ap.attn_bytes_dec, &sd, nullptr) != DUET_OK || sd == 0)
+    return nullptr;
+  for (auto& p : c->parts)
+    if (p.s_d == sd) return &p;
+  return nullptr;
+}
+
+// Causal prefill attention (a6.4) of the prefill rows of plan ap (metadata in side S) — the launch of
+// duet_step and of duet_op_prefill_attn.  Returns the kernels launched (<= 0: could not launch).
+static int prefill_attn(duet_ctx* c, Side& S, const AttnPlan& ap, const void* q, int q_stride, void* o,
+                        int total_rows, const void* k_pool, const void* v_pool, int n_pages, int num_sms,
+                        cudaStream_t st) {
+  const auto& sp = c->spec;
+  PrefillAttnArgs pa{};
+  pa.q = q;
+  pa.q_stride = q_stride;
+  pa.o = o;
+  pa.n_seqs = ap.n_seqs;
+  pa.hq = sp.n_q_heads;
+  pa.hkv = sp.n_kv_heads;
+  pa.dh = sp.head_dim;
+  pa.row0 = S.row0();
+  pa.qlen = S.qlen();
+  pa.cpre = S.cpre();
+  pa.seq_row = S.seqrow();
+  pa.table = S.table();
+  pa.max_pages = S.pitch;
+  pa.page_size = kPageSize;
+  pa.k_pool = k_pool;
+  pa.v_pool = v_pool;
+  pa.max_q = ap.max_q;
+  pa.total_q = ap.n_pre;
+  pa.num_sms = num_sms;
+  pa.tok_pos = S.pos();
+  pa.tok_row = S.tok();
+  pa.max_len = ap.max_len_pre;
+  pa.n_pages = n_pages;
+  pa.total_rows = total_rows;
+  return launch_prefill_attn(c->dt, pa, st);
+}
+
+// Paged decode attention (a5.4, split-K + LSE combine) of the decode rows of plan ap, which follow the
+// ap.n_pre prefill rows in side S's metadata; q / o point at the first decode row.
+static int decode_attn(duet_ctx* c, Side& S, const AttnPlan& ap, const void* q, int q_stride, void* o,
+                       const void* k_pool, const void* v_pool, int n_pages, int num_sms, cudaStream_t st) {
+  const auto& sp = c->spec;
+  DecodeAttnArgs da{};
+  da.q = q;
+  da.q_stride = q_stride;
+  da.o = o;
+  da.n = ap.n_dec;
+  da.hq = sp.n_q_heads;
+  da.hkv = sp.n_kv_heads;
+  da.dh = sp.head_dim;
+  da.pos = S.pos() + ap.n_pre;
+  da.tok_row = S.tok() + ap.n_pre;
+  da.table = S.table();
+  da.max_pages = S.pitch;
+  da.page_size = kPageSize;
+  da.k_pool = k_pool;
+  da.v_pool = v_pool;
+  da.part_o = S.part_o;
+  da.part_ml = S.part_ml;
+  da.max_splits = kMaxSplits;
+  da.num_sms = num_sms;
+  da.max_len = ((ap.max_len_dec + 1023) / 1024) * 1024;  // same bucket in both modes
+  da.n_pages = n_pages;
+  return launch_decode_attn(c->dt, da, st);
 }
 
 // x_in2 / y_final2 / row_split: rows >= row_split of the layer input / final output live in a second
@@ -370,11 +443,11 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
   ncclComm_t comm = (&S == &c->dec) ? c->comm_dec : c->comm_pre;
   const bool lead = comm == nullptr || c->tp_rank == 0;
   const ncclDataType_t nccl_dt = dt == DT::BF16 ? ncclBfloat16 : ncclFloat32;
-  // sum of the ranks' partial [n_rows][d] rows in place (2 allreduces per layer)
-  auto allreduce = [&](void* buf) -> int {
-    if (!comm) return 0;
-    const ncclResult_t r = NCCL.AllReduce(buf, buf, (size_t)n_rows * d, nccl_dt, ncclSum, comm, st);
-    return r == ncclSuccess ? 1 : -1000000;  // a negative count is reported by the check below
+  // sum of the ranks' partial [rows][d] rows in place (2 allreduces per layer)
+  auto allreduce = [&](void* buf, int rows) -> int {
+    if (!comm || rows <= 0) return 1;
+    const ncclResult_t r = NCCL.AllReduce(buf, buf, (size_t)rows * d, nccl_dt, ncclSum, comm, st);
+    return r == ncclSuccess ? 1 : -1;
   };
   auto with_ws = [&](GemmArgs& g) {
     g.ws = S.gemm_ws;
@@ -382,10 +455,15 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
   };
   // DUET_DEBUG_SYNC=1: synchronize after every launch and report it (hang / fault triage only)
   static const bool dbg_sync = getenv("DUET_DEBUG_SYNC") != nullptr;
+  // every launch is checked where it is made: a launcher returns the number of kernels it queued
+  // (> 0 here, n_rows > 0) or a negative value when it could not launch (e.g. a TMA map that cannot be
+  // encoded), which fails the step naming the call
 #define TIMED(cls, fl, by, call)                                                                  \
   do {                                                                                            \
     const int pi_ = prof_begin(c, st, cls);                                                       \
-    nk += (call);                                                                                 \
+    const int r_ = (call);                                                                        \
+    if (r_ <= 0) DUET_FAIL(DUET_ERR_CUDA, "layer %d: %s could not be launched (%d)", l, #call, r_); \
+    nk += r_;                                                                                     \
     prof_end(c, st, pi_, cls, fl, by);                                                            \
     if (dbg_sync && !c->capturing) {                                                              \
       fprintf(stderr, "[duet] layer %d: %s ...", l, #call);                                       \
@@ -432,34 +510,10 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       sms_da = cp->s_d;
     }
     if (ap.n_pre > 0) {
-      PrefillAttnArgs pa{};
-      pa.q = S.qkv;
-      pa.q_stride = nqkv;
-      pa.o = S.o;
-      pa.n_seqs = ap.n_seqs;
-      pa.hq = hq;
-      pa.hkv = hkv;
-      pa.dh = dh;
-      pa.row0 = S.row0();
-      pa.qlen = S.qlen();
-      pa.cpre = S.cpre();
-      pa.seq_row = S.seqrow();
-      pa.table = S.table();
-      pa.max_pages = S.pitch;
-      pa.page_size = kPageSize;
-      pa.k_pool = kv->k_pool[l];
-      pa.v_pool = kv->v_pool[l];
-      pa.max_q = ap.max_q;
-      pa.total_q = ap.n_pre;
-      pa.num_sms = sms_pa;
-      pa.tok_pos = S.pos();
-      pa.tok_row = S.tok();
-      pa.max_len = ap.max_len_pre;
-      pa.n_pages = kv->n_pages;
-      pa.total_rows = n_rows;
       const int pi = prof_begin(c, st_pa, DUET_KCLASS_PREFILL_ATTN);
-      const int r = launch_prefill_attn(dt, pa, st_pa);
-      if (r < 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "prefill attention: unsupported head layout");
+      const int r = prefill_attn(c, S, ap, S.qkv, nqkv, S.o, n_rows, kv->k_pool[l], kv->v_pool[l], kv->n_pages,
+                                 sms_pa, st_pa);
+      if (r <= 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "layer %d: prefill attention could not be launched", l);
       prof_end(c, st_pa, pi, DUET_KCLASS_PREFILL_ATTN, ap.attn_flops_pre, ap.attn_bytes_pre);
       if (dbg_sync && !c->capturing) {
         fprintf(stderr, "[duet] layer %d: prefill attention ...", l);
@@ -468,30 +522,11 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       nk += r;
     }
     if (ap.n_dec > 0) {
-      DecodeAttnArgs da{};
-      da.q = (const char*)S.qkv + (size_t)ap.n_pre * nqkv * es;
-      da.q_stride = nqkv;
-      da.o = (char*)S.o + (size_t)ap.n_pre * hq * dh * es;
-      da.n = ap.n_dec;
-      da.hq = hq;
-      da.hkv = hkv;
-      da.dh = dh;
-      da.pos = S.pos() + ap.n_pre;
-      da.tok_row = S.tok() + ap.n_pre;
-      da.table = S.table();
-      da.max_pages = S.pitch;
-      da.page_size = kPageSize;
-      da.k_pool = kv->k_pool[l];
-      da.v_pool = kv->v_pool[l];
-      da.part_o = S.part_o;
-      da.part_ml = S.part_ml;
-      da.max_splits = kMaxSplits;
-      da.num_sms = sms_da;
-      da.max_len = ((ap.max_len_dec + 1023) / 1024) * 1024;  // same bucket in both modes
-      da.n_pages = kv->n_pages;
       const int pi = prof_begin(c, st_da, DUET_KCLASS_DECODE_ATTN);
-      const int r = launch_decode_attn(dt, da, st_da);
-      if (r < 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "decode attention: unsupported head layout");
+      const int r = decode_attn(c, S, ap, (const char*)S.qkv + (size_t)ap.n_pre * nqkv * es, nqkv,
+                                (char*)S.o + (size_t)ap.n_pre * hq * dh * es, kv->k_pool[l], kv->v_pool[l],
+                                kv->n_pages, sms_da, st_da);
+      if (r <= 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "layer %d: decode attention could not be launched", l);
       prof_end(c, st_da, pi, DUET_KCLASS_DECODE_ATTN, ap.attn_flops_dec, ap.attn_bytes_dec);
       nk += r;
     }
@@ -513,7 +548,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       go.C2 = (char*)S.x1 + (size_t)row_split * d * es;  // output stays in one buffer
     }
     TIMED(DUET_KCLASS_GEMM, gemm_fl(d, hq * dh), gemm_by(d, hq * dh, d, true), launch_gemm(dt, go, num_sms, st));
-    if (comm) TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, allreduce(S.x1));
+    if (comm) TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, allreduce(S.x1, n_rows));
     // 6. h2 = RMSNorm(x1) g2
     TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e, launch_rmsnorm(dt, S.x1, W.g_norm2, S.h2, n_rows, d, eps, st));
     // 7. act = silu(h2 W_g^T) * (h2 W_u^T)
@@ -530,10 +565,15 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       gd.row_split = row_split;
     }
     TIMED(DUET_KCLASS_GEMM, gemm_fl(d, m), gemm_by(d, m, d, true), launch_gemm(dt, gd, num_sms, st));
-    if (comm) TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, allreduce(Y));
+    if (comm) {
+      // rows >= row_split of the last layer's output went to y_final2 (the temporal batch's decode
+      // rows in the caller's decode buffer): each buffer is reduced over its own rows
+      const bool split_out = l == sp.n_layers - 1 && row_split < n_rows;
+      TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, allreduce(Y, split_out ? row_split : n_rows));
+      if (split_out) TIMED(DUET_KCLASS_OTHER, 0.0, 0.0, allreduce(y_final2, n_rows - row_split));
+    }
   }
 #undef TIMED
-  if (nk < 0) DUET_FAIL(DUET_ERR_NCCL, "ncclAllReduce failed inside the layer stack");
   DUET_TRY(check_launch("layer stack"));
   *kernels += nk;
   return DUET_OK;
@@ -670,6 +710,16 @@ extern "C" duet_status duet_ctx_create(int32_t device, const duet_model_spec* sp
         const double phi = (double)p * inv;
         tab[(size_t)p * half + i] = make_float2((float)std::cos(phi), (float)std::sin(phi));
       }
+    // co-run rates: the round-1 prior until duet_calibrate measures them
+    c->cal_fa.assign(c->total_sms + 1, 0.0);
+    c->cal_bw.assign(c->total_sms + 1, 0.0);
+    for (int s = 1; s <= c->total_sms; ++s) {
+      c->cal_fa[s] = 4.0e12 * s;
+      c->cal_bw[s] = s == c->total_sms ? 6.1e12 : 5.9e12 * (1.0 - std::exp(-s / 28.0));
+    }
+    CUDA_TRY(cudaMalloc(&c->tok_ts, kTokTsSlots * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMalloc(&c->tok_cnt, sizeof(int)));
+    CUDA_TRY(cudaMemset(c->tok_cnt, 0, sizeof(int)));
     CUDA_TRY(cudaMalloc(&c->rope, tab.size() * sizeof(float2)));
     CUDA_TRY(cudaMemcpy(c->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
     return DUET_OK;
@@ -722,6 +772,8 @@ extern "C" duet_status duet_ctx_destroy(duet_ctx* c) {
   side_free(c->dec);
   side_free(c->pre);
   if (c->rope) cudaFree(c->rope);
+  if (c->tok_ts) cudaFree(c->tok_ts);
+  if (c->tok_cnt) cudaFree(c->tok_cnt);
   if (c->stage) cudaFreeHost(c->stage);
   if (c->stage_d) cudaFree(c->stage_d);
   if (c->s_up) cudaStreamDestroy(c->s_up);
@@ -777,6 +829,15 @@ static duet_status check_pages(duet_ctx* c, const int32_t* table, int32_t max_pa
   return DUET_OK;
 }
 
+// a new generation of page marks: every page may be claimed once until the next call
+static void begin_page_check(duet_ctx* c, int n_pages) {
+  if ((int)c->page_mark.size() < n_pages) c->page_mark.assign(n_pages, 0);
+  if (++c->page_gen == 0) {
+    std::fill(c->page_mark.begin(), c->page_mark.end(), 0);
+    c->page_gen = 1;
+  }
+}
+
 static duet_status validate_step(duet_ctx* c, const duet_layer_weights* w, const duet_prefill* pre,
                                  const duet_decode* dec, const duet_kv_pages* kv, int k) {
   if (!w) DUET_FAIL(DUET_ERR_INVALID_ARG, "weights are NULL");
@@ -791,11 +852,7 @@ static duet_status validate_step(duet_ctx* c, const duet_layer_weights* w, const
   for (int l = 0; l < c->spec.n_layers; ++l)
     if (!kv->k_pool[l] || !kv->v_pool[l]) DUET_FAIL(DUET_ERR_INVALID_ARG, "layer %d: kv pool NULL", l);
   if (kv->n_pages <= 0) DUET_FAIL(DUET_ERR_INVALID_ARG, "n_pages = %d", kv->n_pages);
-  if ((int)c->page_mark.size() < kv->n_pages) c->page_mark.assign(kv->n_pages, 0);
-  if (++c->page_gen == 0) {
-    std::fill(c->page_mark.begin(), c->page_mark.end(), 0);
-    c->page_gen = 1;
-  }
+  begin_page_check(c, kv->n_pages);
   if (pre && pre->n_seqs > 0) {
     if (pre->n_seqs > c->lim.max_prefill_seqs)
       DUET_FAIL(DUET_ERR_CAPACITY, "n_seqs = %d > max_prefill_seqs %d", pre->n_seqs, c->lim.max_prefill_seqs);
@@ -930,20 +987,24 @@ static duet_status lm_head(duet_ctx* c, Side& S, cudaStream_t st, int num_sms, i
                            const duet_lm_head* head, void* x_next, const int* step, int* kernels) {
   const int d = c->spec.d_model, V = c->spec.vocab;
   const size_t e = dt_size(c->dt);
-  int nk = 0;
+  int nk = 0, r = 0;
   int pi = prof_begin(c, st, DUET_KCLASS_OTHER);
-  nk += launch_rmsnorm(c->dt, y, head->g_norm, S.h, n, d, (float)c->spec.norm_eps, st);
+  if ((r = launch_rmsnorm(c->dt, y, head->g_norm, S.h, n, d, (float)c->spec.norm_eps, st)) <= 0)
+    DUET_FAIL(DUET_ERR_CUDA, "LM head: final RMSNorm could not be launched");
+  nk += r;
   prof_end(c, st, pi, DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e);
   GemmArgs g{S.h, head->w_head, S.logits, nullptr, nullptr, n, V, d, d, d, V, 0, EPI_STORE};
   g.ws = S.gemm_ws;
   g.ws_floats = S.gemm_ws_floats;
   pi = prof_begin(c, st, DUET_KCLASS_GEMM);
-  nk += launch_gemm(c->dt, g, num_sms, st);
+  if ((r = launch_gemm(c->dt, g, num_sms, st)) <= 0) DUET_FAIL(DUET_ERR_CUDA, "LM head: GEMM could not be launched");
+  nk += r;
   prof_end(c, st, pi, DUET_KCLASS_GEMM, 2.0 * n * (double)V * d, ((double)n * d + (double)V * d + (double)n * V) * e);
   pi = prof_begin(c, st, DUET_KCLASS_OTHER);
-  nk += launch_argmax_embed(S.logits, V, head->embed, x_next, d, head->tokens, step, n, st);
+  if ((r = launch_argmax_embed(S.logits, V, head->embed, x_next, d, head->tokens, step, n, st)) <= 0)
+    DUET_FAIL(DUET_ERR_CUDA, "LM head: argmax / embedding could not be launched");
+  nk += r;
   prof_end(c, st, pi, DUET_KCLASS_OTHER, 0.0, ((double)n * V + (x_next ? 2.0 * n * d : 0.0)) * e);
-  if (nk < 0) DUET_FAIL(DUET_ERR_CUDA, "LM head launch failed");
   DUET_TRY(check_launch("lm head"));
   *kernels += nk;
   return DUET_OK;
@@ -961,7 +1022,7 @@ static duet_status decode_step_kernels(duet_ctx* c, cudaStream_t st, int num_sms
   // with an LM head the next input is the greedy token's embedding (f1), else the output (reading #26)
   if (head) DUET_TRY(lm_head(c, S, st, num_sms, n, S.ylast, head, S.xin, S.step(), kernels));
   *kernels += launch_decode_advance(c->dt, S.ylast, head ? nullptr : S.xin, y_out, n, c->spec.d_model, S.pos(),
-                                    S.step(), st);
+                                    S.step(), st, c->tok_ts, c->tok_cnt);
   DUET_TRY(check_launch("decode advance"));
   return DUET_OK;
 }
@@ -979,6 +1040,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
   const int k = spatial ? split->k : 1;
   if (k < 1) DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "k = %d must be >= 1", k);
   DUET_TRY(validate_step(c, w, pre, dec, kv, k));
+  if (c->comm_dec || c->comm_pre) DUET_TRY(comms_healthy(c));
   cudaStream_t ust = (cudaStream_t)stream;
   const bool has_pre = pre && pre->n_seqs > 0;
   const bool has_dec = dec && dec->n_reqs > 0;
@@ -1012,6 +1074,12 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     probe.K = d;
     probe.lda = probe.ldb = probe.ldc = probe.ldr = d;
     probe.epi = EPI_RESIDUAL;
+    if (has_pre && has_dec) {  // the caller's buffers must meet the kernel's alignment
+      probe.R = pre->x;
+      probe.C = pre->y;
+      probe.R2 = dec->x;
+      probe.C2 = dec->y;
+    }
     const bool split_io = has_pre && has_dec && c->dt == DT::BF16 && gemm2_supported(probe, c->total_sms) &&
                           c->spec.ffn_dim % 64 == 0 && (c->spec.n_q_heads * c->spec.head_dim) % 64 == 0;
     // f4 co-run: the two attentions of each layer side by side, decode on an S_d group and prefill
@@ -1057,6 +1125,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     // the decode rows' greedy tokens (f1; k = 1 in temporal mode): from their outputs in dec->y
     if (has_dec && dec->head) DUET_TRY(lm_head(c, c->pre, st, c->total_sms, ap.n_dec, dec->y, dec->head, nullptr,
                                                nullptr, &kernels));
+    if (has_dec) kernels += launch_stamp(c->tok_ts, c->tok_cnt, st);  // the decode rows' token time
     CUDA_TRY(cudaEventRecord(c->ev_pre1, st));
     CUDA_TRY(cudaStreamWaitEvent(ust, c->ev_pre1, 0));
     c->last_kernels = kernels;
@@ -1110,8 +1179,17 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
         e = cudaGraphInstantiate(&ge.exec, graph, 0);
         cudaGraphDestroy(graph);
         if (e != cudaSuccess) DUET_FAIL(DUET_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+        if (c->graphs.size() >= kGraphCap) {  // evict the least recently used graph
+          auto lru = c->graphs.begin();
+          for (auto g = c->graphs.begin(); g != c->graphs.end(); ++g)
+            if (g->second.last_use < lru->second.last_use) lru = g;
+          CUDA_TRY(cudaStreamSynchronize(P->s_dec));  // its last replay may still be queued
+          cudaGraphExecDestroy(lru->second.exec);
+          c->graphs.erase(lru);
+        }
         it = c->graphs.emplace(key, ge).first;
       }
+      it->second.last_use = ++c->graph_clock;
       for (int j = 0; j < k; ++j) CUDA_TRY(cudaGraphLaunch(it->second.exec, st));
       kernels += k * it->second.kernels;
     }
@@ -1195,11 +1273,44 @@ extern "C" duet_status duet_ctx_set_comms(duet_ctx* c, int32_t rank, const void*
   ncclUniqueId a, b;
   memcpy(&a, id_decode, sizeof(a));
   memcpy(&b, id_prefill, sizeof(b));
-  NCCL_TRY(NCCL.CommInitRank(&c->comm_dec, c->spec.tp, a, rank));
-  NCCL_TRY(NCCL.CommInitRank(&c->comm_pre, c->spec.tp, b, rank));
+  // each side's collectives run inside its own green context next to that side's compute;
+  // cap the CTAs NCCL may occupy so an allreduce never fills a small decode partition (env overrides:
+  // DUET_NCCL_MAXCTAS_DEC / _PRE, DUET_NCCL_NVLSCTAS)
+  auto env_int = [](const char* n, int dflt) { const char* v = getenv(n); return v ? atoi(v) : dflt; };
+  ncclConfig_t cfg_dec = NCCL_CONFIG_INITIALIZER, cfg_pre = NCCL_CONFIG_INITIALIZER;
+  cfg_dec.maxCTAs = env_int("DUET_NCCL_MAXCTAS_DEC", 4);
+  cfg_pre.maxCTAs = env_int("DUET_NCCL_MAXCTAS_PRE", 16);
+  cfg_dec.nvlsCTAs = std::min(cfg_dec.maxCTAs, env_int("DUET_NCCL_NVLSCTAS", 4));
+  cfg_pre.nvlsCTAs = std::min(cfg_pre.maxCTAs, env_int("DUET_NCCL_NVLSCTAS", 16));
+  cfg_dec.commName = "duet-decode";
+  cfg_pre.commName = "duet-prefill";
+  NCCL_TRY(NCCL.CommInitRankConfig(&c->comm_dec, c->spec.tp, a, rank, &cfg_dec));
+  NCCL_TRY(NCCL.CommInitRankConfig(&c->comm_pre, c->spec.tp, b, rank, &cfg_pre));
   c->tp_rank = rank;
   c->graphs.clear();  // captured decode graphs predate the communicators
   return DUET_OK;
+}
+
+// Asynchronous NCCL errors (SURVEY §5 failure detection): a peer failure or a network error surfaces
+// here, not as a CUDA error; duet_step polls it before enqueuing work on a TP ctx.
+static duet_status comms_healthy(duet_ctx* c) {
+  ncclComm_t cs[2] = {c->comm_dec, c->comm_pre};
+  const char* names[2] = {"decode", "prefill"};
+  for (int i = 0; i < 2; ++i) {
+    if (!cs[i]) continue;
+    ncclResult_t ae = ncclSuccess;
+    NCCL_TRY(NCCL.CommGetAsyncError(cs[i], &ae));
+    if (ae != ncclSuccess && ae != ncclInProgress)
+      DUET_FAIL(DUET_ERR_NCCL, "%s-side communicator reports an asynchronous error: %s", names[i],
+                NCCL.GetErrorString(ae));
+  }
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_ctx_check_comms(duet_ctx* c) {
+  clear_error();
+  if (!c) DUET_FAIL(DUET_ERR_INVALID_ARG, "ctx is NULL");
+  return comms_healthy(c);
 }
 
 extern "C" duet_status duet_calibrate_allreduce(duet_ctx* c, double* alpha_s, double* bw_bytes_s) {
@@ -1257,7 +1368,8 @@ extern "C" duet_status duet_op_gemm(duet_ctx* c, const void* A, const void* B, v
   GemmArgs g{A, B, C, R, bias, M, N, K, K, K, N, N, epi};
   g.ws = c->pre.gemm_ws;  // op calls are stream-ordered by the caller, never concurrent with a step
   g.ws_floats = c->pre.gemm_ws_floats;
-  launch_gemm(c->dt, g, c->total_sms, (cudaStream_t)stream);
+  if (M > 0 && launch_gemm(c->dt, g, c->total_sms, (cudaStream_t)stream) <= 0)
+    DUET_FAIL(DUET_ERR_UNSUPPORTED, "gemm M=%d N=%d K=%d could not be launched (operand alignment?)", M, N, K);
   DUET_TRY(check_launch("gemm"));
   return DUET_OK;
 }
@@ -1267,6 +1379,140 @@ extern "C" duet_status duet_op_rmsnorm(duet_ctx* c, const void* x, const void* g
   if (!c || !x || !g || !h) DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL operand");
   launch_rmsnorm(c->dt, x, g, h, n, c->spec.d_model, (float)c->spec.norm_eps, (cudaStream_t)stream);
   DUET_TRY(check_launch("rmsnorm"));
+  return DUET_OK;
+}
+
+// Stream of an op: the caller's (s_sms == 0, full device) or one side of a green-context partition,
+// ordered after the caller's stream; *join is the partition stream to join back (nullptr: none).
+static duet_status op_stream(duet_ctx* c, int s_sms, bool decode_side, cudaStream_t ust, cudaStream_t* st, int* sms,
+                             cudaStream_t* join) {
+  *join = nullptr;
+  if (s_sms == 0) {
+    *st = ust;
+    *sms = c->total_sms;
+    return DUET_OK;
+  }
+  Partition* P = nullptr;
+  for (auto& p : c->parts)
+    if ((decode_side ? p.s_d : c->total_sms - p.s_d) == s_sms) P = &p;
+  if (!P) DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "%d SMs is not an achievable %s partition", s_sms,
+                    decode_side ? "decode" : "prefill");
+  DUET_TRY(ensure_partition(c, *P));
+  *st = decode_side ? P->s_dec : P->s_pre;
+  *sms = decode_side ? P->s_d : P->s_p;
+  CUDA_TRY(cudaEventRecord(c->ev_in, ust));
+  CUDA_TRY(cudaStreamWaitEvent(*st, c->ev_in, 0));
+  *join = *st;
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_op_decode_attn(duet_ctx* c, const void* q, int32_t q_stride, void* o, int32_t n,
+                                           const int32_t* pos, const int32_t* page_table, int32_t max_pages,
+                                           const void* k_pool, const void* v_pool, int32_t n_pages, int32_t s_d,
+                                           void* stream) {
+  clear_error();
+  if (!c || !q || !o || !pos || !page_table || !k_pool || !v_pool) DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL operand");
+  if (n < 1 || n > c->lim.max_decode_reqs) DUET_FAIL(DUET_ERR_CAPACITY, "n = %d outside [1, max_decode_reqs]", n);
+  if (q_stride < c->spec.n_q_heads * c->spec.head_dim || n_pages <= 0 || max_pages < 1)
+    DUET_FAIL(DUET_ERR_INVALID_ARG, "q_stride = %d, n_pages = %d, max_pages = %d", q_stride, n_pages, max_pages);
+  begin_page_check(c, n_pages);
+  for (int r = 0; r < n; ++r) {
+    if (pos[r] < 0 || pos[r] + 1 > c->lim.max_pos)
+      DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "row %d: pos = %d outside [0, max_pos)", r, pos[r]);
+    DUET_TRY(check_pages(c, page_table, max_pages, r, pos[r] + 1, n_pages, "decode"));
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st, join;
+  int sms;
+  DUET_TRY(op_stream(c, s_d, true, (cudaStream_t)stream, &st, &sms, &join));
+  duet_decode dd{};
+  dd.n_reqs = n;
+  dd.c = pos;  // the row's own position: attends to 0..pos[r]
+  dd.page_table = page_table;
+  dd.max_pages = max_pages;
+  int* img;
+  int slot, nk = 0;
+  DUET_TRY(stage_slot(c, &img, &slot));
+  AttnPlan ap;
+  const size_t n_int = build_meta(c, c->dec, img, nullptr, &dd, &ap);
+  DUET_TRY(upload_meta(c, c->dec, img, slot, n_int, sms, st, &nk));
+  if (decode_attn(c, c->dec, ap, q, q_stride, o, k_pool, v_pool, n_pages, sms, st) <= 0)
+    DUET_FAIL(DUET_ERR_UNSUPPORTED, "decode attention could not be launched");
+  DUET_TRY(check_launch("decode attention"));
+  if (join) {
+    CUDA_TRY(cudaEventRecord(c->ev_dec1, join));
+    CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_dec1, 0));
+  }
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_op_prefill_attn(duet_ctx* c, const void* q, int32_t q_stride, void* o, int32_t n_seqs,
+                                            const int32_t* q_len, const int32_t* cpre, const int32_t* page_table,
+                                            int32_t max_pages, const void* k_pool, const void* v_pool,
+                                            int32_t n_pages, int32_t s_p, void* stream) {
+  clear_error();
+  if (!c || !q || !o || !q_len || !cpre || !page_table || !k_pool || !v_pool)
+    DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL operand");
+  if (n_seqs < 1 || n_seqs > c->lim.max_prefill_seqs)
+    DUET_FAIL(DUET_ERR_CAPACITY, "n_seqs = %d outside [1, max_prefill_seqs]", n_seqs);
+  if (q_stride < c->spec.n_q_heads * c->spec.head_dim || n_pages <= 0 || max_pages < 1)
+    DUET_FAIL(DUET_ERR_INVALID_ARG, "q_stride = %d, n_pages = %d, max_pages = %d", q_stride, n_pages, max_pages);
+  begin_page_check(c, n_pages);
+  long tot = 0;
+  for (int s = 0; s < n_seqs; ++s) {
+    if (q_len[s] < 1 || cpre[s] < 0 || (long)cpre[s] + q_len[s] > c->lim.max_pos)
+      DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "seq %d: q = %d, c = %d", s, q_len[s], cpre[s]);
+    tot += q_len[s];
+    DUET_TRY(check_pages(c, page_table, max_pages, s, cpre[s] + q_len[s], n_pages, "prefill"));
+  }
+  if (tot > c->lim.max_prefill_tokens + c->lim.max_decode_reqs)
+    DUET_FAIL(DUET_ERR_CAPACITY, "%ld query rows exceed the ctx capacity", tot);
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st, join;
+  int sms;
+  DUET_TRY(op_stream(c, s_p, false, (cudaStream_t)stream, &st, &sms, &join));
+  duet_prefill pp{};
+  pp.n_seqs = n_seqs;
+  pp.q = q_len;
+  pp.c = cpre;
+  pp.page_table = page_table;
+  pp.max_pages = max_pages;
+  int* img;
+  int slot, nk = 0;
+  DUET_TRY(stage_slot(c, &img, &slot));
+  AttnPlan ap;
+  const size_t n_int = build_meta(c, c->pre, img, &pp, nullptr, &ap);
+  DUET_TRY(upload_meta(c, c->pre, img, slot, n_int, sms, st, &nk));
+  if (prefill_attn(c, c->pre, ap, q, q_stride, o, ap.n_pre, k_pool, v_pool, n_pages, sms, st) <= 0)
+    DUET_FAIL(DUET_ERR_UNSUPPORTED, "prefill attention could not be launched");
+  DUET_TRY(check_launch("prefill attention"));
+  if (join) {
+    CUDA_TRY(cudaEventRecord(c->ev_pre1, join));
+    CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_pre1, 0));
+  }
+  return DUET_OK;
+}
+
+// ---------------------------------------------------------------------------------- token times
+
+extern "C" duet_status duet_token_times(duet_ctx* c, int32_t reset, uint64_t* out_ns, int32_t cap, int32_t* n) {
+  clear_error();
+  if (!c) DUET_FAIL(DUET_ERR_INVALID_ARG, "ctx is NULL");
+  CUDA_TRY(cudaSetDevice(c->device));
+  int cnt = 0;
+  if (n || out_ns) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(&cnt, c->tok_cnt, sizeof(int), cudaMemcpyDeviceToHost));
+    if (out_ns && cap > 0 && cnt > kTokTsSlots)
+      DUET_FAIL(DUET_ERR_CAPACITY, "%d stamps since the last reset overran the %d-slot ring", cnt, kTokTsSlots);
+    const int m = out_ns ? std::min(cnt, std::max(cap, 0)) : 0;
+    if (m > 0) CUDA_TRY(cudaMemcpy(out_ns, c->tok_ts, m * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (n) *n = cnt;
+  }
+  if (reset) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemset(c->tok_cnt, 0, sizeof(int)));
+  }
   return DUET_OK;
 }
 
@@ -1350,7 +1596,32 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
     da.n_pages = n_req * pages_per_req;
     attn_bytes = 2.0 * (double)n_req * pages_per_req * page_bytes;
   }
-  std::vector<double> mf(c->total_sms + 1, 0.0), mb(c->total_sms + 1, 0.0);
+  // f4 co-run rates: the prefill-attention kernel on a causal chunk of QF rows over pages of the same
+  // pool (bf16, d_h = 128 contexts whose tensor-core flash kernel runs)
+  const int QF = std::min(2048, std::min(c->lim.max_pages_per_seq * kPageSize, c->lim.max_prefill_tokens)) / 128 * 128;
+  void *dqf = nullptr, *dof = nullptr;
+  AttnPlan apf;
+  double fa_flops = 0;
+  bool use_fa = use_attn && sp.head_dim == 128 && QF >= 128 && QF / kPageSize <= da.n_pages &&
+                c->lim.max_prefill_seqs >= 1;
+  if (use_fa) {
+    const size_t qbytes = (size_t)QF * sp.n_q_heads * sp.head_dim * es;
+    CUDA_TRY(cudaMalloc(&dqf, qbytes));
+    CUDA_TRY(cudaMalloc(&dof, qbytes));
+    launch_fill_hash(c->dt, dqf, qbytes / es, 7u, c->s_full);
+    std::vector<int32_t> tab(QF / kPageSize);
+    for (int j = 0; j < (int)tab.size(); ++j) tab[j] = j;
+    const int32_t q1 = QF, c0 = 0;
+    duet_prefill pp{1, &q1, &c0, tab.data(), (int32_t)tab.size(), nullptr, nullptr};
+    int* img;
+    int slot, nk = 0;
+    DUET_TRY(stage_slot(c, &img, &slot));
+    const size_t n_int = build_meta(c, c->pre, img, &pp, nullptr, &apf);
+    DUET_TRY(upload_meta(c, c->pre, img, slot, n_int, c->total_sms, c->s_full, &nk));
+    CUDA_TRY(cudaStreamSynchronize(c->s_full));
+    fa_flops = apf.attn_flops_pre;
+  }
+  std::vector<double> mf(c->total_sms + 1, 0.0), mb(c->total_sms + 1, 0.0), mfa(c->total_sms + 1, 0.0);
   auto measure = [&](cudaStream_t st, int sms) -> duet_status {
     if (mf[sms] > 0) return DUET_OK;
     std::vector<float> tb, tf;
@@ -1379,6 +1650,22 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
       CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
       tf.push_back(ms);
     }
+    if (use_fa) {
+      std::vector<float> ta;
+      for (int rep = 0; rep < 5; ++rep) {
+        CUDA_TRY(cudaEventRecord(e0, st));
+        if (prefill_attn(c, c->pre, apf, dqf, sp.n_q_heads * sp.head_dim, dof, QF, da.k_pool, da.v_pool, da.n_pages,
+                         sms, st) <= 0)
+          DUET_FAIL(DUET_ERR_CUDA, "calibration: prefill attention could not be launched");
+        CUDA_TRY(cudaEventRecord(e1, st));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        ta.push_back(ms);
+      }
+      std::sort(ta.begin(), ta.end());
+      mfa[sms] = fa_flops / (ta[ta.size() / 2] * 1e-3);
+    }
     DUET_TRY(check_launch("calibration"));
     std::sort(tb.begin(), tb.end());
     std::sort(tf.begin(), tf.end());
@@ -1394,6 +1681,14 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(buf);
+  if (dqf) cudaFree(dqf);
+  if (dof) cudaFree(dof);
+  // the f4 co-run decision of later temporal steps uses the measured attention rates
+  if (use_attn && use_fa)
+    for (int s = 1; s <= c->total_sms; ++s) {
+      c->cal_bw[s] = mb[s];
+      c->cal_fa[s] = mfa[s];
+    }
   if (d_meta) cudaFree(d_meta);
   if (dq) cudaFree(dq);
   if (dout) cudaFree(dout);
@@ -1428,6 +1723,56 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
   }
   for (int s = c->total_sms + 1; s < len; ++s) flops[s] = bw[s] = 0.0;
   return DUET_OK;
+}
+
+// The hardware stream ceiling per partition size (roofline denominators of the decode side, SURVEY
+// §8(d)): plain 16-B LDG streaming of a >= 1 GiB buffer from 2048 threads per SM, median of 5.
+extern "C" duet_status duet_calibrate_stream(duet_ctx* c, double* bw, int32_t len) {
+  clear_error();
+  if (!c || !bw) DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL argument");
+  if (len < c->total_sms + 1) DUET_FAIL(DUET_ERR_CAPACITY, "table needs %d entries", c->total_sms + 1);
+  CUDA_TRY(cudaSetDevice(c->device));
+  for (auto& p : c->parts) DUET_TRY(ensure_partition(c, p));
+  size_t free_b = 0, total_b = 0;
+  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  size_t n_bytes = (size_t)2 << 30;
+  while (n_bytes > ((size_t)256 << 20) && n_bytes + ((size_t)1 << 30) > free_b) n_bytes >>= 1;
+  void* buf = nullptr;
+  unsigned long long* sink = nullptr;
+  CUDA_TRY(cudaMalloc(&buf, n_bytes));
+  CUDA_TRY(cudaMalloc(&sink, 4 * 160 * sizeof(unsigned long long)));
+  launch_fill_hash(DT::BF16, buf, n_bytes / 2, 5u, c->s_full);
+  CUDA_TRY(cudaStreamSynchronize(c->s_full));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  for (int s = 0; s < len; ++s) bw[s] = 0.0;
+  auto measure = [&](cudaStream_t st, int sms) -> duet_status {
+    if (bw[sms] > 0) return DUET_OK;
+    std::vector<float> t;
+    for (int rep = 0; rep < 5; ++rep) {
+      CUDA_TRY(cudaEventRecord(e0, st));
+      launch_stream_read(buf, n_bytes, sink, sms, st);
+      CUDA_TRY(cudaEventRecord(e1, st));
+      CUDA_TRY(cudaEventSynchronize(e1));
+      float ms;
+      CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+      t.push_back(ms);
+    }
+    std::sort(t.begin(), t.end());
+    bw[sms] = (double)n_bytes / (t[t.size() / 2] * 1e-3);
+    return DUET_OK;
+  };
+  duet_status st = measure(c->s_full, c->total_sms);
+  for (auto& p : c->parts) {
+    if (st == DUET_OK) st = measure(p.s_dec, p.s_d);
+    if (st == DUET_OK) st = measure(p.s_pre, p.s_p);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  cudaFree(sink);
+  return st;
 }
 
 // ---------------------------------------------------------------------------------- live timing

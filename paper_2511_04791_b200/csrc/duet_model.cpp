@@ -308,6 +308,11 @@ extern "C" duet_status duet_choose_split(const duet_model_spec* spec, const duet
     }
     b_sp = S_p; b_sd = best_sd; b_k = kb; b_tp = t_p; b_td = best_td;
     flags = DUET_FLAG_INFEASIBLE;
+    // reading #20b: both modes miss tau; the spatial fallback stays only if its rho is not below the
+    // temporal rho (Alg. 1's objective) — else the mixed batch runs temporally, flagged
+    const double rho_t = t_mixed > 0 ? (double)(T_dec + T_pre) / t_mixed : 0.0;
+    if (rho_best < rho_t && !(opts & (DUET_OPT_VERBATIM_INFEASIBLE | DUET_OPT_FORCE_SPATIAL)))
+      return temporal(DUET_FLAG_INFEASIBLE);
   }
   out->mode = DUET_MODE_SPATIAL;
   out->s_p = b_sp;
@@ -318,5 +323,44 @@ extern "C" duet_status duet_choose_split(const duet_model_spec* spec, const duet
   out->t_p = b_tp;
   out->t_d = b_td;
   out->rho = rho_best;
+  return DUET_OK;
+}
+
+// f4: the attention co-run of a temporal step.  The two attentions of one layer are
+// independent (prefill: tensor-bound causal attention; decode: HBM-bound paged attention), so they may
+// run side by side on an S_d / S - S_d split instead of one after the other on the full device.  With
+// the calibrated per-size rates (prefill-attention FLOP/s, decode-attention B/s), pick the first
+// candidate minimising max(F / fa(S - S_d), B / bw(S_d)); co-run only when that beats the sequential
+// F / fa(S) + B / bw(S) by more than the fork/join overhead.
+extern "C" duet_status duet_corun_choose(const duet_corun_profile* p, double attn_flops_pre, double attn_bytes_dec,
+                                         int32_t* s_d_out, double* t_out) {
+  duet::clear_error();
+  if (!p || !s_d_out || !p->fa_flops_at_sms || !p->dec_bw_at_sms || (p->n_cand > 0 && !p->cand_sd_sms))
+    DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL argument");
+  const int32_t S = p->total_sms;
+  if (S < 2 || p->n_cand < 0 || attn_flops_pre < 0 || attn_bytes_dec < 0)
+    DUET_FAIL(DUET_ERR_INVALID_ARG, "total_sms = %d, n_cand = %d", S, p->n_cand);
+  if (!(p->fa_flops_at_sms[S] > 0) || !(p->dec_bw_at_sms[S] > 0))
+    DUET_FAIL(DUET_ERR_CONFIG, "full-device rates must be > 0");
+  const double t_seq = attn_flops_pre / p->fa_flops_at_sms[S] + attn_bytes_dec / p->dec_bw_at_sms[S];
+  double best_t = t_seq - p->overhead_s;
+  int32_t best = 0;
+  if (attn_flops_pre > 0 && attn_bytes_dec > 0) {
+    for (int32_t i = 0; i < p->n_cand; ++i) {
+      const int32_t sd = p->cand_sd_sms[i], sp = S - sd;
+      if (sd < p->min_sms || sp < p->min_sms || sd >= S) continue;
+      const double fa = p->fa_flops_at_sms[sp], bw = p->dec_bw_at_sms[sd];
+      if (!(fa > 0) || !(bw > 0)) continue;
+      double t = attn_flops_pre / fa;
+      const double td = attn_bytes_dec / bw;
+      if (td > t) t = td;
+      if (t < best_t) {
+        best_t = t;
+        best = sd;
+      }
+    }
+  }
+  *s_d_out = best;
+  if (t_out) *t_out = best ? best_t : t_seq;
   return DUET_OK;
 }

@@ -1,6 +1,7 @@
 // Trace-driven iteration stream: the host side that forms each mixed iteration
 // the hot path executes.
-//   * batch former: decode-first — every running decode joins (up to max_batch) — then
+//   * batch former: decode-first — every running decode joins (admission keeps the
+//     running requests within max_batch) — then
 //     chunked prefill fills the remaining token budget, oldest in-progress prompt first, then newly
 //     arrived requests in FIFO order;
 //   * KV block allocator: 16-token pages from a free list; a request is admitted
@@ -94,8 +95,11 @@ extern "C" duet_status duet_sched_next(duet_sched* s, double now_s, duet_iterati
   if (!s || !out) DUET_FAIL(DUET_ERR_INVALID_ARG, "sched/out is NULL");
   if (s->it_open) DUET_FAIL(DUET_ERR_INVALID_ARG, "the previous iteration was not committed");
   const auto& cf = s->cfg;
-  // admission: FIFO, only when the whole request (prompt + output + look-ahead) fits the free pages
-  while (!s->waiting.empty() && (int)s->prefilling.size() < cf.max_prefill_seqs) {
+  // admission: FIFO, only when the whole request (prompt + output + look-ahead) fits the free pages,
+  // and only while the admitted, unfinished requests stay within max_batch — so every running decode
+  // gets a row in every iteration (decode-first) and none waits with its pages held
+  while (!s->waiting.empty() && (int)s->prefilling.size() < cf.max_prefill_seqs &&
+         (int)(s->prefilling.size() + s->decoding.size()) < cf.max_batch) {
     Req& r = s->reqs[s->waiting.front()];
     if (r.arrival > now_s) break;
     const int32_t need = pages_for((int64_t)r.prompt + r.output + cf.k_max, cf.page_size);
@@ -111,10 +115,8 @@ extern "C" duet_status duet_sched_next(duet_sched* s, double now_s, duet_iterati
   s->it_ids.clear();
   s->it_q.clear();
   s->it_c.clear();
-  // decode first: every running decode, up to max_batch
-  std::vector<size_t> dec;
-  for (size_t i : s->decoding)
-    if ((int)dec.size() < cf.max_batch) dec.push_back(i);
+  // decode first: every running decode (admission keeps them within max_batch)
+  std::vector<size_t> dec(s->decoding.begin(), s->decoding.end());
   // chunked prefill in the remaining token budget, oldest prompt first
   int32_t budget = cf.token_budget - (int32_t)dec.size();
   std::vector<std::pair<size_t, int32_t>> pre;

@@ -102,6 +102,10 @@ struct DecodeAttnArgs {
 int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st);
 bool decode_tc_supported(const DecodeAttnArgs& a);
 int launch_decode_tc(const DecodeAttnArgs& a, int pages_per_split, int n_splits, cudaStream_t st);
+// K in registers + V by bulk copies (small partitions; kernels_decode_hyb.cu); variant "hy4x3" ...
+bool decode_hyb_supported(const DecodeAttnArgs& a);
+int launch_decode_hyb(const DecodeAttnArgs& a, int pages_per_split, int n_splits, const char* variant,
+                      cudaStream_t st);
 
 // ---------------------------------------------------------------- prefill attention
 // Causal attention of the chunk rows over prefix + chunk (reading #7): sequence s has rows
@@ -144,8 +148,12 @@ int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st);
 // embed[token] (x_next may be NULL)
 int launch_argmax_embed(const void* logits, int vocab, const void* embed, void* x_next, int d, int* tokens,
                         const int* step, int n, cudaStream_t st);
+// ts / ts_cnt (nullable): token-time ring of kTokTsSlots %globaltimer stamps; the bump kernel of every step
+// writes slot (*ts_cnt)++ (the time the step's tokens are complete).  launch_stamp writes one stamp.
+constexpr int kTokTsSlots = 4096;
 int launch_decode_advance(DT dt, const void* y, void* xin, void* y_out, int n, int d, int* pos, int* step,
-                          cudaStream_t st);
+                          cudaStream_t st, unsigned long long* ts = nullptr, int* ts_cnt = nullptr);
+int launch_stamp(unsigned long long* ts, int* cnt, cudaStream_t st);
 
 // Streaming-read kernel for B_HBM(S) calibration: reads n_bytes, writes one word per CTA.
 int launch_stream_read(const void* buf, size_t n_bytes, unsigned long long* sink, int num_sms, cudaStream_t st);

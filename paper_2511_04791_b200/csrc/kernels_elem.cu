@@ -206,11 +206,26 @@ __global__ void decode_advance_kernel(const T* __restrict__ y, T* __restrict__ x
     if (xin) xin[i] = v;  // synthetic feedback (reading #26); with an LM head the embedding is the input
   }
 }
-__global__ void decode_bump_kernel(int n, int* pos, int* step) {
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// token-time ring (TBT per decode step): slot (*cnt)++ mod kTokTsSlots <- %globaltimer
+__device__ __forceinline__ void stamp_token(unsigned long long* ts, int* cnt) {
+  if (!ts) return;
+  const int i = atomicAdd(cnt, 1);
+  ts[i & (kTokTsSlots - 1)] = globaltimer_ns();
+}
+__global__ void decode_bump_kernel(int n, int* pos, int* step, unsigned long long* ts, int* ts_cnt) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) pos[i] += 1;
-  if (i == 0) *step += 1;
+  if (i == 0) {
+    *step += 1;
+    stamp_token(ts, ts_cnt);  // this step's tokens are complete: every earlier kernel of the stream is done
+  }
 }
+__global__ void stamp_kernel(unsigned long long* ts, int* cnt) { stamp_token(ts, cnt); }
 
 // ---------------------------------------------------------------- greedy token + embedding (f1)
 // One CTA per row: token = argmax over the vocab of the bf16 logits (the lowest index among equal
@@ -273,8 +288,13 @@ int launch_argmax_embed(const void* logits, int vocab, const void* embed, void* 
   return 1;
 }
 
+int launch_stamp(unsigned long long* ts, int* cnt, cudaStream_t st) {
+  stamp_kernel<<<1, 1, 0, st>>>(ts, cnt);
+  return 1;
+}
+
 int launch_decode_advance(DT dt, const void* y, void* xin, void* y_out, int n, int d, int* pos, int* step,
-                          cudaStream_t st) {
+                          cudaStream_t st, unsigned long long* ts, int* ts_cnt) {
   if (n <= 0) return 0;
   const int blocks = (int)(((size_t)n * d + 1023) / 1024) < 64 ? (int)(((size_t)n * d + 1023) / 1024) : 64;
   if (dt == DT::BF16)
@@ -282,7 +302,7 @@ int launch_decode_advance(DT dt, const void* y, void* xin, void* y_out, int n, i
   else
     decode_advance_kernel<float><<<blocks, 1024, 0, st>>>((const float*)y, (float*)xin, (float*)y_out, n, d, pos,
                                                           step);
-  decode_bump_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, pos, step);
+  decode_bump_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, pos, step, ts, ts_cnt);
   return 2;
 }
 

@@ -491,6 +491,8 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
 
 bool gemm2_supported(const GemmArgs& a, int num_sms) {
   static const bool on = !getenv("DUET_GEMM2") || atoi(getenv("DUET_GEMM2")) != 0;  // A/B switch
+  auto mis = [](const void* p) { return ((uintptr_t)p & 15) != 0; };  // TMA / 16-B epilogue alignment
+  if (mis(a.A) || mis(a.B) || mis(a.C) || mis(a.R) || mis(a.R2) || mis(a.C2)) return false;
   return on && a.M > 128 && num_sms >= 2 && a.K % tc2::BK == 0 && a.lda % 8 == 0 && a.ldb % 8 == 0 &&
          a.ldc % 8 == 0 && (!a.R || a.ldr % 8 == 0) && (a.epi != EPI_SWIGLU || a.N % 128 == 0);
 }

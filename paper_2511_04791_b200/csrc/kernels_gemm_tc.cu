@@ -643,6 +643,9 @@ bool gemm_tc_supported(const GemmArgs& a) {
   // K in whole 64-element blocks; 16-byte aligned rows for TMA and vector epilogue loads
   if (a.K % tc::BK || a.M <= 0) return false;
   if (a.lda % 8 || a.ldb % 8 || a.ldc % 8 || (a.R && a.ldr % 8)) return false;
+  // TMA maps and the 16-B vector epilogue need 16-byte aligned base pointers
+  auto mis = [](const void* p) { return ((uintptr_t)p & 15) != 0; };
+  if (mis(a.A) || mis(a.B) || mis(a.C) || mis(a.R) || mis(a.R2) || mis(a.C2)) return false;
   if (a.epi == EPI_SWIGLU && a.N % 128) return false;
   if (!tc::encode_fn()) return false;
   return true;

@@ -318,6 +318,7 @@ def test_tp_allreduce_path_world1_bitwise():
     torch.cuda.synchronize()
     assert torch.equal(g2.y_pre, ref2.y_pre) and torch.equal(g2.y_dec, ref2.y_dec)
     assert ctx_tp.calibrate_allreduce() == (0.0, 0.0)
+    ctx_tp.check_comms()          # no asynchronous NCCL error on either side's communicator
     ctx2.close()
     ctx_tp.close()
 

@@ -1,4 +1,5 @@
 """libduet.so host side (no GPU needed): symbols, predictor and Alg. 1 bit-exact vs the oracle."""
+import math
 import random
 import re
 import os
@@ -86,7 +87,7 @@ def test_choose_split_tuple_exact_vs_oracle_and_exhaustive():
         b = _batch(rnd)
         tau = 10 ** rnd.uniform(-5, 0)
         kmax = rnd.choice([1, 8, 32])
-        opts = rnd.choice([0, D.DUET_OPT_FORCE_SPATIAL, D.DUET_OPT_INCLUDE_CLS])
+        opts = rnd.choice([0, D.DUET_OPT_FORCE_SPATIAL, D.DUET_OPT_INCLUDE_CLS, D.DUET_OPT_VERBATIM_INFEASIBLE])
         reqs = [R.Req(*e) for e in b]
         ref = R.choose_split(so, po, reqs, tau, kmax, opts)
         got = D.duet_choose_split(sc, pc, b, tau, kmax, opts)
@@ -95,7 +96,7 @@ def test_choose_split_tuple_exact_vs_oracle_and_exhaustive():
         if i % 5 == 0:
             assert R.choose_split_exhaustive(so, po, reqs, tau, kmax, opts) == ref
         kinds.add((ref.mode, ref.flags))
-    assert {(0, 0), (1, 0), (1, 1), (0, 2)} <= kinds
+    assert {(0, 0), (1, 0), (1, 1), (0, 2), (0, 1)} <= kinds   # (0, 1): the reading #20b guard
 
 
 @settings(max_examples=300, deadline=None)
@@ -150,3 +151,37 @@ def test_optimizer_speed_under_1ms():
         ts.append(time.perf_counter() - t)
     ts.sort()
     assert ts[50] < 1e-3, ts[50]
+
+
+def test_corun_choose_host_logic():
+    """f4 co-run choice (duet_corun_choose): against a direct enumeration of the documented rule on random
+    calibrated-looking tables, plus its limiting cases."""
+    rnd = random.Random(21)
+    S = 148
+    cand = list(range(8, 148, 8))
+    for _ in range(300):
+        fa = [0.0] + [rnd.uniform(3e12, 5e12) * i for i in range(1, S + 1)]
+        sat, s0 = rnd.uniform(4e12, 7e12), rnd.uniform(10, 50)
+        bw = [0.0] + [sat * (1 - math.exp(-i / s0)) for i in range(1, S + 1)]
+        F = 10 ** rnd.uniform(8, 12)
+        B = 10 ** rnd.uniform(6, 10)
+        ov = rnd.choice([0.0, 15e-6])
+        sd, t = D.duet_corun_choose(S, cand, fa, bw, F, B, 16, ov)
+        t_seq = F / fa[S] + B / bw[S]
+        best, best_t = 0, t_seq - ov
+        for c in cand:
+            if c < 16 or S - c < 16:
+                continue
+            tc = max(F / fa[S - c], B / bw[c])
+            if tc < best_t:
+                best, best_t = c, tc
+        assert sd == best
+        assert t == (best_t if best else t_seq)
+    # a phase absent or a tiny batch: never co-run
+    fa = [0.0] + [4e12 * i for i in range(1, S + 1)]
+    bw = [0.0] + [6e12 * min(1.0, i / 40) for i in range(1, S + 1)]
+    assert D.duet_corun_choose(S, cand, fa, bw, 0.0, 1e9)[0] == 0
+    assert D.duet_corun_choose(S, cand, fa, bw, 1e6, 1e4)[0] == 0       # << the 15 us fork/join cost
+    # balanced large attentions (cfg2-like: 34 GFLOP causal, 1.07 GB of KV): co-run on a split
+    sd, t = D.duet_corun_choose(S, cand, fa, bw, 34.4e9, 1.07e9)
+    assert 16 <= sd <= 132 and t < 34.4e9 / fa[S] + 1.07e9 / bw[S]

@@ -25,6 +25,8 @@ def _run(trace, k_choices=(1, 2, 3), seed=0, **cfg):
     now, log = 0.0, []
     total_tokens = 0
     admitted_order = []
+    meta = {r[0]: (r[1], r[2]) for r in trace}     # id -> (prompt, output)
+    running = {}                                   # id -> tokens generated, for requests past their prompt
     for _ in range(100000):
         it = s.next(now)
         if not it["prefill"] and not it["decode"]:
@@ -49,9 +51,21 @@ def _run(trace, k_choices=(1, 2, 3), seed=0, **cfg):
             need = -(-(c + k_max) // P)
             used.extend(tab[n_pre + j][:need])
         assert len(used) == len(set(used))
-        # decode-first: a prefill chunk only when every running decode got a row
+        # decode-first: every request past its prompt and not finished has a decode row, so
+        # no running decode is ever skipped (and none waits while holding its pages)
+        assert sorted(rid for rid, _ in it["decode"]) == sorted(running)
+        assert len(running) + n_pre <= max_batch
+        for rid, c in it["decode"]:                 # the decode input is the last generated token
+            assert c == meta[rid][0] + running[rid] - 1
         k = int(rng.choice(k_choices))
         toks, fin = s.commit(k)
+        for rid in list(running):
+            running[rid] += min(k, meta[rid][1] - running[rid])
+            if running[rid] >= meta[rid][1]:
+                del running[rid]
+        for rid, q, c in it["prefill"]:
+            if c + q == meta[rid][0] and meta[rid][1] > 1:
+                running[rid] = 1                    # the prompt's last position yields token 1
         total_tokens += toks
         log.append((tuple(it["prefill"]), tuple(it["decode"]), toks))
         now += 1e-3
@@ -70,6 +84,15 @@ def test_sched_invariants_and_token_accounting(seed):
     log, total, order = _run(trace, seed=seed, **CFG)
     assert total == sum(p + o for _, p, o, _ in trace)   # every prompt token prefilled, every output produced
     assert order == sorted(order)                        # FIFO admission (ids follow arrival order)
+
+
+@pytest.mark.parametrize("max_batch", [2, 5])
+def test_sched_decodes_never_exceed_max_batch(max_batch):
+    """More arrivals than max_batch: admission waits, so every running decode gets a row each iteration."""
+    trace = _trace(11, n=30, max_prompt=400, max_out=40)
+    log, total, order = _run(trace, seed=3, **dict(CFG, max_batch=max_batch))
+    assert total == sum(p + o for _, p, o, _ in trace)
+    assert max(len(d) for _, d, _ in log) <= max_batch
 
 
 def test_sched_deterministic():

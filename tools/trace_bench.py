@@ -8,8 +8,9 @@ duet_step runs it, duet_sched_commit advances the requests.  Policies:
   static    every iteration temporal (aggregated, one stream)
   adaptive  Alg. 1 (duet_choose_split against the calibrated tables; spatial with k look-ahead steps
             when t_mixed > tau)
-Simulated time advances by each iteration's measured GPU window.  Reports tokens/s, the decode-step
-latency (TBT) distribution and the SLO attainment.  Inputs are synthetic (values do not matter for
+Simulated time advances by each iteration's measured GPU window.  Reports tokens/s, the inter-token gap
+(TBT) distribution — a spatial window's last gap includes the wait for the prefill side to join — and
+the SLO attainment.  Inputs are synthetic (values do not matter for
 timing; KV pages start zeroed).
 
 usage: python tools/trace_bench.py [--model cfg4] [--n-req 24] [--qps 2] [--layers 8] [--max-iters 300]
@@ -34,6 +35,7 @@ def main():
     ap.add_argument("--policies", default="static,adaptive")
     ap.add_argument("--seed", type=int, default=4795)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--no-graph", action="store_true", help="decode steps launched eagerly (no CUDA graphs)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -62,7 +64,7 @@ def main():
     spec = D.make_spec(m.n_layers, m.d_model, m.ffn_dim, m.n_q_heads, m.n_kv_heads, m.head_dim, m.vocab, 2, 1,
                        int(m.qkv_bias), 1, m.rope_theta, m.norm_eps)
     ctx = D.Ctx(spec, budget, max_seqs, max_batch, k_max, max_pages, max_pages * P + 16, D.DUET_DTYPE_BF16,
-                D.DUET_CTX_NO_GRAPH)
+                D.DUET_CTX_NO_GRAPH if args.no_graph else 0)
     parts, total = ctx.partitions()
     fl, bw = ctx.calibrate(total)
     hw = D.HwProfile(total, parts, fl, bw)
@@ -104,9 +106,14 @@ def main():
             torch.cuda.synchronize()
             st = ctx.last_step_times()
             window = st["t_window"]
-            if n_dec:   # per decode step latency seen by the running requests
-                step_lat = st["t_decode"] / k if split.mode == D.DUET_MODE_SPATIAL else window
-                tbt.extend([step_lat] * k)
+            if n_dec:   # inter-token gaps seen by the running requests: in a spatial window k - 1 gaps of
+                # t_decode / k, and the last token also waits for the prefill side to join (the next window
+                # cannot start before it) — that stall is charged to the window's last gap
+                if split.mode == D.DUET_MODE_SPATIAL:
+                    g = st["t_decode"] / k
+                    tbt.extend([g] * (k - 1) + [g + max(0.0, window - st["t_decode"])])
+                else:
+                    tbt.append(window)
             modes["spatial" if split.mode == D.DUET_MODE_SPATIAL else "temporal"] += 1
             toks, _ = sched.commit(k)
             tokens += toks
