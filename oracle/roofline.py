@@ -18,7 +18,8 @@ S_d = S, #17 k clamped to [1, k_max], #18 strict ">" (first found wins),
 #19 temporal at equality, #20 infeasible fallback = argmin t_d, #20b the
 infeasible spatial fallback is kept only when its rho is not below the temporal
 rho (both violate tau; the paper's objective, throughput, decides), #21 a batch
-missing one phase runs temporally, #25 T_pre = sum q over prefill entries,
+missing one phase runs temporally, #23 (opt-in OPT_BOUNDARY_TBT) a candidate (S_d, k)
+must also keep the window-boundary gap t_d + max(0, t_p - k t_d) within tau, #25 T_pre = sum q over prefill entries,
 T_dec = number of decode entries.
 """
 from __future__ import annotations
@@ -27,7 +28,7 @@ import math
 from dataclasses import dataclass
 
 PHASE_PREFILL_FULL, PHASE_PREFILL_CHUNK, PHASE_DECODE = 0, 1, 2
-OPT_FORCE_SPATIAL, OPT_INCLUDE_CLS, OPT_VERBATIM_INFEASIBLE = 1, 2, 4
+OPT_FORCE_SPATIAL, OPT_INCLUDE_CLS, OPT_VERBATIM_INFEASIBLE, OPT_BOUNDARY_TBT = 1, 2, 4, 8
 FLAG_INFEASIBLE, FLAG_DEGENERATE = 1, 2
 MODE_TEMPORAL, MODE_SPATIAL = 0, 1
 
@@ -227,8 +228,16 @@ def _temporal(batch, t_mixed, flags, S):
     return Split(MODE_TEMPORAL, S, 0, 1, flags, t_mixed, t_mixed, t_mixed, rho)
 
 
-def alg1_search(S: int, cand, tau: float, k_max: int, t_d_of, t_p_of, T_dec: int, T_pre: int):
+def boundary_gap(k: int, t_d: float, t_p: float) -> float:
+    """The inter-token gap across a window boundary (reading #23): the window's last decode step, plus
+    the time its decodes wait for the prefill side to join, t_d + max(0, t_p - k t_d)."""
+    return t_d + max(0.0, t_p - float(k) * t_d)
+
+
+def alg1_search(S: int, cand, tau: float, k_max: int, t_d_of, t_p_of, T_dec: int, T_pre: int,
+                boundary: bool = False):
     """Lines 7-21 of Algorithm 1 for given latency functions t_d(S_d), t_p(S_p).
+    boundary (opt-in, reading #23): a (S_d, k) candidate must also keep the boundary gap <= tau.
     Returns (rho*, (S_p, S_d, k, t_p, t_d)) or (0.0, None) when no S_d meets tau."""
     rho_best, best = 0.0, None                                     # l.7
     for S_d in cand:                                               # l.8 (reading #16)
@@ -241,14 +250,18 @@ def alg1_search(S: int, cand, tau: float, k_max: int, t_d_of, t_p_of, T_dec: int
         t_p = t_p_of(S_p)                                          # l.14
         r = math.floor(t_p / t_d)
         for k in (_clamp_k(r, k_max), _clamp_k(r + 1, k_max)):    # l.15 (reading #17)
+            if boundary and boundary_gap(k, t_d, t_p) > tau:
+                continue
             rho = float(k * T_dec + T_pre) / max(float(k) * t_d, t_p)   # l.16
             if rho > rho_best:                                     # l.17-18 (reading #18)
                 rho_best, best = rho, (S_p, S_d, k, t_p, t_d)
     return rho_best, best
 
 
-def exhaustive_search(S: int, cand, tau: float, k_max: int, t_d_of, t_p_of, T_dec: int, T_pre: int):
-    """Brute force over every (S_d in cand, k in [1, k_max]) with t_d <= tau; ties -> smaller S_d, k."""
+def exhaustive_search(S: int, cand, tau: float, k_max: int, t_d_of, t_p_of, T_dec: int, T_pre: int,
+                      boundary: bool = False):
+    """Brute force over every (S_d in cand, k in [1, k_max]) with t_d <= tau (and, with boundary, the
+    boundary gap <= tau); ties -> smaller S_d, k."""
     rho_best, best = 0.0, None
     for S_d in cand:
         if S_d >= S:
@@ -258,6 +271,8 @@ def exhaustive_search(S: int, cand, tau: float, k_max: int, t_d_of, t_p_of, T_de
             continue
         t_p = t_p_of(S - S_d)
         for k in range(1, k_max + 1):
+            if boundary and boundary_gap(k, t_d, t_p) > tau:
+                continue
             rho = float(k * T_dec + T_pre) / max(float(k) * t_d, t_p)
             if rho > rho_best:
                 rho_best, best = rho, (S - S_d, S_d, k, t_p, t_d)
@@ -305,7 +320,8 @@ def _choose(sp: Spec, prof: Profile, batch: list, tau: float, k_max: int, opts: 
     T_dec, T_pre = len(D), sum(r.q for r in P)                     # reading #25
     t_d_of = lambda S_d: predict(sp, prof, D, S_d, incl)["t_total"]
     t_p_of = lambda S_p: predict(sp, prof, P, S_p, incl)["t_total"]
-    rho, best = search(S, prof.cand_sd_sms, tau, k_max, t_d_of, t_p_of, T_dec, T_pre)
+    rho, best = search(S, prof.cand_sd_sms, tau, k_max, t_d_of, t_p_of, T_dec, T_pre,
+                       bool(opts & OPT_BOUNDARY_TBT))
     flags = 0
     if best is None:
         rho, best = infeasible_fallback(S, prof.cand_sd_sms, k_max, t_d_of, t_p_of, T_dec, T_pre)

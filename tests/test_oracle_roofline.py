@@ -173,7 +173,8 @@ def test_alg1_equals_exhaustive_1200_instances():
         sp = R.Spec(rnd.choice([1, 4, 32]), 4096, 14336, 32, 8, 128, 128256, 2)
         tau = 10 ** rnd.uniform(-5, -0.5)
         k_max = rnd.choice([1, 4, 32, 64])
-        opts = rnd.choice([0, R.OPT_FORCE_SPATIAL, R.OPT_VERBATIM_INFEASIBLE])
+        opts = rnd.choice([0, R.OPT_FORCE_SPATIAL, R.OPT_VERBATIM_INFEASIBLE, R.OPT_BOUNDARY_TBT,
+                           R.OPT_BOUNDARY_TBT | R.OPT_FORCE_SPATIAL])
         a = R.choose_split(sp, prof, batch, tau, k_max, opts)
         b = R.choose_split_exhaustive(sp, prof, batch, tau, k_max, opts)
         assert a == b, (i, a, b)
@@ -236,6 +237,33 @@ def test_infeasible_guard_reading_20b():
     s2 = R.choose_split(sp2, prof2, b2, 1e-15)
     assert s2.mode == R.MODE_SPATIAL and s2.flags == R.FLAG_INFEASIBLE
     assert s2.rho >= 51 / s2.t_mixed
+
+
+def test_boundary_tbt_option_reading_23():
+    """Reading #23 (opt-in).  The paper constrains only t_d <= tau; a decode token at a window
+    boundary also waits for the prefill side, gap = t_d + max(0, t_p - k t_d).  On the SPEC toy (S = 8,
+    t_d(S_d) = 24/S_d, t_p(S_p) = 96/S_p ms, T_dec = 16, T_pre = 512, tau = 10 ms) the verbatim
+    winner (S_p, S_d, k) = (5, 3, 2) has a 19.2 - 16 + 8 = 11.2 ms boundary gap > tau.  With the option
+    Alg. 1's two-candidate rule still finds the optimum (the k = floor(t_p/t_d) + 1 candidate never
+    stalls), so it must equal the exhaustive search and a brute force written out below."""
+    t_d_of = lambda S_d: 24.0 / S_d
+    t_p_of = lambda S_p: 96.0 / S_p
+    rho0, best0 = R.alg1_search(8, range(1, 8), 10.0, 64, t_d_of, t_p_of, 16, 512)
+    assert best0[:3] == (5, 3, 2) and R.boundary_gap(2, 8.0, 19.2) > 10.0
+    rho1, best1 = R.alg1_search(8, range(1, 8), 10.0, 64, t_d_of, t_p_of, 16, 512, boundary=True)
+    rho2, best2 = R.exhaustive_search(8, range(1, 8), 10.0, 64, t_d_of, t_p_of, 16, 512, boundary=True)
+    assert (rho1, best1) == (rho2, best2)
+    S_p, S_d, k, t_p, t_d = best1
+    assert R.boundary_gap(k, t_d, t_p) <= 10.0 and rho1 < rho0
+    # brute force written out: every (S_d, k) with t_d <= tau and gap <= tau
+    cands = []
+    for sd in range(1, 8):
+        td, tp = 24.0 / sd, 96.0 / (8 - sd)
+        for kk in range(1, 65):
+            if td <= 10.0 and td + max(0.0, tp - kk * td) <= 10.0:
+                cands.append(((kk * 16 + 512) / max(kk * td, tp), -sd, -kk))
+    top = max(cands)
+    assert abs(top[0] - rho1) < 1e-12 and (-top[1], -top[2]) == (S_d, k)
 
 
 def test_paper_qualitative_anchors():
