@@ -88,7 +88,8 @@ typedef struct {
   double t_linear, t_norm_act, t_attn, t_allreduce, t_block, t_cls, t_total;
 } duet_latency;
 
-enum { DUET_OPT_FORCE_SPATIAL = 1u, DUET_OPT_INCLUDE_CLS = 2u, DUET_OPT_VERBATIM_INFEASIBLE = 4u };
+enum { DUET_OPT_FORCE_SPATIAL = 1u, DUET_OPT_INCLUDE_CLS = 2u, DUET_OPT_VERBATIM_INFEASIBLE = 4u,
+       DUET_OPT_BOUNDARY_TBT = 8u };
 
 /* f_roofline(batch, Pi_SM(sms), B_HBM(sms)) — the attention-aware roofline model of §4.1
  * (P:194-250): token-level operators max(F/Pi, B/B) with F_lin = 2 n d_i d_o,
@@ -124,6 +125,8 @@ typedef struct {
  * (one phase absent -> temporal), INFEASIBLE (no S_d meets tau -> argmin t_d; reading #20b: that
  * spatial split is kept only if its rho >= the temporal rho sum(q)/t_mixed, else the batch runs
  * temporally with the INFEASIBLE flag — VERBATIM_INFEASIBLE or FORCE_SPATIAL keep it spatial).
+ * BOUNDARY_TBT (opt-in, reading #23): a candidate (S_d, k) must also keep the window-boundary gap
+ * t_d + max(0, t_p - k t_d) <= tau (the paper constrains t_d only).
  * Errors: as duet_predict_latency, plus CONFIG for tbt_slo_s <= 0 or k_max < 1. */
 duet_status duet_choose_split(const duet_model_spec* spec, const duet_hw_profile* hw,
                               const duet_req* batch, int32_t n, double tbt_slo_s, int32_t k_max,
@@ -355,6 +358,17 @@ duet_status duet_last_step_times(duet_ctx* ctx, duet_step_times* out);
  * cannot be provisioned are filled by linear interpolation between measured neighbours.
  * Errors: INVALID_ARG, CUDA. */
 duet_status duet_calibrate(duet_ctx* ctx, double* flops_at_sms, double* bw_at_sms, int32_t len);
+
+/* duet_calibrate with the co-run, sustained refinement (reading R-f of DESIGN.md, "achievable"):
+ * after the standalone pass and about a second of full-device GEMMs (the clocks settle at the power
+ * cap), every split (S_d, S_p) runs two phases of ~pair_seconds each — the calibration GEMM on S_p while
+ * the paged decode attention streams on S_d (-> flops_at_sms[S_p], bw_at_sms[S_d]), then the roles
+ * swapped (-> flops_at_sms[S_d], bw_at_sms[S_p]); the full device runs each kernel alone, sustained.
+ * Rates over the middle 60 % of each side's launches.  Falls back to duet_calibrate's tables where a
+ * size was not measured this way (fp32 contexts).  ~2 * n_partitions * pair_seconds + ~1.5 s.
+ * Errors: as duet_calibrate, INVALID_ARG for pair_seconds <= 0. */
+duet_status duet_calibrate_corun(duet_ctx* ctx, double* flops_at_sms, double* bw_at_sms, int32_t len,
+                                 double pair_seconds);
 
 /* The hardware read-stream ceiling per partition size — the roofline denominator of a decode
  * partition, SURVEY §8(d) (not a predictor input): plain 16-byte LDG streaming of a >= 256 MiB buffer

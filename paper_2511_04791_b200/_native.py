@@ -11,7 +11,7 @@ LIB_PATH = os.path.join(_HERE, "libduet.so")
 
 DUET_OK = 0
 DUET_PHASE_PREFILL_FULL, DUET_PHASE_PREFILL_CHUNK, DUET_PHASE_DECODE = 0, 1, 2
-DUET_OPT_FORCE_SPATIAL, DUET_OPT_INCLUDE_CLS, DUET_OPT_VERBATIM_INFEASIBLE = 1, 2, 4
+DUET_OPT_FORCE_SPATIAL, DUET_OPT_INCLUDE_CLS, DUET_OPT_VERBATIM_INFEASIBLE, DUET_OPT_BOUNDARY_TBT = 1, 2, 4, 8
 DUET_MODE_TEMPORAL, DUET_MODE_SPATIAL = 0, 1
 DUET_FLAG_INFEASIBLE, DUET_FLAG_DEGENERATE = 1, 2
 DUET_DTYPE_BF16, DUET_DTYPE_FP32 = 0, 1
@@ -142,6 +142,8 @@ _SIGS = {
                                        C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "duet_corun_choose": (C.c_int, [C.POINTER(duet_corun_profile), C.c_double, C.c_double, C.POINTER(C.c_int32),
                                     C.POINTER(C.c_double)]),
+    "duet_calibrate_corun": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32,
+                                       C.c_double]),
     "duet_calibrate_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int32]),
     "duet_token_times": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.c_int32,
                                    C.POINTER(C.c_int32)]),
@@ -420,6 +422,13 @@ class Ctx:
         fl = (C.c_double * (total_sms + 1))()
         bw = (C.c_double * (total_sms + 1))()
         _check(lib().duet_calibrate(self.h, fl, bw, total_sms + 1))
+        return list(fl), list(bw)
+
+    def calibrate_corun(self, total_sms: int, pair_seconds: float = 0.12):
+        """Pi_SM(S), B_HBM(S) measured under co-run at sustained clocks (duet_calibrate_corun)."""
+        fl = (C.c_double * (total_sms + 1))()
+        bw = (C.c_double * (total_sms + 1))()
+        _check(lib().duet_calibrate_corun(self.h, fl, bw, total_sms + 1, float(pair_seconds)))
         return list(fl), list(bw)
 
     def calibrate_stream(self, total_sms: int):

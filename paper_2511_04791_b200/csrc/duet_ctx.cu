@@ -1518,7 +1518,21 @@ extern "C" duet_status duet_token_times(duet_ctx* c, int32_t reset, uint64_t* ou
 
 // ---------------------------------------------------------------------------------- calibration
 
+static duet_status calibrate_impl(duet_ctx* c, double* flops, double* bw, int32_t len, double pair_s);
+
 extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, int32_t len) {
+  return calibrate_impl(c, flops, bw, len, 0.0);
+}
+
+extern "C" duet_status duet_calibrate_corun(duet_ctx* c, double* flops, double* bw, int32_t len, double pair_seconds) {
+  if (!(pair_seconds > 0)) {
+    clear_error();
+    DUET_FAIL(DUET_ERR_INVALID_ARG, "pair_seconds = %g must be > 0", pair_seconds);
+  }
+  return calibrate_impl(c, flops, bw, len, pair_seconds);
+}
+
+static duet_status calibrate_impl(duet_ctx* c, double* flops, double* bw, int32_t len, double pair_s) {
   clear_error();
   if (!c || !flops || !bw) DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL argument");
   if (len < c->total_sms + 1) DUET_FAIL(DUET_ERR_CAPACITY, "tables need %d entries", c->total_sms + 1);
@@ -1678,6 +1692,69 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
     DUET_TRY(measure(p.s_dec, p.s_d));
     DUET_TRY(measure(p.s_pre, p.s_p));
   }
+  // Co-run, sustained refinement (reading R-f, "achievable"): the tables the predictor needs are
+  // the rates each partition side achieves while the other side runs the OTHER phase's hot kernel and
+  // the GPU sits at its sustained (power-capped) clocks — not a short burst on an idle GPU.  After a
+  // heat-up, every split (S_d, S_p) runs two phases of ~pair_s seconds: the GEMM on S_p while the
+  // decode attention streams on S_d (-> Pi(S_p), B(S_d)), then the roles swapped (-> Pi(S_d), B(S_p));
+  // the full device runs each kernel alone, sustained.  Each rate is taken over the middle 60 % of
+  // its side's launches, where the two loops overlap.
+  std::vector<double> mf_c(c->total_sms + 1, 0.0), mb_c(c->total_sms + 1, 0.0);
+  if (pair_s > 0 && use_attn) {
+    const double g_flops = 2.0 * GM * (double)GN * GK;
+    GemmArgs g{A, B, C, nullptr, nullptr, GM, GN, GK, GK, GK, GN, 0, EPI_STORE};
+    cudaEvent_t ev[4];
+    for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+    // n launches of one kernel on st; events after launch n/5 and before launch n - n/5
+    auto loop = [&](cudaStream_t st, int sms, bool gemm, int n, cudaEvent_t ea, cudaEvent_t eb) -> duet_status {
+      const int lo = n / 5, hi = n - n / 5;
+      for (int i = 0; i < n; ++i) {
+        if (i == lo) CUDA_TRY(cudaEventRecord(ea, st));
+        if (i == hi) CUDA_TRY(cudaEventRecord(eb, st));
+        if (gemm) {
+          if (launch_gemm(c->dt, g, sms, st) <= 0) DUET_FAIL(DUET_ERR_CUDA, "calibration GEMM could not be launched");
+        } else {
+          da.num_sms = sms;
+          if (launch_decode_attn(c->dt, da, st) <= 0)
+            DUET_FAIL(DUET_ERR_CUDA, "calibration decode attention could not be launched");
+        }
+      }
+      return DUET_OK;
+    };
+    auto n_for = [&](double t_one, double secs) { return std::max(5, (int)std::ceil(secs / std::max(t_one, 1e-7))); };
+    auto elapsed = [&](cudaEvent_t a0, cudaEvent_t a1) -> double {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a0, a1);
+      return ms * 1e-3;
+    };
+    const int S = c->total_sms;
+    // heat-up: about a second of the full-device GEMM (the clocks settle at the power cap)
+    DUET_TRY(loop(c->s_full, S, true, n_for(g_flops / mf[S], 1.0), ev[0], ev[1]));
+    CUDA_TRY(cudaStreamSynchronize(c->s_full));
+    for (auto& p : c->parts) {
+      for (int phase = 0; phase < 2; ++phase) {
+        const int sg = phase == 0 ? p.s_p : p.s_d, sa = phase == 0 ? p.s_d : p.s_p;
+        cudaStream_t stg = phase == 0 ? p.s_pre : p.s_dec, sta = phase == 0 ? p.s_dec : p.s_pre;
+        const int ng = n_for(g_flops / mf[sg], pair_s), na = n_for(attn_bytes / mb[sa], pair_s);
+        DUET_TRY(loop(stg, sg, true, ng, ev[0], ev[1]));
+        DUET_TRY(loop(sta, sa, false, na, ev[2], ev[3]));
+        CUDA_TRY(cudaStreamSynchronize(stg));
+        CUDA_TRY(cudaStreamSynchronize(sta));
+        mf_c[sg] = g_flops * (ng - 2 * (ng / 5)) / elapsed(ev[0], ev[1]);
+        mb_c[sa] = attn_bytes * (na - 2 * (na / 5)) / elapsed(ev[2], ev[3]);
+      }
+    }
+    {  // the full device, each kernel alone, sustained
+      const int ng = n_for(g_flops / mf[S], 4 * pair_s), na = n_for(attn_bytes / mb[S], 2 * pair_s);
+      DUET_TRY(loop(c->s_full, S, true, ng, ev[0], ev[1]));
+      DUET_TRY(loop(c->s_full, S, false, na, ev[2], ev[3]));
+      CUDA_TRY(cudaStreamSynchronize(c->s_full));
+      mf_c[S] = g_flops * (ng - 2 * (ng / 5)) / elapsed(ev[0], ev[1]);
+      mb_c[S] = attn_bytes * (na - 2 * (na / 5)) / elapsed(ev[2], ev[3]);
+    }
+    DUET_TRY(check_launch("co-run calibration"));
+    for (auto e : ev) cudaEventDestroy(e);
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(buf);
@@ -1696,6 +1773,10 @@ extern "C" duet_status duet_calibrate(duet_ctx* c, double* flops, double* bw, in
   cudaFree(A);
   cudaFree(B);
   cudaFree(C);
+  for (int s2 = 1; s2 <= c->total_sms; ++s2) {
+    if (mf_c[s2] > 0) mf[s2] = mf_c[s2];
+    if (mb_c[s2] > 0) mb[s2] = mb_c[s2];
+  }
   // fill unmeasured sizes by linear interpolation (from 0 at S = 0)
   std::vector<int> known;
   for (int s = 1; s <= c->total_sms; ++s)

@@ -247,6 +247,7 @@ extern "C" duet_status duet_choose_split(const duet_model_spec* spec, const duet
   View vP{batch, P.data(), (int32_t)P.size()}, vD{batch, D.data(), (int32_t)D.size()};
 
   // l.7-21
+  const bool boundary = (opts & DUET_OPT_BOUNDARY_TBT) != 0;
   double rho_best = 0.0;
   bool found = false;
   int32_t b_sp = 0, b_sd = 0, b_k = 0;
@@ -263,6 +264,10 @@ extern "C" duet_status duet_choose_split(const duet_model_spec* spec, const duet
     const double r = std::floor(t_p / t_d);
     const int32_t ks[2] = {clamp_k(r, k_max), clamp_k(r + 1.0, k_max)};  // l.15 (reading #17)
     for (int32_t k : ks) {
+      if (boundary) {  // reading #23 (opt-in): the window-boundary gap t_d + max(0, t_p - k t_d) <= tau
+        const double stall = t_p - (double)k * t_d;
+        if (t_d + (stall > 0.0 ? stall : 0.0) > tau) continue;
+      }
       double den = (double)k * t_d;
       if (den < t_p) den = t_p;
       const double rho = (double)((int64_t)k * T_dec + T_pre) / den;  // l.16

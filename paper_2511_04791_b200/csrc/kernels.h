@@ -102,10 +102,6 @@ struct DecodeAttnArgs {
 int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st);
 bool decode_tc_supported(const DecodeAttnArgs& a);
 int launch_decode_tc(const DecodeAttnArgs& a, int pages_per_split, int n_splits, cudaStream_t st);
-// K in registers + V by bulk copies (small partitions; kernels_decode_hyb.cu); variant "hy4x3" ...
-bool decode_hyb_supported(const DecodeAttnArgs& a);
-int launch_decode_hyb(const DecodeAttnArgs& a, int pages_per_split, int n_splits, const char* variant,
-                      cudaStream_t st);
 
 // ---------------------------------------------------------------- prefill attention
 // Causal attention of the chunk rows over prefix + chunk (reading #7): sequence s has rows

@@ -405,7 +405,6 @@ int launch_decode_tc(const DecodeAttnArgs& a, int pps, int n_splits, cudaStream_
   // it best, 3 stages (2 CTAs per SM) on the full GPU.  Page -> warp assignment and the merge order
   // depend only on the 4 warps, so both give bitwise-identical results.
   const char* sel = v ? v : (a.num_sms < 120 ? "cp4x2" : "cp4x3x2");
-  if (sel[0] == 'h' && sel[1] == 'y' && decode_hyb_supported(a)) return launch_decode_hyb(a, pps, n_splits, sel, st);
   if (!strcmp(sel, "cp4x2")) launch_variant<4, 2, false>(mk, mv, a, pps, n_splits, st);   // 3 CTAs/SM
   else if (!strcmp(sel, "cp3x3")) launch_variant<3, 3, false>(mk, mv, a, pps, n_splits, st);   // 3 CTAs/SM
   else if (!strcmp(sel, "cp2x3")) launch_variant<2, 3, false>(mk, mv, a, pps, n_splits, st);   // 4 CTAs/SM

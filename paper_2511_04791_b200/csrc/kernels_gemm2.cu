@@ -140,6 +140,22 @@ struct Params {
   const float2* rope;
 };
 
+// Tile order (grouped rasterization): tiles run in groups of GROUP_M 256-row blocks; inside a group the
+// row block varies fastest, so the pairs of one wave share a few weight column blocks (read once from
+// HBM, multicast through L2) and revisit a bounded set of X row blocks (<= GROUP_M x 256 rows, which
+// stays L2-resident).  With the plain row-fastest order over all rows an X larger than L2 — the down
+// projection's 8192 x 14336 activation at cfg3, 235 MB — was re-read from HBM for every column block
+// (profiles/ncu_traffic.json: 1.34x the algorithmic bytes at cfg2, ~16x X at cfg3).
+constexpr int GROUP_M = 8;
+__device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int& mp, int& nb) {
+  const int g = t / (GROUP_M * num_n);
+  const int first = g * GROUP_M;
+  const int gm = min(num_m2 - first, GROUP_M);
+  const int local = t - g * GROUP_M * num_n;
+  mp = first + local % gm;
+  nb = local / gm;
+}
+
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, Params p) {
@@ -196,7 +212,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #ifndef DUET_NO_WPREFETCH
       if (pair < p.num_tiles) {  // fresh ring: the first STAGES stages are free
         pre = num_k < STAGES ? num_k : STAGES;
-        const int row_w0 = w_row(pair / p.num_m2);
+        int mp0, nb0;
+        tile_coords(pair, p.num_m2, p.num_n, mp0, nb0);
+        const int row_w0 = w_row(nb0);
         for (int kb = 0; kb < pre; ++kb) {
           if (leader) mbar_expect_tx(&full[kb], 2 * STAGE_BYTES);
           tma_load_2cta(&map_w, mapa(smem_u32(&full[kb]), 0), sB + kb * B_BYTES, kb * BK, row_w0);
@@ -207,7 +225,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int t = pair; t < p.num_tiles; t += n_pairs) {
-        const int mp = t % p.num_m2, nb = t / p.num_m2;
+        int mp, nb;
+        tile_coords(t, p.num_m2, p.num_n, mp, nb);
         const int row_x = mp * PAIR_M + (int)rank * BM;
         const int row_w = w_row(nb);
         for (int kb = 0; kb < num_k; ++kb) {
@@ -263,7 +282,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int i = 0;
     for (int t = pair; t < p.num_tiles; t += n_pairs, ++i) {
       const int acc = i & 1;
-      const int mp = t % p.num_m2, nb = t / p.num_m2;
+      int mp, nb;
+      tile_coords(t, p.num_m2, p.num_n, mp, nb);
       // EPI_QKV_ROPE: this row's position, KV page and cos/sin row are fetched while the tile's MMAs
       // still run (the dependent pos -> table / rope loads are off the epilogue's critical path)
       int r_pos = 0, r_page = 0;

@@ -87,7 +87,8 @@ def test_choose_split_tuple_exact_vs_oracle_and_exhaustive():
         b = _batch(rnd)
         tau = 10 ** rnd.uniform(-5, 0)
         kmax = rnd.choice([1, 8, 32])
-        opts = rnd.choice([0, D.DUET_OPT_FORCE_SPATIAL, D.DUET_OPT_INCLUDE_CLS, D.DUET_OPT_VERBATIM_INFEASIBLE])
+        opts = rnd.choice([0, D.DUET_OPT_FORCE_SPATIAL, D.DUET_OPT_INCLUDE_CLS, D.DUET_OPT_VERBATIM_INFEASIBLE,
+                           D.DUET_OPT_BOUNDARY_TBT, D.DUET_OPT_BOUNDARY_TBT | D.DUET_OPT_INCLUDE_CLS])
         reqs = [R.Req(*e) for e in b]
         ref = R.choose_split(so, po, reqs, tau, kmax, opts)
         got = D.duet_choose_split(sc, pc, b, tau, kmax, opts)
