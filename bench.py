@@ -541,18 +541,22 @@ def main():
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tok = 0
         n_p_ = chunk if chunk is not None else n_p
+        clk_ = ClockSampler(lrank)   # each leg's own clocks: a power-capped leg is compared at its clock
+        clk_.start()
         a.record(stream)
         for _ in range(n):
             s_, k_ = one_step(split_fn(), chunk=chunk)
             tok += k_ * n_d + n_p_
         b.record(stream)
         torch.cuda.synchronize()
+        c_ = clk_.stop()
         ts = ctx.token_times(reset=True)
         sp_ = split_fn()
         st_ = side_times(sp_, chunk=chunk)
         k_ = sp_.k if sp_.mode == D.DUET_MODE_SPATIAL else 1
         r = {"tok_s": tok / (a.elapsed_time(b) * 1e-3), "window_ms": st_["t_window"] * 1e3,
-             "t_decode_ms": st_["t_decode"] * 1e3, "t_prefill_ms": st_["t_prefill"] * 1e3, "k": k_}
+             "t_decode_ms": st_["t_decode"] * 1e3, "t_prefill_ms": st_["t_prefill"] * 1e3, "k": k_,
+             "sm_mhz": c_.get("sm_mhz"), "clock_reasons": c_.get("reasons")}
         r.update(tbt_stats(ts, k_))
         return r, st_
 

@@ -6,6 +6,8 @@ served by the library end to end on one B200: duet_sched_* forms every mixed ite
 chunked prefill, KV pages with look-ahead reservation, capacity admission), the policy picks the mode,
 duet_step runs it, duet_sched_commit advances the requests.  Policies:
   static    every iteration temporal (aggregated, one stream)
+  static_slo  temporal with the token budget cut until the predicted iteration meets tau (chunked
+            prefill at the SLO, the conventional alternative)
   adaptive  Alg. 1 (duet_choose_split against the calibrated tables; spatial with k look-ahead steps
             when t_mixed > tau)
 Simulated time advances by each iteration's measured GPU window.  Reports tokens/s, the inter-token gap
@@ -32,9 +34,11 @@ def main():
     ap.add_argument("--layers", type=int, default=8, help="Qwen2.5-14B slice depth")
     ap.add_argument("--tau", type=float, default=None, help="TBT SLO per iteration (s); default 100 ms x layers/48")
     ap.add_argument("--max-iters", type=int, default=300)
-    ap.add_argument("--policies", default="static,adaptive")
+    ap.add_argument("--policies", default="static,static_slo,adaptive")
     ap.add_argument("--seed", type=int, default=4795)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--calibration", default="corun", choices=["corun", "burst"],
+                    help="Pi_SM / B_HBM tables: under co-run at sustained clocks (bench default) or short bursts")
     ap.add_argument("--no-graph", action="store_true", help="decode steps launched eagerly (no CUDA graphs)")
     args = ap.parse_args()
     import numpy as np
@@ -66,11 +70,23 @@ def main():
     ctx = D.Ctx(spec, budget, max_seqs, max_batch, k_max, max_pages, max_pages * P + 16, D.DUET_DTYPE_BF16,
                 D.DUET_CTX_NO_GRAPH if args.no_graph else 0)
     parts, total = ctx.partitions()
-    fl, bw = ctx.calibrate(total)
+    fl, bw = ctx.calibrate(total) if args.calibration == "burst" else ctx.calibrate_corun(total, 0.12)
     hw = D.HwProfile(total, parts, fl, bw)
     results = {}
+    # static_slo: the conventional fix for TBT under chunked prefill — a temporal-only
+    # server whose token budget is cut to the largest power of two for which the predicted mixed
+    # iteration (that many prompt tokens at the trace's mean prompt length + a full decode batch at it)
+    # meets tau
+    mean_isl = int(np.mean([p for _, p, _, _ in trace]))
+    slo_budget = 256
+    for b_ in (8192, 4096, 2048, 1024, 512, 256):
+        b_batch = [(b_, mean_isl // 2, 1, 0)] + [(1, mean_isl, 2, 0)] * max_batch
+        if D.duet_predict_latency(spec, hw, b_batch, total, 0)["t_total"] <= tau:
+            slo_budget = b_
+            break
     for policy in args.policies.split(","):
-        sched = D.Sched(page_size=P, n_pages=n_pages, token_budget=budget, max_batch=max_batch,
+        sched = D.Sched(page_size=P, n_pages=n_pages, token_budget=slo_budget if policy == "static_slo" else budget,
+                        max_batch=max_batch,
                         max_prefill_seqs=max_seqs, k_max=k_max, max_pages_per_seq=max_pages)
         for r in trace:
             sched.add(*r)
@@ -93,7 +109,7 @@ def main():
                            table=np.ascontiguousarray(tab[:n_pre]), x=xbuf[:rows], y=ybuf[:rows])
             batch = [(q, c, 0 if c == 0 else 1, 0) for _, q, c in it["prefill"]] + \
                 [(1, c, 2, 0) for _, c in it["decode"]]
-            if policy == "static":
+            if policy in ("static", "static_slo"):
                 split = D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1)
             else:
                 split = D.duet_choose_split(spec, hw, batch, tau, k_max, 0)
@@ -126,9 +142,10 @@ def main():
             "iterations": iters, "tokens": tokens, "gpu_s": gpu_s, "tokens_per_s": tokens / max(gpu_s, 1e-9),
             "tbt_ms_p50": float(np.percentile(tb, 50) * 1e3), "tbt_ms_p90": float(np.percentile(tb, 90) * 1e3),
             "tbt_ms_p99": float(np.percentile(tb, 99) * 1e3), "slo_attainment": float(np.mean(tb <= tau)),
-            "modes": modes, "wall_s": time.perf_counter() - t_wall}
+            "modes": modes, "wall_s": time.perf_counter() - t_wall,
+            "token_budget": slo_budget if policy == "static_slo" else budget}
         print(policy, json.dumps(results[policy]), flush=True)
-    out = {"model": f"qwen2.5-14b x{m.n_layers} layers", "tau_ms": tau * 1e3, "n_req": args.n_req, "qps": args.qps,
+    out = {"model": f"qwen2.5-14b x{m.n_layers} layers", "tau_ms": tau * 1e3, "calibration": args.calibration, "n_req": args.n_req, "qps": args.qps,
            "trace": "lognormal ISL mean 12035 / OSL mean 343 (sigma 1), Gamma arrivals CV 2", "results": results}
     print(json.dumps(out))
     if args.out:
