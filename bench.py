@@ -405,7 +405,7 @@ def main():
     # ------------------------------------------------ kernel-class breakdown (untimed pass, every class)
     # Event records cost ~1 us each on the GPU; the headline timed region below times only the
     # dominant class (for the roofline), this short pass gives the per-class shares.
-    KCLASS = {"gemm": 0, "prefill_attn": 1, "decode_attn": 2, "other": 3}
+    KCLASS = {"gemm": 0, "prefill_attn": 1, "decode_attn": 2, "other": 3, "gemm_decode": 4, "other_decode": 5}
     n_break = min(args.steps, 10)
     ctx.profile_enable(True)
     for _ in range(n_break):
@@ -544,11 +544,14 @@ def main():
         clk_ = ClockSampler(lrank)   # each leg's own clocks: a power-capped leg is compared at its clock
         clk_.start()
         a.record(stream)
+        h_ = time.perf_counter()
         for _ in range(n):
             s_, k_ = one_step(split_fn(), chunk=chunk)
             tok += k_ * n_d + n_p_
+        h_ = (time.perf_counter() - h_) / n
         b.record(stream)
         torch.cuda.synchronize()
+        pg_ = ctx.last_step_times()["prefill_graph"]
         c_ = clk_.stop()
         ts = ctx.token_times(reset=True)
         sp_ = split_fn()
@@ -556,7 +559,8 @@ def main():
         k_ = sp_.k if sp_.mode == D.DUET_MODE_SPATIAL else 1
         r = {"tok_s": tok / (a.elapsed_time(b) * 1e-3), "window_ms": st_["t_window"] * 1e3,
              "t_decode_ms": st_["t_decode"] * 1e3, "t_prefill_ms": st_["t_prefill"] * 1e3, "k": k_,
-             "sm_mhz": c_.get("sm_mhz"), "clock_reasons": c_.get("reasons")}
+             "sm_mhz": c_.get("sm_mhz"), "clock_reasons": c_.get("reasons"),
+             "host_enqueue_ms": h_ * 1e3, "prefill_graph": bool(pg_)}
         r.update(tbt_stats(ts, k_))
         return r, st_
 
@@ -615,20 +619,20 @@ def main():
             D_b = [e for e in batch if e[2] == 2]
             for sd in parts:
                 td = D.duet_predict_latency(spec, hw, D_b, sd, opts & D.DUET_OPT_INCLUDE_CLS)["t_total"]
-                tp = D.duet_predict_latency(spec, hw, P_b, total - sd, opts & D.DUET_OPT_INCLUDE_CLS)["t_total"]
-                r_ = int(np.floor(tp / td))
+                tpp = D.duet_predict_latency(spec, hw, P_b, total - sd, opts & D.DUET_OPT_INCLUDE_CLS)["t_total"]
+                r_ = int(np.floor(tpp / td))
                 ks = [min(max(x, 1), 8) for x in (r_, r_ + 1)]
-                rhos = [(kk * len(D_b) + sum(e[0] for e in P_b)) / max(kk * td, tp) for kk in ks]
+                rhos = [(kk * len(D_b) + sum(e[0] for e in P_b)) / max(kk * td, tpp) for kk in ks]
                 kk = ks[int(np.argmax(rhos))]
-                sp_ = D.split_struct(1, total - sd, sd, kk, 0, split.t_mixed, tp, td, max(rhos))
+                sp_ = D.split_struct(1, total - sd, sd, kk, 0, split.t_mixed, tpp, td, max(rhos))
                 r, st_ = timed(lambda: sp_, n=4)
-                r.update({"s_d": sd, "s_p": total - sd, "t_pred_d_ms": td * 1e3, "t_pred_p_ms": tp * 1e3,
-                          "t_pred_window_ms": max(kk * td, tp) * 1e3, "predicted_tok_s": max(rhos),
+                r.update({"s_d": sd, "s_p": total - sd, "t_pred_d_ms": td * 1e3, "t_pred_p_ms": tpp * 1e3,
+                          "t_pred_window_ms": max(kk * td, tpp) * 1e3, "predicted_tok_s": max(rhos),
                           "optimizer_pick": sd == forced.s_d, "meets_slo_pred": td <= tau,
                           "meets_slo_meas": (r.get("tbt_max_ms") or 1e9) <= tau * 1e3})
                 rows.append(r)
                 log(f"sweep S_d={sd}: k={kk} {r['tok_s']:.0f} tok/s window {r['window_ms']:.2f} ms "
-                    f"(pred {max(kk * td, tp) * 1e3:.2f}) TBT max {r.get('tbt_max_ms', 0):.2f} ms")
+                    f"(pred {max(kk * td, tpp) * 1e3:.2f}) TBT max {r.get('tbt_max_ms', 0):.2f} ms")
             comp["sweep"] = rows
 
     log("e2e")
@@ -746,7 +750,13 @@ def main():
     # ------------------------------------------------ roofline of the dominant kernel class
     pk, pk_src = peaks()
     st_ = kstats[dom]
-    tensor_bound = dom in ("gemm", "prefill_attn")
+    tensor_bound = dom in ("gemm", "prefill_attn", "gemm_decode")
+    # the SMs the dominant class ran on: a spatial step's decode side (decode attention, *_decode) on S_d,
+    # its prefill side on S_p, a temporal step on the whole device
+    if split.mode == D.DUET_MODE_SPATIAL:
+        dom_sms = split.s_d if dom in ("decode_attn", "gemm_decode", "other_decode") else split.s_p
+    else:
+        dom_sms = total
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -763,11 +773,18 @@ def main():
                     "avg_launch_us": st_["seconds"] / st_["launches"] * 1e6,
                     "peak_source": pk_src + (" sustained bf16 (timed region %.1f s)" % (t_ms / 1e3) if sustained
                                              else " burst bf16")}
+            roof["partition"] = {"sms": dom_sms, "peak": peak * dom_sms / total, "frac": ach / (peak * dom_sms / total),
+                                 "note": "the measured peak scaled to the SMs the kernel ran on"}
         else:
             ach = st_["bytes"] / st_["seconds"] / 1e9
             peak = float(pk["hbm_gbs"])
             roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                    "traffic": traffic, "kernel": dom, "launches": st_["launches"], "peak_source": pk_src}
+                    "traffic": traffic, "kernel": dom, "launches": st_["launches"],
+                    "avg_launch_us": st_["seconds"] / st_["launches"] * 1e6, "peak_source": pk_src}
+            if dom_sms < total and stream_bw is not None and stream_bw[dom_sms] > 0:
+                roof["partition"] = {"sms": dom_sms, "peak": stream_bw[dom_sms] / 1e9,
+                                     "frac": ach * 1e9 / stream_bw[dom_sms],
+                                     "note": "LDG stream ceiling on the kernel's S_d-SM partition (duet_calibrate_stream)"}
     else:
         roof = {"bound": "tensor", "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None,
                 "kernel": dom}

@@ -161,9 +161,15 @@ enum {
   DUET_CTX_FINE_SPLIT = 1u,  /* 2-SM (TPC) partitions: CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING;
                                 default is the driver's 8-SM granularity (cuda.h green contexts) */
   DUET_CTX_NO_GRAPH = 2u,    /* launch decode kernels directly instead of replaying a CUDA graph */
-  DUET_CTX_NO_CORUN = 4u     /* temporal steps never co-run the prefill and decode attentions on an SM
+  DUET_CTX_NO_CORUN = 4u,    /* temporal steps never co-run the prefill and decode attentions on an SM
                                 split (f4; by default a measured-rate model decides per step, and the
                                 environment variable DUET_CORUN=<S_d> / 0 forces / disables it) */
+  DUET_CTX_NO_PREFILL_GRAPH = 8u /* spatial steps launch the prefill side's kernels one by one.  By default
+                                the second spatial step with the same prefill shape (rows, sequences,
+                                longest chunk, longest context, partition, buffers) captures the side's
+                                L layers into a CUDA graph and later steps of that shape replay it
+                                (prefill dispatch costs host time per kernel); at most 8 such
+                                graphs are kept (LRU).  Never while live kernel timing is enabled. */
 };
 
 /* Capacity the workspace is sized for.  max_pos bounds every absolute token position
@@ -345,7 +351,11 @@ duet_status duet_step(duet_ctx* ctx, const duet_layer_weights* w, const duet_pre
  * Times in seconds: t_window = first launch -> join; t_decode = decode side (k steps);
  * t_prefill = prefill side.  Temporal: t_window = t_decode = t_prefill.  corun_s_d: SMs of the
  * decode group the two attentions of a temporal step co-ran on (f4; 0 = one after the other). */
-typedef struct { double t_window, t_decode, t_prefill; int32_t mode, k, kernels, corun_s_d; } duet_step_times;
+typedef struct {
+  double t_window, t_decode, t_prefill;
+  int32_t mode, k, kernels, corun_s_d;
+  int32_t prefill_graph; /* spatial: 1 if the prefill side replayed a captured graph (DUET_CTX_NO_PREFILL_GRAPH) */
+} duet_step_times;
 duet_status duet_last_step_times(duet_ctx* ctx, duet_step_times* out);
 
 /* Measures Pi_SM(S) and B_HBM(S) for S = every partition size the ctx can provision (both
@@ -378,17 +388,20 @@ duet_status duet_calibrate_corun(duet_ctx* ctx, double* flops_at_sms, double* bw
 duet_status duet_calibrate_stream(duet_ctx* ctx, double* bw_stream, int32_t len);
 
 /* Live kernel timing (measurement, §8(d)): while enabled, duet_step records CUDA events on the
- * launching stream around every kernel it launches outside CUDA graphs (the prefill side of a
- * spatial step and every kernel of a temporal step), per kernel class, together with the
+ * launching stream around every kernel it launches, per kernel class, together with the
  * algorithmic FLOPs and bytes of each launch (causal attention FLOPs,
  * weights/activations read once).  duet_profile_enable(ctx, mask) resets the counters and times the
  * classes whose bit (1 << DUET_KCLASS_*) is set in mask (0 = off; DUET_PROFILE_ALL = every class);
  * each timed launch costs two event records on its stream (~1 us), so a timed region usually enables
  * only the class it reports.  duet_profile_read synchronizes on the recorded events and returns
  * DUET_KCLASS_N entries. */
+/* GEMM / OTHER count the prefill side of a spatial step and every kernel of a temporal step;
+ * GEMM_DECODE / OTHER_DECODE the decode side of a spatial step.  Timed kernels are never inside a
+ * CUDA graph: while a class of a side is enabled, that side launches its kernels one by one instead
+ * of replaying its graph (decode: DECODE_ATTN, GEMM_DECODE, OTHER_DECODE; prefill: the others). */
 enum { DUET_KCLASS_GEMM = 0, DUET_KCLASS_PREFILL_ATTN = 1, DUET_KCLASS_DECODE_ATTN = 2, DUET_KCLASS_OTHER = 3,
-       DUET_KCLASS_N = 4 };
-#define DUET_PROFILE_ALL 0xF
+       DUET_KCLASS_GEMM_DECODE = 4, DUET_KCLASS_OTHER_DECODE = 5, DUET_KCLASS_N = 6 };
+#define DUET_PROFILE_ALL 0x3F
 typedef struct { int32_t launches; double seconds, flops, bytes; } duet_kernel_stats;
 duet_status duet_profile_enable(duet_ctx* ctx, int32_t class_mask);
 duet_status duet_profile_read(duet_ctx* ctx, duet_kernel_stats* out);

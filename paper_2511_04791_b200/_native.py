@@ -15,7 +15,7 @@ DUET_OPT_FORCE_SPATIAL, DUET_OPT_INCLUDE_CLS, DUET_OPT_VERBATIM_INFEASIBLE, DUET
 DUET_MODE_TEMPORAL, DUET_MODE_SPATIAL = 0, 1
 DUET_FLAG_INFEASIBLE, DUET_FLAG_DEGENERATE = 1, 2
 DUET_DTYPE_BF16, DUET_DTYPE_FP32 = 0, 1
-DUET_CTX_FINE_SPLIT, DUET_CTX_NO_GRAPH, DUET_CTX_NO_CORUN = 1, 2, 4
+DUET_CTX_FINE_SPLIT, DUET_CTX_NO_GRAPH, DUET_CTX_NO_CORUN, DUET_CTX_NO_PREFILL_GRAPH = 1, 2, 4, 8
 DUET_EPI_STORE, DUET_EPI_RESIDUAL, DUET_EPI_SWIGLU = 0, 1, 2
 STATUS_NAMES = {0: "OK", -1: "INVALID_ARG", -2: "OUT_OF_RANGE", -3: "CONFIG", -4: "UNSUPPORTED", -5: "CUDA",
                 -6: "CAPACITY", -7: "NCCL"}
@@ -81,8 +81,8 @@ class duet_kv_pages(C.Structure):
                 ("page_size", C.c_int32)]
 
 
-DUET_KCLASS_N = 4
-DUET_PROFILE_ALL = 0xF
+DUET_KCLASS_N = 6
+DUET_PROFILE_ALL = 0x3F
 
 
 class duet_corun_profile(C.Structure):
@@ -98,7 +98,7 @@ class duet_kernel_stats(C.Structure):
 class duet_step_times(C.Structure):
     _fields_ = [("t_window", C.c_double), ("t_decode", C.c_double), ("t_prefill", C.c_double),
                 ("mode", C.c_int32), ("k", C.c_int32), ("kernels", C.c_int32),
-                ("corun_s_d", C.c_int32)]
+                ("corun_s_d", C.c_int32), ("prefill_graph", C.c_int32)]
 
 
 _lib = None
@@ -399,7 +399,7 @@ class Ctx:
     def profile_read(self) -> dict:
         arr = (duet_kernel_stats * DUET_KCLASS_N)()
         _check(lib().duet_profile_read(self.h, arr))
-        names = ("gemm", "prefill_attn", "decode_attn", "other")
+        names = ("gemm", "prefill_attn", "decode_attn", "other", "gemm_decode", "other_decode")
         return {names[i]: {n: getattr(arr[i], n) for n, _ in duet_kernel_stats._fields_} for i in range(DUET_KCLASS_N)}
 
     def set_comms(self, rank: int, id_decode: bytes, id_prefill: bytes):

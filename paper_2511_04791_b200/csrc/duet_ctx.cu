@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <array>
 #include <map>
 #include <tuple>
 #include <vector>
@@ -169,6 +170,10 @@ struct GraphEntry {
 // decode graphs kept per ctx (key: partition, batch size, layers, pointer hash, context bucket); the
 // least recently used one is destroyed beyond this many (a serving loop changes the batch size often)
 constexpr size_t kGraphCap = 48;
+// prefill-side graphs (f4): one per repeated prefill shape; captured on a shape's second
+// occurrence (a serving loop's one-off chunk shapes would pay the capture for nothing)
+constexpr size_t kPreGraphCap = 8;
+using PreKey = std::array<uint64_t, 6>;
 
 }  // namespace
 
@@ -204,12 +209,16 @@ struct duet_ctx {
   std::vector<uint32_t> page_mark;
   uint32_t page_gen = 0;
   std::map<std::tuple<int, int, int, uint64_t>, GraphEntry> graphs;
+  std::map<PreKey, GraphEntry> pre_graphs;
+  std::map<PreKey, int> pre_seen;
   uint64_t graph_clock = 0;
   // last step
   int last_mode = -1, last_k = 0, last_kernels = 0, last_corun = 0;
+  bool last_pre_graph = false;  // the last spatial step's prefill side replayed a graph
   bool last_has_dec = false, last_has_pre = false;
   // live kernel timing
   bool prof_on = false, capturing = false;
+  bool prof_dec_side = false;  // launches being made belong to a spatial step's decode side
   int prof_mask = 0;
   struct ProfRec {
     int cls, idx;
@@ -228,7 +237,13 @@ struct duet_ctx {
 
 static duet_status comms_healthy(duet_ctx* c);
 
+// decode-side launches of a spatial step are counted in the *_DECODE classes
+static int side_class(duet_ctx* c, int cls) {
+  if (!c->prof_dec_side) return cls;
+  return cls == DUET_KCLASS_GEMM ? DUET_KCLASS_GEMM_DECODE : cls == DUET_KCLASS_OTHER ? DUET_KCLASS_OTHER_DECODE : cls;
+}
 static int prof_begin(duet_ctx* c, cudaStream_t st, int cls) {
+  cls = side_class(c, cls);
   if (!c->prof_on || c->capturing || !(c->prof_mask & (1 << cls))) return -1;
   if (c->prof_used == c->prof_pool.size()) {
     cudaEvent_t a, b;
@@ -241,6 +256,7 @@ static int prof_begin(duet_ctx* c, cudaStream_t st, int cls) {
 }
 static void prof_end(duet_ctx* c, cudaStream_t st, int idx, int cls, double flops, double bytes) {
   if (idx < 0) return;
+  cls = side_class(c, cls);
   cudaEventRecord(c->prof_pool[idx].second, st);
   c->prof_pending.push_back({cls, idx, flops, bytes});
 }
@@ -762,6 +778,8 @@ extern "C" duet_status duet_ctx_destroy(duet_ctx* c) {
   cudaDeviceSynchronize();
   for (auto& kv : c->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  for (auto& kv : c->pre_graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   for (auto& p : c->parts) {
     if (!p.created) continue;
     DRV.StreamDestroy((CUstream)p.s_dec);
@@ -1052,6 +1070,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
   c->last_has_pre = has_pre;
   c->last_mode = split->mode;
   c->last_k = k;
+  c->last_pre_graph = false;
 
   if (!spatial) {
     // ---------------- temporal (aggregated) mode: one full-device stream, k = 1
@@ -1156,9 +1175,19 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     int max_c = 0;
     for (int r = 0; r < n; ++r) max_c = std::max(max_c, dec->c[r]);
     const int max_len = ((max_c + k + 1023) / 1024) * 1024;  // bucket: graphs survive context growth
-    if (c->lim.flags & DUET_CTX_NO_GRAPH) {
-      for (int j = 0; j < k; ++j)
-        DUET_TRY(decode_step_kernels(c, st, P->s_d, w, kv, ap, max_len, dec->y, dec->head, &kernels));
+    constexpr int kDecClasses = (1 << DUET_KCLASS_DECODE_ATTN) | (1 << DUET_KCLASS_GEMM_DECODE) |
+                                (1 << DUET_KCLASS_OTHER_DECODE);
+    const bool timed_dec = c->prof_on && (c->prof_mask & kDecClasses);
+    if ((c->lim.flags & DUET_CTX_NO_GRAPH) || timed_dec) {
+      c->prof_dec_side = true;
+      for (int j = 0; j < k; ++j) {
+        const duet_status sd = decode_step_kernels(c, st, P->s_d, w, kv, ap, max_len, dec->y, dec->head, &kernels);
+        if (sd != DUET_OK) {
+          c->prof_dec_side = false;
+          return sd;
+        }
+      }
+      c->prof_dec_side = false;
     } else {
       auto key = std::make_tuple(P->s_d, n, c->spec.n_layers, hash_ptrs(w, c->spec.n_layers, kv, dec->y, max_len,
                                                                       dec->head));
@@ -1205,7 +1234,57 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in, 0));
     CUDA_TRY(cudaEventRecord(c->ev_pre0, st));
     DUET_TRY(upload_meta(c, c->pre, img, slot, n_int, P->s_p, st, &kernels));
-    DUET_TRY(run_layers(c, c->pre, st, P->s_p, ap.n_pre, pre->x, pre->y, w, kv, ap, &kernels));
+    // the prefill side's L layers as one graph launch (f4): the kernels read the chunk's positions
+    // and page tables from the metadata just uploaded, so a graph serves every batch of the same shape
+    // (rows, sequences, longest chunk and context) and buffers; live kernel timing needs direct launches
+    constexpr int kPreClasses = (1 << DUET_KCLASS_GEMM) | (1 << DUET_KCLASS_PREFILL_ATTN) | (1 << DUET_KCLASS_OTHER);
+    const bool pre_graph = !(c->lim.flags & (DUET_CTX_NO_GRAPH | DUET_CTX_NO_PREFILL_GRAPH)) &&
+                           !(c->prof_on && (c->prof_mask & kPreClasses));
+    GraphEntry* ge = nullptr;
+    if (pre_graph) {
+      const PreKey key{(uint64_t)P->s_d, (uint64_t)ap.n_pre, (uint64_t)ap.n_seqs, (uint64_t)ap.max_q,
+                       (uint64_t)ap.max_len_pre,
+                       hash_ptrs(w, c->spec.n_layers, kv, pre->y, 0) ^ ((uint64_t)(uintptr_t)pre->x * 0x9E3779B97F4A7C15ull)};
+      auto it = c->pre_graphs.find(key);
+      if (it == c->pre_graphs.end()) {
+        if (c->pre_seen.size() > 4096) c->pre_seen.clear();
+        if (++c->pre_seen[key] >= 2) {
+          cudaGraph_t graph;
+          int nk = 0;
+          CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          c->capturing = true;
+          duet_status sc = run_layers(c, c->pre, st, P->s_p, ap.n_pre, pre->x, pre->y, w, kv, ap, &nk);
+          c->capturing = false;
+          cudaError_t e = cudaStreamEndCapture(st, &graph);
+          if (sc != DUET_OK) return sc;
+          if (e != cudaSuccess) DUET_FAIL(DUET_ERR_CUDA, "prefill graph capture failed: %s", cudaGetErrorString(e));
+          GraphEntry g;
+          g.kernels = nk;
+          e = cudaGraphInstantiate(&g.exec, graph, 0);
+          cudaGraphDestroy(graph);
+          if (e != cudaSuccess) DUET_FAIL(DUET_ERR_CUDA, "prefill graph instantiate failed: %s", cudaGetErrorString(e));
+          if (c->pre_graphs.size() >= kPreGraphCap) {  // evict the least recently used one
+            auto lru = c->pre_graphs.begin();
+            for (auto q = c->pre_graphs.begin(); q != c->pre_graphs.end(); ++q)
+              if (q->second.last_use < lru->second.last_use) lru = q;
+            CUDA_TRY(cudaDeviceSynchronize());  // its last replay may still be queued on some partition
+            cudaGraphExecDestroy(lru->second.exec);
+            c->pre_graphs.erase(lru);
+          }
+          c->pre_seen.erase(key);
+          it = c->pre_graphs.emplace(key, g).first;
+        }
+      }
+      if (it != c->pre_graphs.end()) ge = &it->second;
+    }
+    if (ge) {
+      ge->last_use = ++c->graph_clock;
+      CUDA_TRY(cudaGraphLaunch(ge->exec, st));
+      kernels += ge->kernels;
+    } else {
+      DUET_TRY(run_layers(c, c->pre, st, P->s_p, ap.n_pre, pre->x, pre->y, w, kv, ap, &kernels));
+    }
+    c->last_pre_graph = ge != nullptr;
     CUDA_TRY(cudaEventRecord(c->ev_pre1, st));
   }
   // join (a7): the caller's stream waits for both sides; no host sync
@@ -1224,6 +1303,7 @@ extern "C" duet_status duet_last_step_times(duet_ctx* c, duet_step_times* out) {
   out->k = c->last_k;
   out->kernels = c->last_kernels;
   out->corun_s_d = c->last_mode == DUET_MODE_TEMPORAL ? c->last_corun : 0;
+  out->prefill_graph = c->last_mode == DUET_MODE_SPATIAL && c->last_pre_graph ? 1 : 0;
   float ms = 0;
   if (c->last_mode == DUET_MODE_TEMPORAL) {
     CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_pre0, c->ev_pre1));
@@ -1287,7 +1367,13 @@ extern "C" duet_status duet_ctx_set_comms(duet_ctx* c, int32_t rank, const void*
   NCCL_TRY(NCCL.CommInitRankConfig(&c->comm_dec, c->spec.tp, a, rank, &cfg_dec));
   NCCL_TRY(NCCL.CommInitRankConfig(&c->comm_pre, c->spec.tp, b, rank, &cfg_pre));
   c->tp_rank = rank;
-  c->graphs.clear();  // captured decode graphs predate the communicators
+  cudaDeviceSynchronize();  // captured graphs predate the communicators: drop them
+  for (auto& kv : c->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  for (auto& kv : c->pre_graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  c->graphs.clear();
+  c->pre_graphs.clear();
   return DUET_OK;
 }
 

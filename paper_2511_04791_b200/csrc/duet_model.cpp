@@ -188,7 +188,7 @@ duet_status check_profile(const duet_hw_profile* hw) {
 using namespace duet;
 
 extern "C" const char* duet_last_error(void) { return duet::last_error(); }
-extern "C" int32_t duet_abi_version(void) { return 3; }
+extern "C" int32_t duet_abi_version(void) { return 4; }
 
 extern "C" duet_status duet_predict_latency(const duet_model_spec* spec, const duet_hw_profile* hw,
                                             const duet_req* batch, int32_t n, int32_t sms, uint32_t opts,

@@ -7,7 +7,9 @@
   the exact launches duet_step makes): 64 decodes at c = 4096 (split-K + LSE combine) and a q = 2048
   chunk over a 1000-token prefix, every output element of every head compared with the oracle's
   plain softmax (readings #2, #6, #7), on the full device and on a partition;
-* the token-time ring (TBT per decode step).
+* the token-time ring (TBT per decode step);
+* the graph-captured prefill side (f4): direct launch, capture and replay of a 2-layer
+  spatial step, the replay on a new prompt in the same buffers — each against the oracle.
 
 The oracle's K/V for a sampled request are generated on the host from the same counter streams as the
 device pools (synth, exact grid values) — never read back from the GPU.
@@ -18,7 +20,9 @@ import torch
 
 import paper_2511_04791_b200 as D
 from oracle import layer as OL
-from synth import configs, counter_values, counter_values_torch, head_weights, page_tables, workload
+from dataclasses import replace as dc_replace
+
+from synth import S_XPRE, configs, counter_values, counter_values_torch, head_weights, page_tables, workload, x_rows
 from tests.gpu_helpers import GpuWorkload, make_ctx
 from tests.oracle_run import make_kv, rel_err, run
 from tests.test_gpu_parity import TOL, _check_kv, _check_outputs
@@ -249,4 +253,51 @@ def test_token_times_per_decode_step():
     assert len(ts) == 3 + 3 + 1
     assert all(b >= a for a, b in zip(ts, ts[1:]))
     assert ctx.token_times() == []
+    ctx.close()
+
+
+# ------------------------------------------------------------------ graph-captured prefill side
+
+@pytest.mark.parametrize("cfg_name", ["cfg1-bf16", "cfg2-mini"])
+def test_prefill_graph_capture_and_replay(cfg_name):
+    """Spatial steps of one shape: the first launches the prefill side kernel by kernel, the second
+    captures its L layers into a graph, the third replays that graph on a different prompt written into
+    the same input buffer (the kernels read positions and page tables from the step's metadata).
+    Every step against the oracle, and the capture bitwise equal to the direct launch."""
+    cfg = configs.get_config(cfg_name)
+    wl = workload.build(cfg, k=2, n_layers=2)
+    tol = TOL[cfg.dtype]
+    y_pre_a, y_dec_a, kv_a = run(wl)
+    n_p = sum(q for q, _ in wl.pre_seqs)
+    wl_b = dc_replace(wl, x_pre=x_rows(cfg.seed + 17, S_XPRE, n_p, wl.cfg.model.d_model))
+    y_pre_b, y_dec_b, kv_b = run(wl_b)
+    assert rel_err(y_pre_b, y_pre_a) > 10 * tol          # the second prompt really differs
+    g = GpuWorkload(wl, cfg.dtype)
+    ctx = make_ctx(wl, cfg.dtype)
+    parts, total = ctx.partitions()
+    s_d = parts[len(parts) // 2]
+    split = D.split_struct(D.DUET_MODE_SPATIAL, total - s_d, s_d, 2)
+    outs = []
+    for step in range(3):
+        if step == 2:
+            g.x_pre.copy_(torch.from_numpy(wl_b.x_pre).to(device=g.x_pre.device, dtype=g.x_pre.dtype))
+        g.y_pre.zero_()
+        g.step(ctx, split)
+        torch.cuda.synchronize()
+        t = ctx.last_step_times()
+        assert t["prefill_graph"] == (1 if step > 0 else 0), (step, t)
+        if step < 2:
+            _check_outputs(g, y_pre_a, y_dec_a, tol)
+        else:
+            _check_outputs(g, y_pre_b, y_dec_b, tol)
+            _check_kv(g, kv_b, tol)
+        outs.append(g.y_pre.clone())
+    assert torch.equal(outs[0], outs[1])                  # the captured graph = the direct launches
+    # a ctx created with DUET_CTX_NO_PREFILL_GRAPH never captures
+    ctx.close()
+    ctx = make_ctx(wl, cfg.dtype, D.DUET_CTX_NO_PREFILL_GRAPH)
+    for _ in range(2):
+        g.step(ctx, split)
+        torch.cuda.synchronize()
+        assert ctx.last_step_times()["prefill_graph"] == 0
     ctx.close()

@@ -21,7 +21,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     for name in sorted(declared):
         assert hasattr(lib, name), name
     assert set(D.EXPORTED) == declared
-    assert lib.duet_abi_version() == 3
+    assert lib.duet_abi_version() == 4
 
 
 def _spec_pair(rnd):
