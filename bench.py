@@ -340,7 +340,7 @@ def main():
     elif args.calibration == "burst":
         fl, bw = ctx.calibrate(total)
     else:   # the rates each side achieves next to the other side's work, at sustained clocks (reading R-f)
-        fl, bw = ctx.calibrate_corun(total, 0.12)
+        fl, bw = ctx.calibrate_corun(total, 0.2)
     t_cal = time.perf_counter() - t0
     # the hardware read-stream ceiling per partition size (decode-side roofline denominator), before the
     # KV pools take the memory

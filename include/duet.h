@@ -374,11 +374,20 @@ duet_status duet_calibrate(duet_ctx* ctx, double* flops_at_sms, double* bw_at_sm
  * cap), every split (S_d, S_p) runs two phases of ~pair_seconds each — the calibration GEMM on S_p while
  * the paged decode attention streams on S_d (-> flops_at_sms[S_p], bw_at_sms[S_d]), then the roles
  * swapped (-> flops_at_sms[S_d], bw_at_sms[S_p]); the full device runs each kernel alone, sustained.
- * Rates over the middle 60 % of each side's launches.  Falls back to duet_calibrate's tables where a
+ * Rates over launches 40-90 % of each side's loop, then smoothed over the measured sizes
+ * (duet_profile_smooth).  Falls back to duet_calibrate's tables where a
  * size was not measured this way (fp32 contexts).  ~2 * n_partitions * pair_seconds + ~1.5 s.
  * Errors: as duet_calibrate, INVALID_ARG for pair_seconds <= 0. */
 duet_status duet_calibrate_corun(duet_ctx* ctx, double* flops_at_sms, double* bw_at_sms, int32_t len,
                                  double pair_seconds);
+
+/* Smooths one calibration table in place (reading R-g; duet_calibrate_corun applies it to both of its
+ * tables over the sizes it measured): at the measured sizes (strictly ascending, 0 < size < len) the
+ * per-SM rate rate[S]/S of every interior size becomes the median of its own and its two neighbours'
+ * per-SM rates; the end points are kept.  Monotone runs of per-SM rates are left unchanged; one
+ * outlying measurement (a 0.1-s phase on a power-capped GPU) is replaced.  Host-only.
+ * Errors: INVALID_ARG (NULL, n < 0), OUT_OF_RANGE (sizes), CONFIG (a rate <= 0). */
+duet_status duet_profile_smooth(const int32_t* sizes, int32_t n, double* rate_at_sms, int32_t len);
 
 /* The hardware read-stream ceiling per partition size — the roofline denominator of a decode
  * partition, SURVEY §8(d) (not a predictor input): plain 16-byte LDG streaming of a >= 256 MiB buffer

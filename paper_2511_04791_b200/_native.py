@@ -140,6 +140,7 @@ _SIGS = {
     "duet_op_prefill_attn": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
                                        C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32,
                                        C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "duet_profile_smooth": (C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_double), C.c_int32]),
     "duet_corun_choose": (C.c_int, [C.POINTER(duet_corun_profile), C.c_double, C.c_double, C.POINTER(C.c_int32),
                                     C.POINTER(C.c_double)]),
     "duet_calibrate_corun": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32,
@@ -217,6 +218,15 @@ def duet_choose_split(spec: duet_model_spec, hw: HwProfile, batch, tbt_slo_s: fl
     _check(lib().duet_choose_split(C.byref(spec), C.byref(hw.struct), _reqs(batch), len(batch), float(tbt_slo_s),
                                    int(k_max), int(opts), C.byref(out)))
     return out
+
+
+def duet_profile_smooth(sizes, table):
+    """Median-of-three smoothing of per-SM rates over the measured sizes (duet_profile_smooth); returns
+    a new list."""
+    s = (C.c_int32 * max(1, len(sizes)))(*sizes)
+    t = (C.c_double * len(table))(*table)
+    _check(lib().duet_profile_smooth(s, len(sizes), t, len(table)))
+    return list(t)
 
 
 def duet_corun_choose(total_sms, cand_sd_sms, fa_flops_at_sms, dec_bw_at_sms, attn_flops_pre, attn_bytes_dec,

@@ -1791,9 +1791,13 @@ static duet_status calibrate_impl(duet_ctx* c, double* flops, double* bw, int32_
     GemmArgs g{A, B, C, nullptr, nullptr, GM, GN, GK, GK, GK, GN, 0, EPI_STORE};
     cudaEvent_t ev[4];
     for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
-    // n launches of one kernel on st; events after launch n/5 and before launch n - n/5
+    // n launches of one kernel on st; events after launch 2n/5 and before launch n - n/10: the first
+    // 40 % let the clocks settle to the pair's power state (the previous phase ran another mix), the
+    // last 10 % may run after the other side's loop has ended
+    auto lo_of = [](int n) { return 2 * n / 5; };
+    auto hi_of = [](int n) { return n - n / 10; };
     auto loop = [&](cudaStream_t st, int sms, bool gemm, int n, cudaEvent_t ea, cudaEvent_t eb) -> duet_status {
-      const int lo = n / 5, hi = n - n / 5;
+      const int lo = lo_of(n), hi = hi_of(n);
       for (int i = 0; i < n; ++i) {
         if (i == lo) CUDA_TRY(cudaEventRecord(ea, st));
         if (i == hi) CUDA_TRY(cudaEventRecord(eb, st));
@@ -1826,8 +1830,8 @@ static duet_status calibrate_impl(duet_ctx* c, double* flops, double* bw, int32_
         DUET_TRY(loop(sta, sa, false, na, ev[2], ev[3]));
         CUDA_TRY(cudaStreamSynchronize(stg));
         CUDA_TRY(cudaStreamSynchronize(sta));
-        mf_c[sg] = g_flops * (ng - 2 * (ng / 5)) / elapsed(ev[0], ev[1]);
-        mb_c[sa] = attn_bytes * (na - 2 * (na / 5)) / elapsed(ev[2], ev[3]);
+        mf_c[sg] = g_flops * (hi_of(ng) - lo_of(ng)) / elapsed(ev[0], ev[1]);
+        mb_c[sa] = attn_bytes * (hi_of(na) - lo_of(na)) / elapsed(ev[2], ev[3]);
       }
     }
     {  // the full device, each kernel alone, sustained
@@ -1835,11 +1839,18 @@ static duet_status calibrate_impl(duet_ctx* c, double* flops, double* bw, int32_
       DUET_TRY(loop(c->s_full, S, true, ng, ev[0], ev[1]));
       DUET_TRY(loop(c->s_full, S, false, na, ev[2], ev[3]));
       CUDA_TRY(cudaStreamSynchronize(c->s_full));
-      mf_c[S] = g_flops * (ng - 2 * (ng / 5)) / elapsed(ev[0], ev[1]);
-      mb_c[S] = attn_bytes * (na - 2 * (na / 5)) / elapsed(ev[2], ev[3]);
+      mf_c[S] = g_flops * (hi_of(ng) - lo_of(ng)) / elapsed(ev[0], ev[1]);
+      mb_c[S] = attn_bytes * (hi_of(na) - lo_of(na)) / elapsed(ev[2], ev[3]);
     }
     DUET_TRY(check_launch("co-run calibration"));
     for (auto e : ev) cudaEventDestroy(e);
+    // reading R-g: one 0.1-s phase on a power-capped GPU varies by +-10 %; a median of three over the
+    // per-SM rates of neighbouring sizes removes a lone outlier (which would mislead Alg. 1's k)
+    std::vector<int32_t> sizes;
+    for (int s = 1; s <= S; ++s)
+      if (mf_c[s] > 0 && mb_c[s] > 0) sizes.push_back(s);
+    DUET_TRY(duet_profile_smooth(sizes.data(), (int32_t)sizes.size(), mf_c.data(), S + 1));
+    DUET_TRY(duet_profile_smooth(sizes.data(), (int32_t)sizes.size(), mb_c.data(), S + 1));
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

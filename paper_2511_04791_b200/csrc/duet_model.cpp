@@ -5,6 +5,7 @@
 // expression rounds exactly as written; F and B are exact int64 (< 2^53 at every config,
 // so the conversion to double is exact).  The evaluation order is the canonical one of
 // DESIGN.md §Predictor; results are bit-identical to the CPU oracle.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -367,5 +368,31 @@ extern "C" duet_status duet_corun_choose(const duet_corun_profile* p, double att
   }
   *s_d_out = best;
   if (t_out) *t_out = best ? best_t : t_seq;
+  return DUET_OK;
+}
+
+// Calibration-table smoothing (reading R-g): the per-SM rate r(S) = rate[S] / S at the measured sizes
+// (ascending) is replaced, at every interior size, by the median of its own value and its two
+// neighbours'; end points are kept.  A median of three leaves any monotone run of per-SM rates
+// unchanged (Pi_SM per SM is ~flat; B_HBM per SM falls as the partition saturates HBM) and
+// removes a single outlying measurement.
+extern "C" duet_status duet_profile_smooth(const int32_t* sizes, int32_t n, double* rate_at_sms, int32_t len) {
+  duet::clear_error();
+  if (n < 0 || (n > 0 && (!sizes || !rate_at_sms))) DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL argument / n = %d", n);
+  for (int32_t i = 0; i < n; ++i) {
+    if (sizes[i] <= 0 || sizes[i] >= len) DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "size %d outside the table", sizes[i]);
+    if (i > 0 && sizes[i] <= sizes[i - 1]) DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "sizes must be strictly ascending");
+    if (!(rate_at_sms[sizes[i]] > 0)) DUET_FAIL(DUET_ERR_CONFIG, "rate at %d SMs must be > 0", sizes[i]);
+  }
+  if (n < 3) return DUET_OK;
+  std::vector<double> r(n), out(n);
+  for (int32_t i = 0; i < n; ++i) r[i] = rate_at_sms[sizes[i]] / (double)sizes[i];
+  out[0] = r[0];
+  out[n - 1] = r[n - 1];
+  for (int32_t i = 1; i + 1 < n; ++i) {
+    double a = r[i - 1], b = r[i], c = r[i + 1];
+    out[i] = std::max(std::min(a, b), std::min(std::max(a, b), c));  // median of three
+  }
+  for (int32_t i = 0; i < n; ++i) rate_at_sms[sizes[i]] = out[i] * (double)sizes[i];
   return DUET_OK;
 }

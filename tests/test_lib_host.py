@@ -186,3 +186,27 @@ def test_corun_choose_host_logic():
     # balanced large attentions (cfg2-like: 34 GFLOP causal, 1.07 GB of KV): co-run on a split
     sd, t = D.duet_corun_choose(S, cand, fa, bw, 34.4e9, 1.07e9)
     assert 16 <= sd <= 132 and t < 34.4e9 / fa[S] + 1.07e9 / bw[S]
+
+
+def test_profile_smooth_median_of_three():
+    """duet_profile_smooth (reading R-g): a lone outlier among the per-SM rates is replaced by the median
+    of its neighbourhood, monotone runs and the end points are untouched, bad input is rejected."""
+    sizes = [8, 16, 24, 32, 40, 148]
+    per_sm = [10.0, 9.5, 9.0, 6.0, 8.5, 8.0]          # 32 SMs: one low outlier
+    table = [0.0] * 149
+    for s, r in zip(sizes, per_sm):
+        table[s] = r * s
+    out = D.duet_profile_smooth(sizes, table)
+    got = [out[s] / s for s in sizes]
+    assert got[0] == 10.0 and got[-1] == 8.0           # end points kept
+    assert got[3] == 8.5                               # median(9.0, 6.0, 8.5)
+    assert got[1] == 9.5 and got[2] == 9.0 and got[4] == 8.0  # median(6.0, 8.5, 8.0): computed on the raw rates
+    assert all(out[s] == 0.0 for s in range(149) if s not in sizes)
+    mono = [0.0] * 149
+    for s, r in zip(sizes, [12.0, 11.0, 10.0, 9.0, 8.0, 5.0]):
+        mono[s] = r * s
+    assert D.duet_profile_smooth(sizes, mono) == mono  # a monotone run is a fixed point
+    with pytest.raises(D.DuetError):
+        D.duet_profile_smooth([16, 8], table)          # not ascending
+    with pytest.raises(D.DuetError):
+        D.duet_profile_smooth([8, 200], table)         # outside the table

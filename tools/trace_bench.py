@@ -70,7 +70,7 @@ def main():
     ctx = D.Ctx(spec, budget, max_seqs, max_batch, k_max, max_pages, max_pages * P + 16, D.DUET_DTYPE_BF16,
                 D.DUET_CTX_NO_GRAPH if args.no_graph else 0)
     parts, total = ctx.partitions()
-    fl, bw = ctx.calibrate(total) if args.calibration == "burst" else ctx.calibrate_corun(total, 0.12)
+    fl, bw = ctx.calibrate(total) if args.calibration == "burst" else ctx.calibrate_corun(total, 0.2)
     hw = D.HwProfile(total, parts, fl, bw)
     results = {}
     # static_slo: the conventional fix for TBT under chunked prefill — a temporal-only
