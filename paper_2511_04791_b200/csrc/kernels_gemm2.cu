@@ -15,6 +15,10 @@
 // 16 KiB per SM instead of 24 KiB per 128x256x16, and TMA writes 32 instead of 48 KiB per k-block),
 // the limit of the 1-CTA kernel (profiles/r01_probe_umma_rate.txt, profiles/r01_ncu_full_cfg2.md).
 // Tiles are assigned statically, every output is reduced over K in one fixed order.
+// Tile width BN = 256 (UMMA 256x256x16) or 128 (UMMA 256x128x16, each CTA loads 64 W rows) — the
+// narrow tile for grids the wide one leaves under-filled: a 256-row decode batch's O / down / QKV
+// projections have 16-24 wide tiles for the 32-37 CTA pairs of a decode partition.  The choice
+// depends on the shape only (split invariance); the per-element K order is the same for both.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -25,14 +29,17 @@
 namespace duet {
 namespace tc2 {
 
-constexpr int BM = 128, BK = 64, PAIR_M = 256, BN_PAIR = 256;
+constexpr int BM = 128, BK = 64, PAIR_M = 256;
 constexpr int A_BYTES = BM * BK * 2;      // this CTA's 128 rows of X
-constexpr int B_BYTES = 128 * BK * 2;     // this CTA's 128 rows of W
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int STAGES = 6;
-constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+template <int BN> struct Cfg {
+  static constexpr int B_ROWS = BN / 2;                 // this CTA's rows of W
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 6 : 8;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int TMEM_COLS = 2 * BN;              // two accumulators
+};
 constexpr int THREADS = 192;
-constexpr int TMEM_COLS = 512;            // two 256-column accumulators
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -156,10 +163,13 @@ __device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int& m
   nb = local / gm;
 }
 
-template <int EPI>
+template <int EPI, int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, Params p) {
-  constexpr int OUT_COLS = EPI == EPI_SWIGLU ? 128 : 256;
+  using CF = Cfg<BN>;
+  constexpr int STAGES = CF::STAGES, STAGE_BYTES = CF::STAGE_BYTES, B_BYTES = CF::B_BYTES, B_ROWS = CF::B_ROWS;
+  constexpr int TMEM_COLS = CF::TMEM_COLS, BN_PAIR = BN;
+  constexpr int OUT_COLS = EPI == EPI_SWIGLU ? BN / 2 : BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -206,7 +216,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
       auto w_row = [&](int nb) {
-        return EPI == EPI_SWIGLU ? (rank ? p.n_up_off : 0) + nb * 128 : nb * BN_PAIR + (int)rank * 128;
+        return EPI == EPI_SWIGLU ? (rank ? p.n_up_off : 0) + nb * B_ROWS : nb * BN_PAIR + (int)rank * B_ROWS;
       };
       int pre = 0;
 #ifndef DUET_NO_WPREFETCH
@@ -304,7 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const int row = mp * PAIR_M + (int)rank * BM + lane_row;
       const int n0 = nb * OUT_COLS;
       if constexpr (EPI == EPI_QKV_ROPE) {
-        // the tile's 256 columns are two whole heads (d_h = 128): rotate (i, i + 64) pairs of q and k
+        // the tile's BN columns are BN / 128 whole heads (d_h = 128): rotate (i, i + 64) pairs of q and k
         // heads at this row's position; q stays in C, k and v go to their KV slots
         {  // tcgen05.ld is warp-collective: every lane loads, only rows < M store
           const bool row_ok = row < p.M;
@@ -313,7 +323,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const int slot = pos & 15;
           const float2* cs = p.rope + (size_t)pos * 64;
 #pragma unroll 1
-          for (int hh = 0; hh < 2; ++hh) {
+          for (int hh = 0; hh < BN / 128; ++hh) {
             const int head = (n0 >> 7) + hh;
             if (head * 128 >= p.N) break;
             const bool is_q = head < p.hq, is_k = !is_q && head < p.hq + p.hkv;
@@ -376,7 +386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         tmem_ld32(tbase + c, v);
         if constexpr (EPI == EPI_SWIGLU) {
           float u[32];
-          tmem_ld32(tbase + 128 + c, u);
+          tmem_ld32(tbase + OUT_COLS + c, u);  // up columns follow the gate columns
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = silu_f(v[e]) * u[e];
         }
@@ -465,22 +475,24 @@ static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int l
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int EPI>
+template <int EPI, int BN>
 static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
+  using CF = Cfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm2_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(gemm2_kernel<EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
     attr = true;
   }
   CUtensorMap mx, mw;
   const int w_rows = EPI == EPI_SWIGLU ? 2 * a.N : a.N;
-  if (!make_map(&mx, a.A, a.M, a.K, a.lda, BM) || !make_map(&mw, a.B, w_rows, a.K, a.ldb, 128)) return -1;
+  if (!make_map(&mx, a.A, a.M, a.K, a.lda, BM) || !make_map(&mw, a.B, w_rows, a.K, a.ldb, CF::B_ROWS)) return -1;
   Params p{};
   p.M = a.M;
   p.N = a.N;
   p.K = a.K;
   p.num_m2 = (a.M + PAIR_M - 1) / PAIR_M;
-  p.num_n = (a.N + (EPI == EPI_SWIGLU ? 128 : 256) - 1) / (EPI == EPI_SWIGLU ? 128 : 256);
+  constexpr int out_cols = EPI == EPI_SWIGLU ? BN / 2 : BN;
+  p.num_n = (a.N + out_cols - 1) / out_cols;
   p.num_tiles = p.num_m2 * p.num_n;
   p.C = (bf16*)a.C;
   p.R = (const bf16*)a.R;
@@ -503,8 +515,20 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
     p.rope = a.rope->rope;
   }
   const int pairs = p.num_tiles < num_sms / 2 ? p.num_tiles : num_sms / 2;
-  launch_pdl(gemm2_kernel<EPI>, 2 * pairs, THREADS, SMEM, st, mx, mw, p);
+  launch_pdl(gemm2_kernel<EPI, BN>, 2 * pairs, THREADS, CF::SMEM, st, mx, mw, p);
   return 1;
+}
+
+// Tile width from the shape alone: the narrow tile when the wide one gives fewer tiles than the full
+// device has CTA pairs (74 on B200) — then every partition size is under-filled too.  DUET_GEMM2_BN =
+// 128 / 256 forces one width (A/B).
+template <int EPI>
+static int launch_w(const GemmArgs& a, int num_sms, cudaStream_t st) {
+  static const int force = getenv("DUET_GEMM2_BN") ? atoi(getenv("DUET_GEMM2_BN")) : 0;
+  const int wide_cols = EPI == EPI_SWIGLU ? 128 : 256;
+  const long wide_tiles = (long)((a.M + PAIR_M - 1) / PAIR_M) * ((a.N + wide_cols - 1) / wide_cols);
+  const bool narrow = force ? force == 128 : wide_tiles < 74;
+  return narrow ? launch<EPI, 128>(a, num_sms, st) : launch<EPI, 256>(a, num_sms, st);
 }
 
 }  // namespace tc2
@@ -514,14 +538,15 @@ bool gemm2_supported(const GemmArgs& a, int num_sms) {
   auto mis = [](const void* p) { return ((uintptr_t)p & 15) != 0; };  // TMA / 16-B epilogue alignment
   if (mis(a.A) || mis(a.B) || mis(a.C) || mis(a.R) || mis(a.R2) || mis(a.C2)) return false;
   return on && a.M > 128 && num_sms >= 2 && a.K % tc2::BK == 0 && a.lda % 8 == 0 && a.ldb % 8 == 0 &&
-         a.ldc % 8 == 0 && (!a.R || a.ldr % 8 == 0) && (a.epi != EPI_SWIGLU || a.N % 128 == 0);
+         a.ldc % 8 == 0 && (!a.R || a.ldr % 8 == 0) && (a.epi != EPI_SWIGLU || a.N % 128 == 0) &&
+         (a.epi != EPI_QKV_ROPE || a.N % 128 == 0);
 }
 
 int launch_gemm2(const GemmArgs& a, int num_sms, cudaStream_t st) {
-  if (a.epi == EPI_QKV_ROPE) return a.rope ? tc2::launch<EPI_QKV_ROPE>(a, num_sms, st) : -1;
-  if (a.epi == EPI_SWIGLU) return tc2::launch<EPI_SWIGLU>(a, num_sms, st);
-  if (a.epi == EPI_RESIDUAL) return tc2::launch<EPI_RESIDUAL>(a, num_sms, st);
-  return tc2::launch<EPI_STORE>(a, num_sms, st);
+  if (a.epi == EPI_QKV_ROPE) return a.rope ? tc2::launch_w<EPI_QKV_ROPE>(a, num_sms, st) : -1;
+  if (a.epi == EPI_SWIGLU) return tc2::launch_w<EPI_SWIGLU>(a, num_sms, st);
+  if (a.epi == EPI_RESIDUAL) return tc2::launch_w<EPI_RESIDUAL>(a, num_sms, st);
+  return tc2::launch_w<EPI_STORE>(a, num_sms, st);
 }
 
 }  // namespace duet
