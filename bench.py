@@ -834,8 +834,12 @@ def main():
             "partition_roofline": part_roof,
             "roofline": roof,
             "kernel_seconds_per_step": share,
-            "kernel_timing": f"CUDA events on the launching stream: the {dom} launches inside the timed region "
-                             f"(roofline); per-class seconds per step from an untimed {n_break}-step pass",
+            "kernel_timing": (f"the {dom} launches inside the timed region (roofline): "
+                              + ("device-side %globaltimer span of every decode-attention launch inside the decode "
+                                 "CUDA graphs (duet_profile: no events in graphs)"
+                                 if dom == "decode_attn" and split.mode == D.DUET_MODE_SPATIAL else
+                                 "CUDA events on the launching stream")
+                              + f"; per-class seconds per step from an untimed {n_break}-step pass"),
             "gpu_launches": int(kernels),
             "clocks": clk,
             "e2e": e2e,

@@ -405,9 +405,12 @@ duet_status duet_calibrate_stream(duet_ctx* ctx, double* bw_stream, int32_t len)
  * only the class it reports.  duet_profile_read synchronizes on the recorded events and returns
  * DUET_KCLASS_N entries. */
 /* GEMM / OTHER count the prefill side of a spatial step and every kernel of a temporal step;
- * GEMM_DECODE / OTHER_DECODE the decode side of a spatial step.  Timed kernels are never inside a
- * CUDA graph: while a class of a side is enabled, that side launches its kernels one by one instead
- * of replaying its graph (decode: DECODE_ATTN, GEMM_DECODE, OTHER_DECODE; prefill: the others). */
+ * GEMM_DECODE / OTHER_DECODE the decode side of a spatial step.  Event-timed kernels are never inside
+ * a CUDA graph: while GEMM_DECODE or OTHER_DECODE is enabled the decode side launches its kernels one
+ * by one, while a prefill-side class is enabled the prefill side does.  DECODE_ATTN alone keeps the
+ * decode graph: the graph is captured with a device-side timer in the decode-attention kernel (the
+ * earliest CTA start to the latest CTA end of every launch, %globaltimer; the split-K combine, when
+ * the batch splits, is not included), read by duet_profile_read. */
 enum { DUET_KCLASS_GEMM = 0, DUET_KCLASS_PREFILL_ATTN = 1, DUET_KCLASS_DECODE_ATTN = 2, DUET_KCLASS_OTHER = 3,
        DUET_KCLASS_GEMM_DECODE = 4, DUET_KCLASS_OTHER_DECODE = 5, DUET_KCLASS_N = 6 };
 #define DUET_PROFILE_ALL 0x3F

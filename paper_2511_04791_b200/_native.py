@@ -81,7 +81,8 @@ class duet_kv_pages(C.Structure):
                 ("page_size", C.c_int32)]
 
 
-DUET_KCLASS_N = 6
+(DUET_KCLASS_GEMM, DUET_KCLASS_PREFILL_ATTN, DUET_KCLASS_DECODE_ATTN, DUET_KCLASS_OTHER, DUET_KCLASS_GEMM_DECODE,
+ DUET_KCLASS_OTHER_DECODE, DUET_KCLASS_N) = range(7)
 DUET_PROFILE_ALL = 0x3F
 
 

@@ -98,6 +98,10 @@ struct DecodeAttnArgs {
   int num_sms;
   int max_len;      // upper bound of pos[r] + 1 over the batch (host-known), for split sizing
   int n_pages;      // pool extent (TMA maps)
+  // device-side launch timing (live kernel timing inside CUDA graphs): [0] earliest CTA start,
+  // [1] latest CTA end (%globaltimer ns), [2] CTAs done, [3] sum of launch durations (ns), [4] launches;
+  // the last CTA of a launch adds end - start to [3] and re-arms [0..2].  nullptr = off.
+  unsigned long long* dev_timer = nullptr;
 };
 int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st);
 bool decode_tc_supported(const DecodeAttnArgs& a);
@@ -136,6 +140,9 @@ bool fa_prefill_supported(const PrefillAttnArgs& a);
 int launch_fa_prefill(const PrefillAttnArgs& a, cudaStream_t st);
 bool fa_tc_supported(const PrefillAttnArgs& a);
 int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st);
+// CTA-pair (cta_group::2) version, opt-in with DUET_FA2=1 (measured slower than the one-CTA kernel)
+bool fa2_tc_supported(const PrefillAttnArgs& a);
+int launch_fa2_tc(const PrefillAttnArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- decode window bookkeeping
 // End of one decode step (P:335 look-ahead): y_out[step][r] = y[r]; xin[r] = y[r];

@@ -253,6 +253,10 @@ int launch_prefill_attn(DT dt, const PrefillAttnArgs& p, cudaStream_t st) {
   if (dt == DT::BF16) {
     static const char* impl = getenv("DUET_FA");  // "mma": force the mma.sync kernel (A/B comparisons)
     const bool force_mma = impl && impl[0] == 'm';
+    if (!force_mma && fa2_tc_supported(p)) {
+      const int r = launch_fa2_tc(p, st);
+      if (r > 0) return r;
+    }
     if (!force_mma && fa_tc_supported(p)) {
       const int r = launch_fa_tc(p, st);
       if (r > 0) return r;

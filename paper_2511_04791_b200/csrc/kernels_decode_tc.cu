@@ -87,6 +87,27 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// device-side launch timing (DecodeAttnArgs::dev_timer): called by thread 0 of every CTA
+__device__ __forceinline__ void dev_timer_start(unsigned long long* t) { atomicMin(&t[0], gtimer()); }
+__device__ __forceinline__ void dev_timer_end(unsigned long long* t) {
+  atomicMax(&t[1], gtimer());
+  __threadfence();
+  const unsigned long long total = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+  if (atomicAdd(&t[2], 1ull) == total - 1) {  // the launch's last CTA
+    __threadfence();
+    const unsigned long long t0 = atomicAdd(&t[0], 0ull), t1 = atomicAdd(&t[1], 0ull);
+    atomicAdd(&t[3], t1 > t0 ? t1 - t0 : 0ull);
+    atomicAdd(&t[4], 1ull);
+    atomicExch(&t[0], ~0ull);
+    atomicExch(&t[1], 0ull);
+    atomicExch(&t[2], 0ull);
+  }
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -102,6 +123,7 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   pdl_wait();
+  if (a.dev_timer && threadIdx.x == 0) dev_timer_start(a.dev_timer);
   const int split = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.hq / a.hkv;
@@ -341,6 +363,10 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
         a.part_ml[base * 2 + 1] = L;
       }
     }
+  }
+  if (a.dev_timer) {
+    __syncthreads();
+    if (threadIdx.x == 0) dev_timer_end(a.dev_timer);
   }
 }
 
