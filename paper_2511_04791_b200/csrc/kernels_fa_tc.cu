@@ -33,22 +33,27 @@
 namespace duet {
 namespace fatc {
 
-constexpr int BQ = 128, BKV = 128, DH = 128, PAGE = 16, K_STAGES = 2, V_STAGES = 3;
+constexpr int BQ = 128, BKV = 128, DH = 128, PAGE = 16;
 constexpr int Q_SUB = BQ * 128;            // [128 rows][64 cols] SW128 sub-tile = 16 KiB
 constexpr int KV_SUB = BKV * 128;          // [128 keys][64 cols] = 16 KiB
 constexpr int Q_BYTES = 2 * Q_SUB;         // 32 KiB per head
 constexpr int KV_BYTES = 2 * KV_SUB;       // 32 KiB per tensor per stage
 constexpr int OFF_Q = 0;                   // head A, head B
 constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
-constexpr int OFF_V = OFF_K + K_STAGES * KV_BYTES;
-constexpr int OFF_BAR = OFF_V + V_STAGES * KV_BYTES;
-constexpr int OFF_TRACE = OFF_BAR + 256;   // DUET_FA_TRACE: per-tile clock stamps of CTA (0,0,0)
+// K ring KS stages, V ring VS stages (the Q tiles take 64 KiB, so KS + VS <= 5)
+template <int KS, int VS> struct Ring {
+  static constexpr int OFF_V = OFF_K + KS * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_V + VS * KV_BYTES;
+  static constexpr int OFF_TRACE = OFF_BAR + 256;   // DUET_FA_TRACE: per-tile clock stamps of CTA (0,0,0)
+  static constexpr int SMEM = OFF_TRACE + 10 * 16 * 4 + 1024;
+  static_assert(SMEM <= 227 * 1024, "smem");
+  
+};
 constexpr int TRACE_EV = 10, TRACE_MAXJ = 16;
-constexpr int SMEM = OFF_TRACE + TRACE_EV * TRACE_MAXJ * 4 + 1024;
+
 constexpr int THREADS = 14 * 32;
 constexpr int TMEM_COLS = 512;             // per head: S_j / P_j (128) | O (128)
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
-static_assert(SMEM <= 227 * 1024, "smem");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -156,6 +161,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// two 32-column loads in flight, one wait (the softmax's TMEM reads are on its critical path)
+__device__ __forceinline__ void tmem_ld32x2(uint32_t taddr0, uint32_t taddr1, uint32_t (&r)[32], uint32_t (&q)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr0));
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]), "=r"(q[8]),
+        "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15]), "=r"(q[16]),
+        "=r"(q[17]), "=r"(q[18]), "=r"(q[19]), "=r"(q[20]), "=r"(q[21]), "=r"(q[22]), "=r"(q[23]), "=r"(q[24]),
+        "=r"(q[25]), "=r"(q[26]), "=r"(q[27]), "=r"(q[28]), "=r"(q[29]), "=r"(q[30]), "=r"(q[31])
+      : "r"(taddr1));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
@@ -180,7 +205,10 @@ struct Params {
   const bf16* v_pool;
 };
 
+template <int K_STAGES, int V_STAGES>
 __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant__ CUtensorMap map_q, Params p) {
+  using RG = Ring<K_STAGES, V_STAGES>;
+  constexpr int OFF_V = RG::OFF_V, OFF_BAR = RG::OFF_BAR, OFF_TRACE = RG::OFF_TRACE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bar = (uint64_t*)(smem + OFF_BAR);
@@ -381,8 +409,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
           uint32_t v0[32], v1[32];
-          tmem_ld32(t_s + c * 64, v0);
-          tmem_ld32(t_s + c * 64 + 32, v1);
+          tmem_ld32x2(t_s + c * 64, t_s + c * 64 + 32, v0, v1);
           if (full_tile) {
 #pragma unroll
             for (int e = 0; e < 32; e += 2)
@@ -419,8 +446,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
           uint32_t v0[32], v1[32], pk[32];
-          tmem_ld32(t_s + c * 64, v0);
-          tmem_ld32(t_s + c * 64 + 32, v1);
+          tmem_ld32x2(t_s + c * 64, t_s + c * 64 + 32, v0, v1);
           if (full_tile) {
             const uint64_t sc2 = pack_f2(sc, sc), nm2 = pack_f2(-m_used, -m_used);
             uint64_t acc2 = pack_f2(0.f, 0.f);
@@ -540,9 +566,14 @@ bool fa_tc_supported(const PrefillAttnArgs& a) {
 }
 
 int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {
+  // DUET_FA_RING = "KSxVS": K / V ring depths (A/B); K 3 / V 2 and K 2 / V 3 measure the same
+  // (profiles/r02_fa_ring_ab.txt: the MMA warp's K waits are the per-CTA pipeline fill, not ring depth)
+  static int ks = 3, vs = 2;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(fatc::fa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::SMEM);
+    if (const char* e = getenv("DUET_FA_RING")) sscanf(e, "%dx%d", &ks, &vs);
+    cudaFuncSetAttribute(fatc::fa_tc_kernel<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::Ring<2, 3>::SMEM);
+    cudaFuncSetAttribute(fatc::fa_tc_kernel<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::Ring<3, 2>::SMEM);
     attr = true;
   }
   CUtensorMap mq;
@@ -557,7 +588,8 @@ int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   // (timing experiment, garbage output); "tn" does both
   p.trace = trace ? (trace[0] == 'n' ? 2 : (trace[0] == 't' && trace[1] == 'n' ? 3 : 1)) : 0;
   dim3 grid(p.n_pairs, p.n_qtiles, a.n_seqs);
-  launch_pdl(fatc::fa_tc_kernel, grid, fatc::THREADS, fatc::SMEM, st, mq, p);
+  if (ks == 2 && vs == 3) launch_pdl(fatc::fa_tc_kernel<2, 3>, grid, fatc::THREADS, fatc::Ring<2, 3>::SMEM, st, mq, p);
+  else launch_pdl(fatc::fa_tc_kernel<3, 2>, grid, fatc::THREADS, fatc::Ring<3, 2>::SMEM, st, mq, p);
   return 1;
 }
 

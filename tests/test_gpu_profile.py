@@ -34,7 +34,9 @@ def test_decode_attention_device_timer_in_graph():
     for name, st in res.items():
         assert st["launches"] == 4 * 3 * 2, (name, st)        # steps x k x layers, each counted once
         assert st["seconds"] > 0 and st["bytes"] > 0, (name, st)
-    # the same launches, the same algorithmic bytes; device span vs event bracket within 2x
-    assert res["graph"]["bytes"] == pytest.approx(res["direct"]["bytes"], rel=1e-9)
+    # the same launches, the same algorithmic bytes
+    assert res["graph"]["bytes"] == pytest.approx(res["direct"]["bytes"], rel=1e-9), res
+    # the device span (first CTA start to last CTA end) of these ~10 us launches is at most the event
+    # bracket of the same launch made directly (which adds the launch latency), and not implausibly short
     r = res["graph"]["seconds"] / res["direct"]["seconds"]
-    assert 0.5 < r < 2.0, r
+    assert 0.1 < r < 1.5, (r, res)
