@@ -262,6 +262,7 @@ def main():
     ap.add_argument("--calibration", default="corun", choices=["corun", "burst"],
                     help="predictor tables: co-run at sustained clocks (default) or standalone bursts")
     ap.add_argument("--profile-only", action="store_true", help="a few steps, no extras (for ncu)")
+    ap.add_argument("--split", default=None, help="S_d,k: run this spatial split instead of Alg. 1's (profiling)")
     ap.add_argument("--lm-head", action="store_true",
                     help="close the decode window with the LM head + greedy tokens (f1; t_cls in the predictor)")
     ap.add_argument("--tp", type=int, default=1,
@@ -364,6 +365,9 @@ def main():
     def decide():
         if args.mode == "temporal":
             return D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1)
+        if args.split:   # a fixed (S_d, k) — e.g. a profiler run reproducing a measured run's split
+            sd_, k_ = (int(x) for x in args.split.split(","))
+            return D.split_struct(D.DUET_MODE_SPATIAL, total - sd_, sd_, k_)
         return D.duet_choose_split(spec, hw, batch, tau, k_max, opts)
 
     def prefill_arg(bufs=None, chunk=None):

@@ -297,6 +297,13 @@ static duet_status side_alloc(duet_ctx* c, Side& s, int cap_rows, int cap_seqs, 
                               {(int)m, (int)d, EPI_SWIGLU}, {(int)d, (int)m, EPI_RESIDUAL}};
     for (auto& sh : shapes) s.gemm_ws_floats = std::max(s.gemm_ws_floats, gemm_tc_splitk_need(M, sh[0], sh[1], sh[2]));
   }
+  // ... and of the CTA-pair GEMMs of under-filled grids (M > 128 in 256-row steps up to cap_rows)
+  for (int M = 256; M - 256 < cap_rows && M <= 4096; M += 256) {
+    const int Mc = std::min(M, cap_rows);
+    const int shapes[2][3] = {{(int)d, (int)nq, EPI_RESIDUAL}, {(int)d, (int)m, EPI_RESIDUAL}};
+    for (auto& sh : shapes) s.gemm_ws_floats = std::max(s.gemm_ws_floats, gemm2_splitk_need(Mc, sh[0], sh[1], sh[2]));
+    s.gemm_ws_floats = std::max(s.gemm_ws_floats, gemm2_splitk_need(Mc, (int)nqkv, (int)d, EPI_STORE));
+  }
   if (s.gemm_ws_floats > 0) CUDA_TRY(cudaMalloc(&s.gemm_ws, s.gemm_ws_floats * sizeof(float)));
   // LM head logits of the decode rows (f1), bf16 contexts with a vocabulary
   if (c->dt == DT::BF16 && sp.vocab > 0 && c->lim.max_decode_reqs > 0)

@@ -44,6 +44,8 @@ struct GemmArgs {
 };
 // fp32 partial floats a split-K launch of this shape needs (0 when it runs unsplit)
 size_t gemm_tc_splitk_need(int M, int N, int K, int epi);
+// fp32 partial floats a CTA-pair (M > 128) launch of this shape needs (0 when it runs unsplit)
+size_t gemm2_splitk_need(int M, int N, int K, int epi);
 
 // num_sms: SMs of the partition the launch runs in (persistent grid sizing).
 // Returns the number of kernels launched (0 on a launch error, checked by the caller).

@@ -145,6 +145,11 @@ struct Params {
   bf16* k_pool;
   bf16* v_pool;
   const float2* rope;
+  // split-K (STORE / RESIDUAL epilogues of under-filled grids): work unit u = tile (u % num_tiles) x
+  // K chunk (u / num_tiles) of kb_per k-blocks; chunk s writes fp32 partials to ws[s][M][N] and
+  // gemm2_reduce_kernel sums the chunks in order 0..ksplit-1 and applies the epilogue
+  int ksplit, kb_per;
+  float* ws;
 };
 
 // Tile order (grouped rasterization): tiles run in groups of GROUP_M 256-row blocks; inside a group the
@@ -185,6 +190,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
   const int num_k = p.K / BK;
+  const int num_units = p.num_tiles * p.ksplit;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -220,28 +226,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       };
       int pre = 0;
 #ifndef DUET_NO_WPREFETCH
-      if (pair < p.num_tiles) {  // fresh ring: the first STAGES stages are free
-        pre = num_k < STAGES ? num_k : STAGES;
+      if (pair < num_units) {  // fresh ring: the first STAGES stages are free
+        const int kb00 = (pair / p.num_tiles) * p.kb_per;
+        const int nkb0 = min(num_k, kb00 + p.kb_per) - kb00;
+        pre = nkb0 < STAGES ? nkb0 : STAGES;
         int mp0, nb0;
-        tile_coords(pair, p.num_m2, p.num_n, mp0, nb0);
+        tile_coords(pair % p.num_tiles, p.num_m2, p.num_n, mp0, nb0);
         const int row_w0 = w_row(nb0);
-        for (int kb = 0; kb < pre; ++kb) {
-          if (leader) mbar_expect_tx(&full[kb], 2 * STAGE_BYTES);
-          tma_load_2cta(&map_w, mapa(smem_u32(&full[kb]), 0), sB + kb * B_BYTES, kb * BK, row_w0);
+        for (int i = 0; i < pre; ++i) {
+          if (leader) mbar_expect_tx(&full[i], 2 * STAGE_BYTES);
+          tma_load_2cta(&map_w, mapa(smem_u32(&full[i]), 0), sB + i * B_BYTES, (kb00 + i) * BK, row_w0);
         }
       }
 #endif
       pdl_wait();
       int s = 0;
       uint32_t ph = 0;
-      for (int t = pair; t < p.num_tiles; t += n_pairs) {
+      for (int u = pair; u < num_units; u += n_pairs) {
+        const int t = u % p.num_tiles, kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
         int mp, nb;
         tile_coords(t, p.num_m2, p.num_n, mp, nb);
         const int row_x = mp * PAIR_M + (int)rank * BM;
         const int row_w = w_row(nb);
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           const uint32_t lbar = mapa(smem_u32(&full[s]), 0);
-          if (t == pair && kb < pre) {  // weights already requested before pdl_wait
+          if (u == pair && kb - kb0 < pre) {  // weights already requested before pdl_wait
             tma_load_2cta(&map_x, lbar, sA + s * A_BYTES, kb * BK, row_x);
           } else {
             mbar_wait(&empty[s], ph ^ 1);
@@ -263,18 +272,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int i = 0;
-      for (int t = pair; t < p.num_tiles; t += n_pairs, ++i) {
+      for (int u = pair; u < num_units; u += n_pairs, ++i) {
+        const int kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
         const int acc = i & 1;
         mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN_PAIR;
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma2(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (kb | k) != 0);
+            umma2(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (kb != kb0 || k != 0));
           commit_both(&empty[s]);
           if (++s == STAGES) {
             s = 0;
@@ -290,7 +300,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int lane_row = quad * 32 + lane;
     const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
     int i = 0;
-    for (int t = pair; t < p.num_tiles; t += n_pairs, ++i) {
+    for (int u = pair; u < num_units; u += n_pairs, ++i) {
+      const int t = u % p.num_tiles, sk = u / p.num_tiles;
       const int acc = i & 1;
       int mp, nb;
       tile_coords(t, p.num_m2, p.num_n, mp, nb);
@@ -308,11 +319,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
       }
       mbar_wait(&tfull[acc], (i >> 1) & 1);
-      if (t + n_pairs >= p.num_tiles) pdl_trigger();  // last tile: only the epilogue is left
+      if (u + n_pairs >= num_units) pdl_trigger();  // last unit: only the epilogue is left
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN_PAIR;
       const int row = mp * PAIR_M + (int)rank * BM + lane_row;
       const int n0 = nb * OUT_COLS;
+      if constexpr (EPI == EPI_STORE || EPI == EPI_RESIDUAL) {
+        if (p.ksplit > 1) {  // fp32 partial of K chunk sk; the reduce kernel applies the epilogue
+#pragma unroll 1
+          for (int c = 0; c < OUT_COLS; c += 32) {
+            float v[32];
+            tmem_ld32(tbase + c, v);
+            if (row < p.M && n0 + c < p.N) {
+              float* dst = p.ws + ((size_t)sk * p.M + row) * p.N + n0 + c;
+              if (n0 + c + 32 <= p.N) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e)
+                  if (n0 + c + e < p.N) dst[e] = v[e];
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_tempty0 + acc * 8);
+          continue;
+        }
+      }
       if constexpr (EPI == EPI_QKV_ROPE) {
         // the tile's BN columns are BN / 128 whole heads (d_h = 128): rotate (i, i + 64) pairs of q and k
         // heads at this row's position; q stays in C, k and v go to their KV slots
@@ -449,6 +485,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   }
 }
 
+// Split-K reduction + epilogue: every thread sums 8 consecutive outputs over the K chunks in order
+// 0..ksplit-1 (fixed order: results do not depend on the grid) and applies bias / residual.
+template <int EPI>
+__global__ void __launch_bounds__(256) gemm2_reduce_kernel(Params p) {
+  pdl_wait();
+  const int n8 = p.N / 8;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long)p.M * n8) return;
+  const int row = (int)(idx / n8), col = (int)(idx % n8) * 8;
+  float v[8];
+  {
+    const float* src = p.ws + (size_t)row * p.N + col;
+    const float4 a = __ldcg(reinterpret_cast<const float4*>(src)), b = __ldcg(reinterpret_cast<const float4*>(src + 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  for (int s = 1; s < p.ksplit; ++s) {
+    const float* src = p.ws + ((size_t)s * p.M + row) * p.N + col;
+    const float4 a = __ldcg(reinterpret_cast<const float4*>(src)), b = __ldcg(reinterpret_cast<const float4*>(src + 4));
+    v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w; v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+  }
+  const bool hi = row >= p.row_split;
+  const int rrow = hi ? row - p.row_split : row;
+  if constexpr (EPI == EPI_RESIDUAL) {
+    float r[8];
+    load16<bf16>((hi ? p.R2 : p.R) + (size_t)rrow * p.ldr + col, r);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] += r[e];
+  } else if (p.bias) {
+    float b[8];
+    load16<bf16>(p.bias + col, b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] += b[e];
+  }
+  store16<bf16>((hi ? p.C2 : p.C) + (size_t)rrow * p.ldc + col, v);
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -473,6 +545,20 @@ static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int l
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// K chunks for an under-filled grid, from the shape alone (split invariance): a STORE / RESIDUAL GEMM
+// with fewer tiles than the full device has CTA pairs (74) is cut into ceil(148 / tiles) <= 8 chunks of
+// >= 8 k-blocks — e.g. the 256-row decode batch's O and down projections (32 narrow tiles, a second
+// wave of 4 tiles on a 56-SM partition) — provided the caller's workspace holds the fp32 partials.
+static int splitk_count(int epi, int tiles, int num_k, int M, int N, const float* ws, size_t ws_floats) {
+  static const bool off = getenv("DUET_GEMM2_SPLITK") && atoi(getenv("DUET_GEMM2_SPLITK")) == 0;
+  if (off || !ws || (epi != EPI_STORE && epi != EPI_RESIDUAL) || tiles >= 74 || N % 8) return 1;
+  int ks = (148 + tiles - 1) / tiles;
+  if (ks > 8) ks = 8;
+  while (ks > 1 && num_k / ks < 8) --ks;
+  if (ks > 1 && (size_t)ks * M * N > ws_floats) return 1;
+  return ks;
 }
 
 template <int EPI, int BN>
@@ -514,8 +600,21 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
     p.v_pool = (bf16*)a.rope->v_pool;
     p.rope = a.rope->rope;
   }
-  const int pairs = p.num_tiles < num_sms / 2 ? p.num_tiles : num_sms / 2;
+  const int num_k = a.K / BK;
+  const int ks = splitk_count(EPI, p.num_tiles, num_k, a.M, a.N, a.ws, a.ws_floats);
+  p.kb_per = (num_k + ks - 1) / ks;
+  p.ksplit = (num_k + p.kb_per - 1) / p.kb_per;
+  p.ws = a.ws;
+  const int units = p.num_tiles * p.ksplit;
+  const int pairs = units < num_sms / 2 ? units : num_sms / 2;
   launch_pdl(gemm2_kernel<EPI, BN>, 2 * pairs, THREADS, CF::SMEM, st, mx, mw, p);
+  if (p.ksplit > 1) {
+    if constexpr (EPI == EPI_STORE || EPI == EPI_RESIDUAL) {
+      const long n = (long)a.M * (a.N / 8);
+      launch_pdl(gemm2_reduce_kernel<EPI>, (unsigned)((n + 255) / 256), 256, 0, st, p);
+      return 2;
+    }
+  }
   return 1;
 }
 
@@ -532,6 +631,18 @@ static int launch_w(const GemmArgs& a, int num_sms, cudaStream_t st) {
 }
 
 }  // namespace tc2
+
+size_t gemm2_splitk_need(int M, int N, int K, int epi) {
+  if (M <= 128 || K % tc2::BK || (epi != EPI_STORE && epi != EPI_RESIDUAL) || N % 8) return 0;
+  const long wide_tiles = (long)((M + tc2::PAIR_M - 1) / tc2::PAIR_M) * ((N + 255) / 256);
+  const int cols = wide_tiles < 74 ? 128 : 256;
+  const long tiles = (long)((M + tc2::PAIR_M - 1) / tc2::PAIR_M) * ((N + cols - 1) / cols);
+  if (tiles >= 74) return 0;
+  int ks = (int)((148 + tiles - 1) / tiles);
+  if (ks > 8) ks = 8;
+  while (ks > 1 && (K / tc2::BK) / ks < 8) --ks;
+  return ks > 1 ? (size_t)ks * M * N : 0;
+}
 
 bool gemm2_supported(const GemmArgs& a, int num_sms) {
   static const bool on = !getenv("DUET_GEMM2") || atoi(getenv("DUET_GEMM2")) != 0;  // A/B switch

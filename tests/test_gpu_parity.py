@@ -234,14 +234,17 @@ def test_page_table_errors_are_caught_before_launch():
                                        (2048, 6144, 4096, 0), (64, 4096, 14336, 1), (64, 14336, 4096, 2),
                                        (100, 512, 256, 2), (8, 768, 256, 3), (77, 6144, 4096, 3),
                                        (300, 1000, 512, 3), (128, 200, 128, 1), (600, 768, 2048, 1),
-                                       (520, 256, 1024, 2), (2112, 4096, 4096, 1)])
+                                       (520, 256, 1024, 2), (2112, 4096, 4096, 1),
+                                       (256, 4096, 4096, 1), (256, 4096, 14336, 1), (512, 4096, 4096, 0),
+                                       (384, 4096, 2048, 3)])
 def test_op_gemm_bf16(M, N, K, epi):
-    """tcgen05 GEMM vs float64 torch: CTA-pair 256x256 tiles (M > 128), swap-AB tiles with shape-only
-    split-K (M <= 128), every epilogue (3 = store + bias), ragged M / N, M spanning several CTA pairs."""
+    """tcgen05 GEMM vs float64 torch: CTA-pair 256x256 / 256x128 tiles (M > 128) with shape-only split-K
+    for under-filled grids (the 256-row decode batch's O / down: 600 / 256 / 512 / 384 rows here),
+    swap-AB tiles with shape-only split-K (M <= 128), every epilogue (3 = store + bias), ragged M / N."""
     torch.manual_seed(0)
     cfg = configs.get_config("cfg2")
     wl = workload.build(cfg, pre_seqs=[(16, 0)], dec_ctx=[], k=1, with_weights=False)
-    ctx = make_ctx(wl, "bf16")
+    ctx = make_ctx(wl, "bf16", extra_tokens=M)    # workspace sized for M-row launches (split-K partials)
     A = (torch.randn(M, K, device="cuda") / 4).bfloat16()
     Bn = 2 * N if epi == 2 else N
     B = (torch.randn(Bn, K, device="cuda") / K ** 0.5).bfloat16()
