@@ -404,12 +404,18 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
         tc_after();
         const int lim = pos - j * BKV;  // keys 0..lim of this tile are visible to this row
         const bool full_tile = lim >= BKV - 1;
-        // pass 1: row max over the visible keys (two 64-column halves)
-        float mx = -INFINITY;
+        // One pass over S in two 64-column chunks (online softmax at chunk granularity): each chunk is
+        // read from TMEM once, its max taken in registers, the exponentials taken against the running
+        // reference m_used, and P written over the chunk's S columns.  The reference is re-based only
+        // when a chunk's max exceeds it by more than 2^8: O and l are rescaled (PV_{j-1} is complete:
+        // s_full tracks it) and, for the second chunk, so is the first chunk's P already in TMEM.
+        // (The two-pass version read S twice: TMEM traffic that also slowed the MMAs, FA_TRACE.)
+        float l0 = 0.f, l1 = 0.f;
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
-          uint32_t v0[32], v1[32];
+          uint32_t v0[32], v1[32], pk[32];
           tmem_ld32x2(t_s + c * 64, t_s + c * 64 + 32, v0, v1);
+          float mx = -INFINITY;
           if (full_tile) {
 #pragma unroll
             for (int e = 0; e < 32; e += 2)
@@ -422,31 +428,36 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
               if (c * 64 + 32 + e <= lim) mx = fmaxf(mx, __uint_as_float(v1[e]));
             }
           }
-        }
-        const float m_new = fmaxf(m_used, mx * sc);  // sc > 0: the max commutes with the scaling
-        // re-base when the max grew by more than 2^8; PV_{j-1} is complete (s_full tracks it)
-        const bool mine = m_new > m_used + RESCALE_THRESHOLD;
-        if (__any_sync(0xffffffffu, mine)) {
-          if (j >= 1) {
-            const float f = mine ? exp2f(m_used - m_new) : 1.f;
+          const float m_new = fmaxf(m_used, mx * sc);  // sc > 0: the max commutes with the scaling
+          const bool mine = m_new > m_used + RESCALE_THRESHOLD;
+          if (__any_sync(0xffffffffu, mine)) {  // rare after the first chunk of a row
+            const float f = mine ? exp2f(m_used - m_new) : 1.f;  // 0 while m_used = -inf (nothing to scale)
             l *= f;
+            l0 *= f;
+            l1 *= f;
+            if (j >= 1) {
 #pragma unroll 1
-            for (int c = 0; c < DH; c += 32) {
-              uint32_t v[32];
-              tmem_ld32(T_O(h) + lane_base + c, v);
+              for (int cc = 0; cc < DH; cc += 32) {
+                uint32_t v[32];
+                tmem_ld32(T_O(h) + lane_base + cc, v);
 #pragma unroll
-              for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * f);
-              tmem_st32(T_O(h) + lane_base + c, v);
+                for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * f);
+                tmem_st32(T_O(h) + lane_base + cc, v);
+              }
             }
+            if (c == 1) {  // the first chunk's P (bf16 pairs in columns 0..31) against the new reference
+              uint32_t v[32];
+              tmem_ld32(t_s, v);
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                const float2 q = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[e]));
+                __nv_bfloat162 t = __floats2bfloat162_rn(q.x * f, q.y * f);
+                v[e] = *reinterpret_cast<uint32_t*>(&t);
+              }
+              tmem_st32(t_s, v);
+            }
+            if (mine) m_used = m_new;
           }
-          if (mine) m_used = m_new;
-        }
-        // pass 2: exponentials -> bf16 pairs -> TMEM columns 32c..32c+31 (over S columns already read)
-        float l0 = 0.f, l1 = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          uint32_t v0[32], v1[32], pk[32];
-          tmem_ld32x2(t_s + c * 64, t_s + c * 64 + 32, v0, v1);
           if (full_tile) {
             const uint64_t sc2 = pack_f2(sc, sc), nm2 = pack_f2(-m_used, -m_used);
             uint64_t acc2 = pack_f2(0.f, 0.f);

@@ -168,8 +168,11 @@ __device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int& m
   nb = local / gm;
 }
 
-template <int EPI, int BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+// PROD = 2: the X tiles and the W tiles are requested by two producer warps (0 and 6): one TMA-issuing
+// thread streams ~55 GB/s per SM from HBM (profiles/r01_probe_tma_bw.txt), which a 256-row decode
+// batch's weight-streaming GEMMs on a small partition need more than once over
+template <int EPI, int BN, int PROD>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1) * 32, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, Params p) {
   using CF = Cfg<BN>;
   constexpr int STAGES = CF::STAGES, STAGE_BYTES = CF::STAGE_BYTES, B_BYTES = CF::B_BYTES, B_ROWS = CF::B_ROWS;
@@ -214,9 +217,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   // set-up above overlaps the previous kernel's tail; its outputs are read below.  The producer waits
   // later: the weights (never written by an earlier kernel) of its first stages are requested first.
-  if (warp != 0) pdl_wait();
+  if (warp != 0 && !(PROD == 2 && warp == 6)) pdl_wait();
 
-  if (warp == 0) {
+  auto w_row_of = [&](int nb) {
+    return EPI == EPI_SWIGLU ? (rank ? p.n_up_off : 0) + nb * B_ROWS : nb * BN_PAIR + (int)rank * B_ROWS;
+  };
+  if (PROD == 2 && warp == 6) {
+    if (lane == 0) {
+      // ---------------- W producer (both CTAs): the weight tiles only; weights are never written by an
+      // earlier kernel, so no pdl_wait; the X producer posts every stage's expect_tx (the tx count may
+      // go transiently negative when a W tile lands first)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = pair; u < num_units; u += n_pairs) {
+        const int t = u % p.num_tiles, kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
+        int mp, nb;
+        tile_coords(t, p.num_m2, p.num_n, mp, nb);
+        const int row_w = w_row_of(nb);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          tma_load_2cta(&map_w, mapa(smem_u32(&full[s]), 0), sB + s * B_BYTES, kb * BK, row_w);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (PROD == 2 && warp == 0) {
+    if (lane == 0) {
+      // ---------------- X producer (both CTAs) + the leader's expect_tx of both CTAs' stage bytes
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+      pdl_wait();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = pair; u < num_units; u += n_pairs) {
+        const int t = u % p.num_tiles, kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
+        int mp, nb;
+        tile_coords(t, p.num_m2, p.num_n, mp, nb);
+        const int row_x = mp * PAIR_M + (int)rank * BM;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+          tma_load_2cta(&map_x, mapa(smem_u32(&full[s]), 0), sA + s * A_BYTES, kb * BK, row_x);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs): own X rows and own W rows; leader's `full` counts both
       asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
@@ -294,7 +346,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         commit_both(&tfull[acc]);
       }
     }
-  } else {
+  } else if (warp >= 2 && warp <= 5) {
     // ---------------- epilogue warps 2..5 (both CTAs): this CTA's 128 rows, TMEM quadrant = warp % 4
     const int quad = warp & 3;
     const int lane_row = quad * 32 + lane;
@@ -561,12 +613,12 @@ static int splitk_count(int epi, int tiles, int num_k, int M, int N, const float
   return ks;
 }
 
-template <int EPI, int BN>
+template <int EPI, int BN, int PROD>
 static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   using CF = Cfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm2_kernel<EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+    cudaFuncSetAttribute(gemm2_kernel<EPI, BN, PROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
     attr = true;
   }
   CUtensorMap mx, mw;
@@ -607,7 +659,7 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   p.ws = a.ws;
   const int units = p.num_tiles * p.ksplit;
   const int pairs = units < num_sms / 2 ? units : num_sms / 2;
-  launch_pdl(gemm2_kernel<EPI, BN>, 2 * pairs, THREADS, CF::SMEM, st, mx, mw, p);
+  launch_pdl(gemm2_kernel<EPI, BN, PROD>, 2 * pairs, THREADS + (PROD - 1) * 32, CF::SMEM, st, mx, mw, p);
   if (p.ksplit > 1) {
     if constexpr (EPI == EPI_STORE || EPI == EPI_RESIDUAL) {
       const long n = (long)a.M * (a.N / 8);
@@ -627,7 +679,10 @@ static int launch_w(const GemmArgs& a, int num_sms, cudaStream_t st) {
   const int wide_cols = EPI == EPI_SWIGLU ? 128 : 256;
   const long wide_tiles = (long)((a.M + PAIR_M - 1) / PAIR_M) * ((a.N + wide_cols - 1) / wide_cols);
   const bool narrow = force ? force == 128 : wide_tiles < 74;
-  return narrow ? launch<EPI, 128>(a, num_sms, st) : launch<EPI, 256>(a, num_sms, st);
+  // DUET_GEMM2_PROD = 1 / 2: producer warps (A/B); default 2
+  static const int prod = getenv("DUET_GEMM2_PROD") ? atoi(getenv("DUET_GEMM2_PROD")) : 2;
+  if (prod == 1) return narrow ? launch<EPI, 128, 1>(a, num_sms, st) : launch<EPI, 256, 1>(a, num_sms, st);
+  return narrow ? launch<EPI, 128, 2>(a, num_sms, st) : launch<EPI, 256, 2>(a, num_sms, st);
 }
 
 }  // namespace tc2
