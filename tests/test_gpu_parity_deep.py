@@ -301,3 +301,17 @@ def test_prefill_graph_capture_and_replay(cfg_name):
         torch.cuda.synchronize()
         assert ctx.last_step_times()["prefill_graph"] == 0
     ctx.close()
+
+
+@pytest.mark.skipif(bool(__import__("os").environ.get("DUET_FA2")), reason="already the CTA-pair run")
+def test_cta_pair_prefill_attention_parity_subprocess():
+    """The opt-in CTA-pair (cta_group::2) prefill attention (DUET_FA2=1, read once per process: a fresh
+    process) against the oracle at BASELINE size — full device and a partition — and in a layer stack."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DUET_FA2="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        "-k", "prefill_attention_output or (stack and cfg2)"], env=env, capture_output=True,
+                       text=True, timeout=900, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

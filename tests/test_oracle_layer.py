@@ -346,3 +346,25 @@ def test_decode_window_with_head_feeds_embedding():
     y2 = OL.decode_window(m, wl.weights, x2, [c + 1 for c in wl.dec_ctx], wl.dec_tables, kv, 1)
     assert np.array_equal(toks[0][1], t1)
     assert np.allclose(y[1], y2[0], rtol=0, atol=1e-12)
+
+
+def test_decode_window_feedback_chains_outputs():
+    """Reading #26 (head = None): step j+1's input is step j's final-layer OUTPUT (not the window's
+    input x): a k = 2 window equals two single-step windows chained by hand, and differs from feeding x
+    again."""
+    from oracle import layer as OL
+    from synth import configs, workload
+    from tests.oracle_run import make_kv
+    cfg = configs.get_config("cfg1")
+    wl = workload.build(cfg, k=2)
+    m = OL.Model.from_cfg(cfg.model)
+    y = OL.decode_window(m, wl.weights, wl.x_dec, wl.dec_ctx, wl.dec_tables, make_kv(wl), 2)
+    kv = make_kv(wl)
+    y1 = OL.decode_window(m, wl.weights, wl.x_dec, wl.dec_ctx, wl.dec_tables, kv, 1)
+    y2 = OL.decode_window(m, wl.weights, y1[0], [c + 1 for c in wl.dec_ctx], wl.dec_tables, kv, 1)
+    assert np.allclose(y[0], y1[0], rtol=0, atol=1e-12)
+    assert np.allclose(y[1], y2[0], rtol=0, atol=1e-12)
+    kv_x = make_kv(wl)
+    OL.decode_window(m, wl.weights, wl.x_dec, wl.dec_ctx, wl.dec_tables, kv_x, 1)
+    y2_x = OL.decode_window(m, wl.weights, wl.x_dec, [c + 1 for c in wl.dec_ctx], wl.dec_tables, kv_x, 1)
+    assert not np.allclose(y[1], y2_x[0], rtol=0, atol=1e-3)   # feeding x again is a different result
