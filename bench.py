@@ -263,6 +263,8 @@ def main():
                     help="predictor tables: co-run at sustained clocks (default) or standalone bursts")
     ap.add_argument("--profile-only", action="store_true", help="a few steps, no extras (for ncu)")
     ap.add_argument("--split", default=None, help="S_d,k: run this spatial split instead of Alg. 1's (profiling)")
+    ap.add_argument("--fine-split", action="store_true",
+                    help="2-SM (TPC) partition granularity (DUET_CTX_FINE_SPLIT) instead of the driver's 8-SM default")
     ap.add_argument("--lm-head", action="store_true",
                     help="close the decode window with the LM head + greedy tokens (f1; t_cls in the predictor)")
     ap.add_argument("--tp", type=int, default=1,
@@ -322,7 +324,8 @@ def main():
     max_pages = max(wl.pre_tables.shape[1], wl.dec_tables.shape[1])
     max_pos = max([c + q for q, c in wl.pre_seqs] + [c + 8 for c in wl.dec_ctx]) + 16
     ctx = D.Ctx(spec, n_p, len(wl.pre_seqs), n_d, 8, max_pages, max_pos,
-                D.DUET_DTYPE_BF16 if cfg.dtype == "bf16" else D.DUET_DTYPE_FP32)
+                D.DUET_DTYPE_BF16 if cfg.dtype == "bf16" else D.DUET_DTYPE_FP32,
+                D.DUET_CTX_FINE_SPLIT if args.fine_split else 0)
     parts, total = ctx.partitions()
     nvl_bw, ar_alpha = 900e9, 3e-6
     if tp > 1:
@@ -829,7 +832,7 @@ def main():
                        "l2": f"inputs > L2 ({step_bytes / 1e9:.1f} GB of weights + KV read per step), no flush",
                        "parallelism": f"tp{tp} (head-sharded, NCCL allreduce after O and down)" if tp > 1
                        else f"dp{ws} (independent replicas)", "calibration_s": round(t_cal, 2),
-                       "calibration": args.calibration},
+                       "calibration": args.calibration, "partition_granularity_sms": 2 if args.fine_split else 8},
             "predictor": {"t_pred_ms": t_pred * 1e3, "t_meas_ms": side["t_window"] * 1e3, "err": pred_err,
                           "t_meas_decode_ms": side["t_decode"] * 1e3, "t_meas_prefill_ms": side["t_prefill"] * 1e3,
                           "per_side": pe,
