@@ -224,7 +224,9 @@ def run_reference(args, ws, rank):
         return
     # per-step sample sized so that warmup + steps stay within ~2-3 minutes of CPU time
     n_steps = args.steps + args.warmup
-    smp = OracleSample(args.config, 128, 4) if n_steps <= 120 else OracleSample(args.config, 32, 2)
+    # (~2.9 s per 128-row + 4-decode cfg3 sample on 16 host threads)
+    smp = OracleSample(args.config, 128, 4) if n_steps <= 30 else \
+        OracleSample(args.config, 64, 2) if n_steps <= 120 else OracleSample(args.config, 32, 2)
     for _ in range(args.warmup):
         smp.run()
     tok = sec = 0.0
