@@ -168,9 +168,10 @@ __device__ __forceinline__ void tile_coords(int t, int num_m2, int num_n, int& m
   nb = local / gm;
 }
 
-// PROD = 2: the X tiles and the W tiles are requested by two producer warps (0 and 6): one TMA-issuing
-// thread streams ~55 GB/s per SM from HBM (profiles/r01_probe_tma_bw.txt), which a 256-row decode
-// batch's weight-streaming GEMMs on a small partition need more than once over
+// PROD = 2: the X tiles and the W tiles are requested by two producer warps (0 and 6); PROD = 4: four
+// (X even / odd k-blocks: warps 0 / 7, W: 6 / 8).  One TMA-issuing thread streams ~55 GB/s per SM
+// (~0.28 us per box, profiles/r01_probe_tma_bw.txt): a narrow (128-column) tile's k-block needs 24 KiB in
+// 0.18 us of MMA, so the 256-row decode GEMMs ran TMA-issue-bound at 31-47 % tensor pipe (ncu)
 template <int EPI, int BN, int PROD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1) * 32, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, Params p) {
@@ -217,50 +218,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
   const uint32_t tmem_base = *tmem_slot;
   // set-up above overlaps the previous kernel's tail; its outputs are read below.  The producer waits
   // later: the weights (never written by an earlier kernel) of its first stages are requested first.
-  if (warp != 0 && !(PROD == 2 && warp == 6)) pdl_wait();
+  // producer roles (PROD >= 2): warp 0 / 7 request X tiles, warp 6 / 8 W tiles; with PROD = 4 each of a
+  // pair takes the k-blocks of one parity (every box costs its issuing thread ~0.28 us, a narrow tile's
+  // k-block only ~0.18 us of MMA)
+  int role = -1, par = -1;  // role 0 = X (+ the leader's expect_tx), 1 = W; par = k-block parity (-1: all)
+  if (PROD >= 2) {
+    if (warp == 0) { role = 0; par = PROD == 4 ? 0 : -1; }
+    else if (warp == 6) { role = 1; par = PROD == 4 ? 0 : -1; }
+    else if (PROD == 4 && warp == 7) { role = 0; par = 1; }
+    else if (PROD == 4 && warp == 8) { role = 1; par = 1; }
+  }
+  if (warp != 0 && role < 0) pdl_wait();
 
   auto w_row_of = [&](int nb) {
     return EPI == EPI_SWIGLU ? (rank ? p.n_up_off : 0) + nb * B_ROWS : nb * BN_PAIR + (int)rank * B_ROWS;
   };
-  if (PROD == 2 && warp == 6) {
+  if (role >= 0) {
     if (lane == 0) {
-      // ---------------- W producer (both CTAs): the weight tiles only; weights are never written by an
-      // earlier kernel, so no pdl_wait; the X producer posts every stage's expect_tx (the tx count may
-      // go transiently negative when a W tile lands first)
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+      // ---------------- X producer(s): X tiles + the leader's expect_tx of both CTAs' stage bytes;
+      // W producer(s): weight tiles only — weights are never written by an earlier kernel, so no
+      // pdl_wait (a W tile may land before the stage's expect_tx: the tx count goes transiently negative)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(role == 0 ? &map_x : &map_w) : "memory");
+      if (role == 0) pdl_wait();
       int s = 0;
-      uint32_t ph = 0;
-      for (int u = pair; u < num_units; u += n_pairs) {
-        const int t = u % p.num_tiles, kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
-        int mp, nb;
-        tile_coords(t, p.num_m2, p.num_n, mp, nb);
-        const int row_w = w_row_of(nb);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
-          tma_load_2cta(&map_w, mapa(smem_u32(&full[s]), 0), sB + s * B_BYTES, kb * BK, row_w);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-      }
-    }
-  } else if (PROD == 2 && warp == 0) {
-    if (lane == 0) {
-      // ---------------- X producer (both CTAs) + the leader's expect_tx of both CTAs' stage bytes
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
-      pdl_wait();
-      int s = 0;
-      uint32_t ph = 0;
+      uint32_t ph = 0, g = 0;
       for (int u = pair; u < num_units; u += n_pairs) {
         const int t = u % p.num_tiles, kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
         int mp, nb;
         tile_coords(t, p.num_m2, p.num_n, mp, nb);
         const int row_x = mp * PAIR_M + (int)rank * BM;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
-          if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
-          tma_load_2cta(&map_x, mapa(smem_u32(&full[s]), 0), sA + s * A_BYTES, kb * BK, row_x);
+        const int row_w = w_row_of(nb);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          if (par < 0 || (int)(g & 1) == par) {
+            mbar_wait(&empty[s], ph ^ 1);
+            const uint32_t lbar = mapa(smem_u32(&full[s]), 0);
+            if (role == 0) {
+              if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+              tma_load_2cta(&map_x, lbar, sA + s * A_BYTES, kb * BK, row_x);
+            } else {
+              tma_load_2cta(&map_w, lbar, sB + s * B_BYTES, kb * BK, row_w);
+            }
+          }
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
@@ -679,10 +677,12 @@ static int launch_w(const GemmArgs& a, int num_sms, cudaStream_t st) {
   const int wide_cols = EPI == EPI_SWIGLU ? 128 : 256;
   const long wide_tiles = (long)((a.M + PAIR_M - 1) / PAIR_M) * ((a.N + wide_cols - 1) / wide_cols);
   const bool narrow = force ? force == 128 : wide_tiles < 74;
-  // DUET_GEMM2_PROD = 1 / 2: producer warps (A/B); default 2
-  static const int prod = getenv("DUET_GEMM2_PROD") ? atoi(getenv("DUET_GEMM2_PROD")) : 2;
+  // DUET_GEMM2_PROD = 1 / 2 / 4: producer warps (A/B); default 4 for the narrow tile, 2 for the wide one
+  static const int prod = getenv("DUET_GEMM2_PROD") ? atoi(getenv("DUET_GEMM2_PROD")) : 0;
   if (prod == 1) return narrow ? launch<EPI, 128, 1>(a, num_sms, st) : launch<EPI, 256, 1>(a, num_sms, st);
-  return narrow ? launch<EPI, 128, 2>(a, num_sms, st) : launch<EPI, 256, 2>(a, num_sms, st);
+  if (prod == 4) return narrow ? launch<EPI, 128, 4>(a, num_sms, st) : launch<EPI, 256, 4>(a, num_sms, st);
+  if (prod == 2) return narrow ? launch<EPI, 128, 2>(a, num_sms, st) : launch<EPI, 256, 2>(a, num_sms, st);
+  return narrow ? launch<EPI, 128, 4>(a, num_sms, st) : launch<EPI, 256, 2>(a, num_sms, st);
 }
 
 }  // namespace tc2
