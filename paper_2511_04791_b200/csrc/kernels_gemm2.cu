@@ -21,6 +21,7 @@
 // depends on the shape only (split invariance); the per-element K order is the same for both.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "dev_common.cuh"
@@ -668,35 +669,36 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   return 1;
 }
 
-// Tile width from the shape alone: the narrow tile when the wide one gives fewer tiles than the full
-// device has CTA pairs (74 on B200) — then every partition size is under-filled too.  DUET_GEMM2_BN =
-// 128 / 256 forces one width (A/B).
+// Tile width: 256 by default — under-filled grids split K instead (splitk_count).  The 128-column tile
+// (DUET_GEMM2_BN=128) fills more pairs but its k-block is half the MMA work for the same X tile: on the
+// 256-row decode batch at 56 SMs the narrow tiles averaged 72.6 us per GEMM launch, the wide tiles with
+// split-K 66.5 us (profiles/r02_gemm2_tile_ab.txt).  DUET_GEMM2_BN = 128 / 256 forces one width (A/B).
 template <int EPI>
 static int launch_w(const GemmArgs& a, int num_sms, cudaStream_t st) {
   static const int force = getenv("DUET_GEMM2_BN") ? atoi(getenv("DUET_GEMM2_BN")) : 0;
-  const int wide_cols = EPI == EPI_SWIGLU ? 128 : 256;
-  const long wide_tiles = (long)((a.M + PAIR_M - 1) / PAIR_M) * ((a.N + wide_cols - 1) / wide_cols);
-  const bool narrow = force ? force == 128 : wide_tiles < 74;
-  // DUET_GEMM2_PROD = 1 / 2 / 4: producer warps (A/B); default 4 for the narrow tile, 2 for the wide one
-  static const int prod = getenv("DUET_GEMM2_PROD") ? atoi(getenv("DUET_GEMM2_PROD")) : 0;
+  const bool narrow = force == 128;
+  // DUET_GEMM2_PROD = 1 / 2 / 4: producer warps (A/B); default 2 (4 measured equal, 1 within 1 %)
+  static const int prod = getenv("DUET_GEMM2_PROD") ? atoi(getenv("DUET_GEMM2_PROD")) : 2;
   if (prod == 1) return narrow ? launch<EPI, 128, 1>(a, num_sms, st) : launch<EPI, 256, 1>(a, num_sms, st);
   if (prod == 4) return narrow ? launch<EPI, 128, 4>(a, num_sms, st) : launch<EPI, 256, 4>(a, num_sms, st);
   if (prod == 2) return narrow ? launch<EPI, 128, 2>(a, num_sms, st) : launch<EPI, 256, 2>(a, num_sms, st);
-  return narrow ? launch<EPI, 128, 4>(a, num_sms, st) : launch<EPI, 256, 2>(a, num_sms, st);
+  return narrow ? launch<EPI, 128, 2>(a, num_sms, st) : launch<EPI, 256, 2>(a, num_sms, st);
 }
 
 }  // namespace tc2
 
 size_t gemm2_splitk_need(int M, int N, int K, int epi) {
   if (M <= 128 || K % tc2::BK || (epi != EPI_STORE && epi != EPI_RESIDUAL) || N % 8) return 0;
-  const long wide_tiles = (long)((M + tc2::PAIR_M - 1) / tc2::PAIR_M) * ((N + 255) / 256);
-  const int cols = wide_tiles < 74 ? 128 : 256;
-  const long tiles = (long)((M + tc2::PAIR_M - 1) / tc2::PAIR_M) * ((N + cols - 1) / cols);
-  if (tiles >= 74) return 0;
-  int ks = (int)((148 + tiles - 1) / tiles);
-  if (ks > 8) ks = 8;
-  while (ks > 1 && (K / tc2::BK) / ks < 8) --ks;
-  return ks > 1 ? (size_t)ks * M * N : 0;
+  size_t need = 0;
+  for (int cols : {128, 256}) {  // either tile width (DUET_GEMM2_BN may force one)
+    const long tiles = (long)((M + tc2::PAIR_M - 1) / tc2::PAIR_M) * ((N + cols - 1) / cols);
+    if (tiles >= 74) continue;
+    int ks = (int)((148 + tiles - 1) / tiles);
+    if (ks > 8) ks = 8;
+    while (ks > 1 && (K / tc2::BK) / ks < 8) --ks;
+    if (ks > 1) need = std::max(need, (size_t)ks * M * N);
+  }
+  return need;
 }
 
 bool gemm2_supported(const GemmArgs& a, int num_sms) {

@@ -238,7 +238,7 @@ def test_page_table_errors_are_caught_before_launch():
                                        (256, 4096, 4096, 1), (256, 4096, 14336, 1), (512, 4096, 4096, 0),
                                        (384, 4096, 2048, 3)])
 def test_op_gemm_bf16(M, N, K, epi):
-    """tcgen05 GEMM vs float64 torch: CTA-pair 256x256 / 256x128 tiles (M > 128) with shape-only split-K
+    """tcgen05 GEMM vs float64 torch: CTA-pair 256x256 tiles (M > 128) with shape-only split-K
     for under-filled grids (the 256-row decode batch's O / down: 600 / 256 / 512 / 384 rows here),
     swap-AB tiles with shape-only split-K (M <= 128), every epilogue (3 = store + bias), ragged M / N."""
     torch.manual_seed(0)
@@ -458,3 +458,17 @@ def test_forced_attention_corun_parity_subprocess():
                         "-k", "llama_shapes or qwen or running_max"], env=env, capture_output=True, text=True,
                        timeout=900, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "3 passed" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.skipif(bool(__import__("os").environ.get("DUET_GEMM2_BN")), reason="already the forced-width run")
+def test_narrow_pair_tile_gemm_parity_subprocess():
+    """The optional 256 x 128 CTA-pair tile (DUET_GEMM2_BN=128, read once per process: a fresh process)
+    and the four-producer variant pass the op-level GEMM tests and a layer test against the oracle."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DUET_GEMM2_BN="128", DUET_GEMM2_PROD="4")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        "-k", "op_gemm or llama_shapes"], env=env, capture_output=True, text=True,
+                       timeout=900, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
