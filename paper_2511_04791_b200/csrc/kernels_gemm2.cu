@@ -604,8 +604,10 @@ static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int l
 // wave of 4 tiles on a 56-SM partition) — provided the caller's workspace holds the fp32 partials.
 static int splitk_count(int epi, int tiles, int num_k, int M, int N, const float* ws, size_t ws_floats) {
   static const bool off = getenv("DUET_GEMM2_SPLITK") && atoi(getenv("DUET_GEMM2_SPLITK")) == 0;
+  // DUET_GEMM2_SPLIT_UNITS: work units aimed at (A/B; <= 148, the workspace is sized for 148)
+  static const int target = getenv("DUET_GEMM2_SPLIT_UNITS") ? std::min(148, atoi(getenv("DUET_GEMM2_SPLIT_UNITS"))) : 148;
   if (off || !ws || (epi != EPI_STORE && epi != EPI_RESIDUAL) || tiles >= 74 || N % 8) return 1;
-  int ks = (148 + tiles - 1) / tiles;
+  int ks = (target + tiles - 1) / tiles;
   if (ks > 8) ks = 8;
   while (ks > 1 && num_k / ks < 8) --ks;
   if (ks > 1 && (size_t)ks * M * N > ws_floats) return 1;
