@@ -599,13 +599,13 @@ static bool make_map(CUtensorMap* m, const void* base, int rows, int cols, int l
 }
 
 // K chunks for an under-filled grid, from the shape alone (split invariance): a STORE / RESIDUAL GEMM
-// with fewer tiles than the full device has CTA pairs (74) is cut into ceil(148 / tiles) <= 8 chunks of
+// with fewer tiles than the full device has CTA pairs (74) is cut into ceil(74 / tiles) <= 8 chunks of
 // >= 8 k-blocks — e.g. the 256-row decode batch's O and down projections (32 narrow tiles, a second
 // wave of 4 tiles on a 56-SM partition) — provided the caller's workspace holds the fp32 partials.
 static int splitk_count(int epi, int tiles, int num_k, int M, int N, const float* ws, size_t ws_floats) {
   static const bool off = getenv("DUET_GEMM2_SPLITK") && atoi(getenv("DUET_GEMM2_SPLITK")) == 0;
   // DUET_GEMM2_SPLIT_UNITS: work units aimed at (A/B; <= 148, the workspace is sized for 148)
-  static const int target = getenv("DUET_GEMM2_SPLIT_UNITS") ? std::min(148, atoi(getenv("DUET_GEMM2_SPLIT_UNITS"))) : 148;
+  static const int target = getenv("DUET_GEMM2_SPLIT_UNITS") ? std::min(148, atoi(getenv("DUET_GEMM2_SPLIT_UNITS"))) : 74;
   if (off || !ws || (epi != EPI_STORE && epi != EPI_RESIDUAL) || tiles >= 74 || N % 8) return 1;
   int ks = (target + tiles - 1) / tiles;
   if (ks > 8) ks = 8;
