@@ -262,6 +262,39 @@ duet_status duet_ctx_set_comms(duet_ctx* ctx, int32_t rank, const void* id_decod
 duet_status duet_calibrate_allreduce(duet_ctx* ctx, double* alpha_s, double* bw_bytes_s);
 duet_status duet_ctx_check_comms(duet_ctx* ctx);
 
+/* ----------------------------------------------------------------- fused GEMM + allreduce (f3)
+ * SURVEY §8(f) f3; P:233-236 (§4.1 Communication Operators: in a head-sharded TP block the O and FFN-down
+ * outputs are partial sums over the N ranks, followed by an allreduce of the [n][d] rows, twice per
+ * layer).  The row-parallel projection and its allreduce run as ONE CTA-pair tcgen05 kernel: the
+ * epilogue of each 256 x 256 output tile t pushes the fp32 partial over peer memory (NVLink) into the
+ * receive slot of the tile's owner rank t mod N and releases an arrival counter there; the owner sums the
+ * N partials in rank order 0..N-1 (its own straight from TMEM), adds the residual, rounds once to bf16
+ * and stores the rows into every rank's output (all-gather by push), releasing each rank's completion
+ * counter.  Communication overlaps the remaining tiles' MMAs; no NCCL kernel runs in the partition.
+ * Every wait polls local memory; every remote access is a store or a release-add; counters are re-armed
+ * by their waiters, so a launch or a CUDA-graph replay needs no epoch.
+ *
+ * duet_ctx_ar_handle: allocates (once) the ctx's fused-allreduce arena — per side the receive slots, the
+ *   counters and two [rows][d] bf16 outputs, sized from the limits — and writes its cudaIpcMemHandle_t
+ *   (64 bytes) to out (len >= 64).  Needs duet_ctx_set_comms first (rank, group).  Every rank must have
+ *   created its ctx with the same spec and limits (the arenas share one layout).
+ * duet_ctx_ar_open: handles = [n][64] bytes, every rank's handle in rank order (an all-gather of
+ *   duet_ctx_ar_handle); maps the peers' arenas (cudaIpcOpenMemHandle).  From then on duet_step runs the
+ *   O and down projections of every > 128-row batch (the prefill side; temporal steps; a > 128-row decode
+ *   side) through the fused kernel; batches of <= 128 rows keep the NCCL allreduce.  Every rank calls it
+ *   before any rank's next duet_step.  With tp = 1 the kernel is the plain residual GEMM (bitwise).
+ *   Errors: INVALID_ARG (no comms / no arena / n != tp / already open), CUDA (IPC).
+ * duet_op_gemm_ar_emul: the fused kernel with n_ranks ranks (1..8) EMULATED in one grid on this GPU
+ *   (each rank on total_sms / 2 / n_ranks CTA pairs, all resident: ranks that wait on one another must
+ *   share a launch when there are fewer GPUs than ranks).  A: [n_ranks][M][K], B: [n_ranks][N][K]
+ *   (rank r's shards stacked), R: [M][N], C: [n_ranks][M][N] (every rank's output); each must equal
+ *   R + sum_r A_r B_r^T, and all ranks' outputs are bitwise equal.  M > 128, N % 32 == 0, K % 64 == 0,
+ *   bf16 ctx, device pointers, 16-byte aligned.  Errors: INVALID_ARG, OUT_OF_RANGE, UNSUPPORTED, CUDA. */
+duet_status duet_ctx_ar_handle(duet_ctx* ctx, void* out, int32_t len);
+duet_status duet_ctx_ar_open(duet_ctx* ctx, int32_t n, const void* handles);
+duet_status duet_op_gemm_ar_emul(duet_ctx* ctx, int32_t n_ranks, const void* A, const void* B, const void* R,
+                                 void* C, int32_t M, int32_t N, int32_t K, void* stream);
+
 /* The achievable decode-partition sizes, ascending (host array of capacity *n on input;
  * *n is set to the count).  total_sms: SMs of the device. */
 duet_status duet_ctx_partitions(duet_ctx* ctx, int32_t* sd_sms, int32_t* n, int32_t* total_sms);

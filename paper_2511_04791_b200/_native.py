@@ -135,6 +135,10 @@ _SIGS = {
     "duet_ctx_set_comms": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "duet_calibrate_allreduce": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "duet_ctx_check_comms": (C.c_int, [C.c_void_p]),
+    "duet_ctx_ar_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "duet_ctx_ar_open": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "duet_op_gemm_ar_emul": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "duet_op_decode_attn": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32, C.c_void_p, C.c_void_p,
                                       C.c_int32, C.c_int32, C.c_void_p]),
@@ -422,6 +426,27 @@ class Ctx:
     def check_comms(self):
         """Raises DuetError(NCCL) when a communicator reports an asynchronous error (duet_ctx_check_comms)."""
         _check(lib().duet_ctx_check_comms(self.h))
+
+    def ar_handle(self) -> bytes:
+        """This rank's fused-allreduce arena as a 64-byte cudaIpcMemHandle_t (duet_ctx_ar_handle)."""
+        buf = C.create_string_buffer(64)
+        _check(lib().duet_ctx_ar_handle(self.h, buf, 64))
+        return buf.raw
+
+    def ar_open(self, handles):
+        """handles: every rank's ar_handle() in rank order (duet_ctx_ar_open)."""
+        blob = b"".join(bytes(h) for h in handles)
+        buf = C.create_string_buffer(blob, len(blob))
+        _check(lib().duet_ctx_ar_open(self.h, len(handles), buf))
+
+    def op_gemm_ar_emul(self, A, B, R, Cout, stream=None):
+        """A [n][M][K], B [n][N][K], R [M][N], Cout [n][M][N] (duet_op_gemm_ar_emul)."""
+        n, M, K = A.shape
+        N = B.shape[1]
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        _check(lib().duet_op_gemm_ar_emul(self.h, n, _ptr(A), _ptr(B), _ptr(R), _ptr(Cout), M, N, K,
+                                          C.c_void_p(stream)))
 
     def calibrate_allreduce(self):
         """(alpha seconds, B_NVLink bytes/s) of the P:237 allreduce model (duet_calibrate_allreduce)."""

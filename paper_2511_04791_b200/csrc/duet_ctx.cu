@@ -238,6 +238,21 @@ struct duet_ctx {
   // token-time ring (SURVEY §8(d) TBT per decode step): %globaltimer when each step's tokens are done
   unsigned long long* tok_ts = nullptr;
   int* tok_cnt = nullptr;
+  // fused GEMM + allreduce: one IPC-exported arena per rank holding, per side, the
+  // receive slots, the counters and the two [rows][d] outputs (x1 and the layer output) the owners push
+  // into; ar_grp[side] is the group as seen from this rank (peer-mapped pointers), ar_on once opened
+  struct ArSide {
+    size_t off_slots = 0, off_cnt = 0, off_out0 = 0, off_out1 = 0;
+  } ar_lay[2];
+  size_t ar_bytes = 0;
+  char* ar_arena = nullptr;
+  char* ar_peer[kMaxTp] = {};
+  GemmAr ar_grp[2];
+  bool ar_on = false;
+  // duet_op_gemm_ar_emul workspace (every emulated rank's slots and counters)
+  float* emu_slots = nullptr;
+  unsigned* emu_cnt = nullptr;
+  size_t emu_slot_floats = 0, emu_cnt_n = 0;
 };
 
 static duet_status comms_healthy(duet_ctx* c);
@@ -479,6 +494,23 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     const ncclResult_t r = NCCL.AllReduce(buf, buf, (size_t)rows * d, nccl_dt, ncclSum, comm, st);
     return r == ncclSuccess ? 1 : -1;
   };
+  // f3: with the fused-allreduce group open, the O and down projections of a > 128-row batch run as
+  // one GEMM + allreduce kernel each (outputs in this side's arena buffers out0 / out1, pushed there by
+  // the tiles' owner ranks); the NCCL allreduce stays for batches the CTA-pair kernel does not take
+  const int side_i = (&S == &c->dec) ? 0 : 1;
+  const bool ar_side = c->ar_on && comm != nullptr && dt == DT::BF16;
+  GemmAr ar_o, ar_d;
+  char* ar_out0 = nullptr;
+  char* ar_out1 = nullptr;
+  if (ar_side) {
+    const auto& L = c->ar_lay[side_i];
+    ar_o = c->ar_grp[side_i];
+    ar_d = ar_o;
+    for (int r = 0; r < ar_o.n; ++r) ar_d.out[r] = (char*)ar_o.out[r] + (L.off_out1 - L.off_out0);
+    ar_out0 = c->ar_arena + L.off_out0;
+    ar_out1 = c->ar_arena + L.off_out1;
+  }
+  const void* x_carry = x_in;
   auto with_ws = [&](GemmArgs& g) {
     g.ws = S.gemm_ws;
     g.ws_floats = S.gemm_ws_floats;
@@ -502,7 +534,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     }                                                                                             \
   } while (0)
   for (int l = 0; l < sp.n_layers; ++l) {
-    const void* X = l == 0 ? x_in : ((l & 1) ? S.xa : S.xb);
+    const void* X = x_carry;  // layer 0: x_in; then the previous layer's output (ping-pong or arena)
     void* Y = l == sp.n_layers - 1 ? y_final : ((l & 1) ? S.xb : S.xa);
     const duet_layer_weights& W = w[l];
     // 1. h = RMSNorm(x) g1
@@ -580,25 +612,48 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       go.row_split = row_split;
       go.C2 = (char*)S.x1 + (size_t)row_split * d * es;  // output stays in one buffer
     }
+    const void* x1 = S.x1;
+    bool fused_o = false;
+    if (ar_side && !(l == 0 && row_split < n_rows)) {  // f3: O projection + allreduce in one kernel
+      GemmArgs ga{S.o, W.w_o, nullptr, X, nullptr, n_rows, d, hq * dh, hq * dh, hq * dh, d, d, EPI_RESIDUAL_AR};
+      ga.ar = &ar_o;
+      if (gemm2_supported(ga, num_sms)) {
+        go = ga;
+        fused_o = true;
+        x1 = ar_out0;
+      }
+    }
     TIMED(DUET_KCLASS_GEMM, gemm_fl(d, hq * dh), gemm_by(d, hq * dh, d, true), launch_gemm(dt, go, num_sms, st));
-    if (comm) TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, allreduce(S.x1, n_rows));
+    if (comm && !fused_o) TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, allreduce(S.x1, n_rows));
     // 6. h2 = RMSNorm(x1) g2
-    TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e, launch_rmsnorm(dt, S.x1, W.g_norm2, S.h2, n_rows, d, eps, st));
+    TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e, launch_rmsnorm(dt, x1, W.g_norm2, S.h2, n_rows, d, eps, st));
     // 7. act = silu(h2 W_g^T) * (h2 W_u^T)
     GemmArgs gg{S.h2, W.w_gate_up, S.act, nullptr, nullptr, n_rows, m, d, d, d, m, 0, EPI_SWIGLU};
     with_ws(gg);
     TIMED(DUET_KCLASS_GEMM, gemm_fl(2.0 * m, d), gemm_by(2.0 * m, d, m, false), launch_gemm(dt, gg, num_sms, st));
     // 8. y = x1 + act W_d^T
-    GemmArgs gd{S.act, W.w_down, Y, lead ? S.x1 : nullptr, nullptr, n_rows, d, m, m, m, d, d,
+    GemmArgs gd{S.act, W.w_down, Y, lead ? x1 : nullptr, nullptr, n_rows, d, m, m, m, d, d,
                 lead ? EPI_RESIDUAL : EPI_STORE};
     with_ws(gd);
     if (l == sp.n_layers - 1 && row_split < n_rows) {
       gd.C2 = y_final2;
-      gd.R2 = lead ? (const char*)S.x1 + (size_t)row_split * d * es : nullptr;
+      gd.R2 = lead ? (const char*)x1 + (size_t)row_split * d * es : nullptr;
       gd.row_split = row_split;
     }
+    bool fused_d = false;
+    if (ar_side && !(l == sp.n_layers - 1 && row_split < n_rows)) {  // f3: down projection + allreduce
+      GemmArgs ga{S.act, W.w_down, nullptr, x1, nullptr, n_rows, d, m, m, m, d, d, EPI_RESIDUAL_AR};
+      ga.ar = &ar_d;
+      if (gemm2_supported(ga, num_sms)) {
+        gd = ga;
+        fused_d = true;
+      }
+    }
     TIMED(DUET_KCLASS_GEMM, gemm_fl(d, m), gemm_by(d, m, d, true), launch_gemm(dt, gd, num_sms, st));
-    if (comm) {
+    x_carry = fused_d ? (const void*)ar_out1 : (const void*)Y;
+    if (fused_d && l == sp.n_layers - 1)  // the caller's output buffer is not peer-mapped
+      TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, launch_copy_bytes(Y, ar_out1, (size_t)n_rows * d * es, num_sms, st));
+    if (comm && !fused_d) {
       // rows >= row_split of the last layer's output went to y_final2 (the temporal batch's decode
       // rows in the caller's decode buffer): each buffer is reduced over its own rows
       const bool split_out = l == sp.n_layers - 1 && row_split < n_rows;
@@ -807,6 +862,11 @@ extern "C" duet_status duet_ctx_destroy(duet_ctx* c) {
   side_free(c->dec);
   side_free(c->pre);
   if (c->rope) cudaFree(c->rope);
+  for (int r = 0; r < kMaxTp; ++r)
+    if (c->ar_peer[r] && c->ar_peer[r] != c->ar_arena) cudaIpcCloseMemHandle(c->ar_peer[r]);
+  if (c->ar_arena) cudaFree(c->ar_arena);
+  if (c->emu_slots) cudaFree(c->emu_slots);
+  if (c->emu_cnt) cudaFree(c->emu_cnt);
   if (c->tok_ts) cudaFree(c->tok_ts);
   if (c->tok_cnt) cudaFree(c->tok_cnt);
   if (c->dev_timer) cudaFree(c->dev_timer);
@@ -1417,6 +1477,142 @@ static duet_status comms_healthy(duet_ctx* c) {
       DUET_FAIL(DUET_ERR_NCCL, "%s-side communicator reports an asynchronous error: %s", names[i],
                 NCCL.GetErrorString(ae));
   }
+  return DUET_OK;
+}
+
+// ---------------------------------------------------------------- fused GEMM + allreduce (f3)
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// ar_grp[side] from the ranks' arena bases (the layout is the same on every rank: same spec and limits)
+static void ar_fill_groups(duet_ctx* c) {
+  const int n = c->spec.tp, d = c->spec.d_model;
+  Side* sides[2] = {&c->dec, &c->pre};
+  for (int i = 0; i < 2; ++i) {
+    const auto& L = c->ar_lay[i];
+    GemmAr& g = c->ar_grp[i];
+    g = GemmAr{};
+    g.n = n;
+    g.rank = c->tp_rank;
+    g.emul = 0;
+    const size_t ncnt = gemm_ar_counters(std::max(sides[i]->cap_rows, 1), d, n);
+    for (int r = 0; r < n; ++r) {
+      char* b = c->ar_peer[r];
+      g.slots[r] = (float*)(b + L.off_slots);
+      g.cnt[r] = (unsigned*)(b + L.off_cnt);
+      g.done[r] = g.cnt[r] + ncnt;
+      g.out[r] = b + L.off_out0;  // the O projection's; run_layers swaps in off_out1 for the down projection
+    }
+  }
+}
+
+extern "C" duet_status duet_ctx_ar_handle(duet_ctx* c, void* out, int32_t len) {
+  clear_error();
+  if (!c || !out || len < (int32_t)sizeof(cudaIpcMemHandle_t))
+    DUET_FAIL(DUET_ERR_INVALID_ARG, "ctx / out is NULL or len < %d", (int)sizeof(cudaIpcMemHandle_t));
+  if (!c->comm_pre) DUET_FAIL(DUET_ERR_INVALID_ARG, "duet_ctx_set_comms first (the rank and the group)");
+  if (c->spec.tp > kMaxTp) DUET_FAIL(DUET_ERR_UNSUPPORTED, "tp = %d > %d", c->spec.tp, kMaxTp);
+  if (c->dt != DT::BF16) DUET_FAIL(DUET_ERR_UNSUPPORTED, "the fused allreduce runs on the bf16 CTA-pair GEMM");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (!c->ar_arena) {
+    const int n = c->spec.tp, d = c->spec.d_model;
+    Side* sides[2] = {&c->dec, &c->pre};
+    size_t off = 0;
+    for (int i = 0; i < 2; ++i) {
+      const int R = std::max(sides[i]->cap_rows, 1);
+      auto& L = c->ar_lay[i];
+      L.off_slots = off;
+      off = align256(off + gemm_ar_slot_floats(R, d, n) * sizeof(float));
+      L.off_cnt = off;
+      off = align256(off + (gemm_ar_counters(R, d, n) + 1) * sizeof(unsigned));
+      L.off_out0 = off;
+      off = align256(off + (size_t)R * d * 2);
+      L.off_out1 = off;
+      off = align256(off + (size_t)R * d * 2);
+    }
+    char* a = nullptr;
+    CUDA_TRY(cudaMalloc(&a, off));
+    CUDA_TRY(cudaMemset(a, 0, off));  // counters start at zero (their waiters re-arm them)
+    c->ar_arena = a;
+    c->ar_bytes = off;
+  }
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->ar_arena));
+  memcpy(out, &h, sizeof(h));
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_ctx_ar_open(duet_ctx* c, int32_t n, const void* handles) {
+  clear_error();
+  if (!c || !handles) DUET_FAIL(DUET_ERR_INVALID_ARG, "ctx / handles is NULL");
+  if (!c->ar_arena) DUET_FAIL(DUET_ERR_INVALID_ARG, "duet_ctx_ar_handle first");
+  if (n != c->spec.tp) DUET_FAIL(DUET_ERR_INVALID_ARG, "%d handles for a tp = %d group", n, c->spec.tp);
+  if (c->ar_on) DUET_FAIL(DUET_ERR_INVALID_ARG, "the fused allreduce is already open");
+  CUDA_TRY(cudaSetDevice(c->device));
+  for (int r = 0; r < n; ++r) {
+    if (r == c->tp_rank) {
+      c->ar_peer[r] = c->ar_arena;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char*)handles + (size_t)r * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->ar_peer[r] = (char*)p;
+  }
+  ar_fill_groups(c);
+  cudaDeviceSynchronize();  // captured graphs use the NCCL allreduce: drop them
+  for (auto& kv : c->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  for (auto& kv : c->pre_graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  c->graphs.clear();
+  c->pre_graphs.clear();
+  c->ar_on = true;
+  return DUET_OK;
+}
+
+extern "C" duet_status duet_op_gemm_ar_emul(duet_ctx* c, int32_t n_ranks, const void* A, const void* B, const void* R,
+                                           void* C, int32_t M, int32_t N, int32_t K, void* stream) {
+  clear_error();
+  if (!c || !A || !B || !R || !C) DUET_FAIL(DUET_ERR_INVALID_ARG, "NULL operand");
+  if (n_ranks < 1 || n_ranks > kMaxTp) DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "n_ranks = %d (1..%d)", n_ranks, kMaxTp);
+  if (c->dt != DT::BF16) DUET_FAIL(DUET_ERR_UNSUPPORTED, "bf16 ctx only");
+  if (M <= 128 || N <= 0 || N % 32 || K <= 0 || K % 64)
+    DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "shape M=%d N=%d K=%d (M > 128, N %% 32 == 0, K %% 64 == 0)", M, N, K);
+  if (n_ranks > c->total_sms / 2) DUET_FAIL(DUET_ERR_UNSUPPORTED, "%d ranks need >= %d SMs", n_ranks, 2 * n_ranks);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t sf = gemm_ar_slot_floats(M, N, n_ranks), cn = gemm_ar_counters(M, N, n_ranks) + 1;
+  if (sf * n_ranks > c->emu_slot_floats) {
+    if (c->emu_slots) CUDA_TRY(cudaFree(c->emu_slots));
+    c->emu_slots = nullptr;
+    c->emu_slot_floats = 0;
+    CUDA_TRY(cudaMalloc(&c->emu_slots, sf * n_ranks * sizeof(float)));
+    c->emu_slot_floats = sf * n_ranks;
+  }
+  if (cn * n_ranks > c->emu_cnt_n) {
+    if (c->emu_cnt) CUDA_TRY(cudaFree(c->emu_cnt));
+    c->emu_cnt = nullptr;
+    c->emu_cnt_n = 0;
+    CUDA_TRY(cudaMalloc(&c->emu_cnt, cn * n_ranks * sizeof(unsigned)));
+    CUDA_TRY(cudaMemset(c->emu_cnt, 0, cn * n_ranks * sizeof(unsigned)));
+    c->emu_cnt_n = cn * n_ranks;
+  }
+  GemmAr ar;
+  ar.n = n_ranks;
+  ar.rank = 0;
+  ar.emul = 1;
+  for (int r = 0; r < n_ranks; ++r) {
+    ar.slots[r] = c->emu_slots + (size_t)r * sf;
+    ar.cnt[r] = c->emu_cnt + (size_t)r * cn;
+    ar.done[r] = ar.cnt[r] + cn - 1;
+    ar.out[r] = (char*)C + (size_t)r * M * N * 2;
+  }
+  GemmArgs g{A, B, nullptr, R, nullptr, M, N, K, K, K, N, N, EPI_RESIDUAL_AR};
+  g.ar = &ar;
+  if (!gemm2_supported(g, c->total_sms)) DUET_FAIL(DUET_ERR_UNSUPPORTED, "operands misaligned for the CTA-pair GEMM");
+  if (launch_gemm2(g, c->total_sms, (cudaStream_t)stream) <= 0)
+    DUET_FAIL(DUET_ERR_UNSUPPORTED, "fused GEMM + allreduce M=%d N=%d K=%d could not be launched", M, N, K);
+  DUET_TRY(check_launch("gemm_ar_emul"));
   return DUET_OK;
 }
 

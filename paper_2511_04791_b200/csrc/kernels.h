@@ -18,7 +18,32 @@ inline size_t dt_size(DT t) { return t == DT::BF16 ? 2 : 4; }
 //                C[m][j] = silu(acc_gate) * acc_up
 //  EPI_QKV_ROPE: C = acc (+ bias) for the q heads after RoPE; k heads (RoPE) and v heads are written to
 //                their paged KV slots instead (QKV GEMM + RoPE + KV append fused; CTA-pair kernel only)
-enum { EPI_STORE = 0, EPI_RESIDUAL = 1, EPI_SWIGLU = 2, EPI_QKV_ROPE = 3 };
+//  EPI_RESIDUAL_AR: row-parallel GEMM + allreduce fused: every rank's
+//                C = R + sum over the tp ranks of their A_r . B_r^T; the partial tiles are exchanged
+//                inside the epilogue over peer memory (GemmAr; CTA-pair kernel only)
+enum { EPI_STORE = 0, EPI_RESIDUAL = 1, EPI_SWIGLU = 2, EPI_QKV_ROPE = 3, EPI_RESIDUAL_AR = 4 };
+
+// Fused GEMM + allreduce (EPI_RESIDUAL_AR).  Tile t (256 x 256 outputs, grouped order of the CTA-pair
+// kernel) is owned by rank t % n.  Every non-owner pushes its fp32 partial tile into the owner's receive
+// slot and releases a per-(tile, warp) arrival counter there; the owner sums the n partials in rank order
+// 0..n-1 (its own from TMEM), adds R, rounds once to bf16 and stores the rows into every rank's output
+// (all-gather by push), releasing each rank's completion counter; one CTA per rank waits for its
+// completion counter before the grid ends.  All waits poll local memory; every remote access is a
+// store or a release-add.  Counters are reset by their waiter, so a launch (or a graph replay) needs no
+// epoch.  Pointers of rank r: on a real TP group peer-mapped (cudaIpc), for emulation local buffers.
+constexpr int kMaxTp = 8;
+struct GemmAr {
+  int n = 1;              // ranks (<= kMaxTp)
+  int rank = 0;           // this rank (emul = 0)
+  int emul = 0;           // 1: all n ranks run in this one grid (one GPU; A / B stacked per rank)
+  float* slots[kMaxTp];   // rank r's receive slots [owned tile][sender][256][256] fp32
+  void* out[kMaxTp];      // rank r's output C (same pitch ldc on every rank)
+  unsigned* cnt[kMaxTp];  // rank r's arrival counters [owned tile][8], zero between launches
+  unsigned* done[kMaxTp]; // rank r's completion counter, zero between launches
+};
+// receive-slot floats / counters one rank needs for an M x N output over n ranks
+size_t gemm_ar_slot_floats(int M, int N, int n);
+size_t gemm_ar_counters(int M, int N, int n);
 
 struct GemmArgs {
   const void* A;
@@ -41,6 +66,8 @@ struct GemmArgs {
   int row_split = 1 << 30;
   // EPI_QKV_ROPE: the RoPE / KV-append operands (kernels.h RopeKvArgs; head_dim 128, page size 16)
   const struct RopeKvArgs* rope = nullptr;
+  // EPI_RESIDUAL_AR: the tp group (C is ignored: outputs go to ar->out[r])
+  const struct GemmAr* ar = nullptr;
 };
 // fp32 partial floats a split-K launch of this shape needs (0 when it runs unsplit)
 size_t gemm_tc_splitk_need(int M, int N, int K, int epi);

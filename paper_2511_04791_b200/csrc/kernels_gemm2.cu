@@ -151,7 +151,24 @@ struct Params {
   // gemm2_reduce_kernel sums the chunks in order 0..ksplit-1 and applies the epilogue
   int ksplit, kb_per;
   float* ws;
+  // EPI_RESIDUAL_AR (f3): the tp group; emulation (ar.emul) runs rank r on pairs [r ppr, (r + 1) ppr) and
+  // reads its operands at X rows r * xrows and W rows r * wrows of the stacked inputs
+  GemmAr ar;
+  int ar_ppr, ar_xrows, ar_wrows;
 };
+
+// system-scope release / acquire on the counters of the fused allreduce (peer memory over NVLink)
+__device__ __forceinline__ void red_release_sys(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // Tile order (grouped rasterization): tiles run in groups of GROUP_M 256-row blocks; inside a group the
 // row block varies fastest, so the pairs of one wave share a few weight column blocks (read once from
@@ -193,7 +210,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  // EPI_RESIDUAL_AR: this CTA's rank (emulation: the grid holds every rank's pairs) and the row offsets
+  // of that rank's operands in the stacked X / W
+  int ar_r = 0, xoff = 0, woff = 0;
+  if constexpr (EPI == EPI_RESIDUAL_AR) {
+    if (p.ar.emul) {
+      ar_r = pair / p.ar_ppr;
+      pair -= ar_r * p.ar_ppr;
+      n_pairs = p.ar_ppr;
+      xoff = ar_r * p.ar_xrows;
+      woff = ar_r * p.ar_wrows;
+    } else {
+      ar_r = p.ar.rank;
+    }
+  }
   const int num_k = p.K / BK;
   const int num_units = p.num_tiles * p.ksplit;
 
@@ -232,7 +263,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
   if (warp != 0 && role < 0) pdl_wait();
 
   auto w_row_of = [&](int nb) {
-    return EPI == EPI_SWIGLU ? (rank ? p.n_up_off : 0) + nb * B_ROWS : nb * BN_PAIR + (int)rank * B_ROWS;
+    return EPI == EPI_SWIGLU ? (rank ? p.n_up_off : 0) + nb * B_ROWS : woff + nb * BN_PAIR + (int)rank * B_ROWS;
   };
   if (role >= 0) {
     if (lane == 0) {
@@ -247,7 +278,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
         const int t = u % p.num_tiles, kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
         int mp, nb;
         tile_coords(t, p.num_m2, p.num_n, mp, nb);
-        const int row_x = mp * PAIR_M + (int)rank * BM;
+        const int row_x = xoff + mp * PAIR_M + (int)rank * BM;
         const int row_w = w_row_of(nb);
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           if (par < 0 || (int)(g & 1) == par) {
@@ -273,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
       auto w_row = [&](int nb) {
-        return EPI == EPI_SWIGLU ? (rank ? p.n_up_off : 0) + nb * B_ROWS : nb * BN_PAIR + (int)rank * B_ROWS;
+        return EPI == EPI_SWIGLU ? (rank ? p.n_up_off : 0) + nb * B_ROWS : woff + nb * BN_PAIR + (int)rank * B_ROWS;
       };
       int pre = 0;
 #ifndef DUET_NO_WPREFETCH
@@ -297,7 +328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
         const int t = u % p.num_tiles, kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
         int mp, nb;
         tile_coords(t, p.num_m2, p.num_n, mp, nb);
-        const int row_x = mp * PAIR_M + (int)rank * BM;
+        const int row_x = xoff + mp * PAIR_M + (int)rank * BM;
         const int row_w = w_row(nb);
         for (int kb = kb0; kb < kb1; ++kb) {
           const uint32_t lbar = mapa(smem_u32(&full[s]), 0);
@@ -399,6 +430,88 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
           if (lane == 0) mbar_arrive_cluster(leader_tempty0 + acc * 8);
           continue;
         }
+      }
+      if constexpr (EPI == EPI_RESIDUAL_AR) {
+        // f3: tile t belongs to rank t % n.  This warp's 32 rows x 256 columns of the partial either go to
+        // the owner's receive slot (sender) or are summed with the n - 1 received partials (owner).
+        const int E = p.ar.n, owner = t % E, ot = t / E;
+        const int wslot = (int)rank * 4 + quad;       // 8 (CTA, warp) row groups per tile
+        const int trow = (int)rank * BM + lane_row;   // row within the 256-row tile
+        if (owner != ar_r) {
+          float* dst = p.ar.slots[owner] + (((size_t)ot * E + ar_r) * PAIR_M + trow) * BN;
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            float v[32];
+            tmem_ld32(tbase + c, v);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              __stcg(reinterpret_cast<float4*>(dst + c + 4 * q), make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+          }
+          __threadfence_system();  // this lane's partial rows before the warp's release
+          __syncwarp();
+          if (lane == 0) red_release_sys(p.ar.cnt[owner] + (size_t)ot * 8 + wslot, 1u);
+        } else {
+          unsigned* cnt = p.ar.cnt[ar_r] + (size_t)ot * 8 + wslot;
+          if (lane == 0) {
+            while (ld_acquire_sys(cnt) < (unsigned)(E - 1)) {
+            }
+            st_relaxed_sys(cnt, 0u);  // re-armed: no sender touches it again before this grid ends
+          }
+          __syncwarp();
+          const bool row_ok = row < p.M;
+          const float* slot0 = p.ar.slots[ar_r] + ((size_t)ot * E * PAIR_M + trow) * BN;
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            float v[32], sum[32];
+            tmem_ld32(tbase + c, v);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) sum[e] = 0.f;
+            for (int sr = 0; sr < E; ++sr) {  // fixed rank order: every rank receives the same sum
+              if (sr == ar_r) {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) sum[e] += v[e];
+              } else {
+                const float* src = slot0 + (size_t)sr * PAIR_M * BN + c;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  const float4 f = __ldcg(reinterpret_cast<const float4*>(src + 4 * q));
+                  sum[4 * q] += f.x;
+                  sum[4 * q + 1] += f.y;
+                  sum[4 * q + 2] += f.z;
+                  sum[4 * q + 3] += f.w;
+                }
+              }
+            }
+            if (row_ok && n0 + c < p.N) {  // N % 32 == 0 (gemm2_supported)
+              const bf16* rsrc = p.R + (size_t)row * p.ldr + n0 + c;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                float rf[8];
+                load16<bf16>(rsrc + q * 8, rf);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) sum[q * 8 + e] += rf[e];
+              }
+              for (int dr = 0; dr < E; ++dr) {  // all-gather by push
+                bf16* dst = (bf16*)p.ar.out[dr] + (size_t)row * p.ldc + n0 + c;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  float o8[8];
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) o8[e] = sum[q * 8 + e];
+                  store16<bf16>(dst + q * 8, o8);
+                }
+              }
+            }
+          }
+          __threadfence_system();
+          __syncwarp();
+          if (lane == 0)
+            for (int dr = 0; dr < E; ++dr) red_release_sys(p.ar.done[dr], 1u);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_tempty0 + acc * 8);
+        continue;
       }
       if constexpr (EPI == EPI_QKV_ROPE) {
         // the tile's BN columns are BN / 128 whole heads (d_h = 128): rotate (i, i + 64) pairs of q and k
@@ -528,6 +641,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
       if (lane == 0) mbar_arrive_cluster(leader_tempty0 + acc * 8);  // the leader's tempty[acc]
     }
   }
+  if constexpr (EPI == EPI_RESIDUAL_AR) {
+    // one CTA per rank holds the grid open until every tile of the result has arrived in this rank's output
+    // (pushed by the tiles' owners), then re-arms the counter for the next launch
+    if (warp == 2 && lane == 0 && rank == 0 && pair == 0) {
+      unsigned* d = p.ar.done[ar_r];
+      while (ld_acquire_sys(d) < (unsigned)(p.num_tiles * 8)) {
+      }
+      st_relaxed_sys(d, 0u);
+    }
+  }
   tc_fence_before();
   cluster_sync();  // no CTA leaves while its peer may still signal its barriers or read its smem
   if (warp == 1) {
@@ -623,8 +746,11 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
     attr = true;
   }
   CUtensorMap mx, mw;
-  const int w_rows = EPI == EPI_SWIGLU ? 2 * a.N : a.N;
-  if (!make_map(&mx, a.A, a.M, a.K, a.lda, BM) || !make_map(&mw, a.B, w_rows, a.K, a.ldb, CF::B_ROWS)) return -1;
+  // f3 emulation: the E ranks' X and W are stacked row-wise ([E][M][K], [E][N][K])
+  const int n_emul = (EPI == EPI_RESIDUAL_AR && a.ar && a.ar->emul) ? a.ar->n : 1;
+  const int w_rows = EPI == EPI_SWIGLU ? 2 * a.N : a.N * n_emul;
+  if (!make_map(&mx, a.A, a.M * n_emul, a.K, a.lda, BM) || !make_map(&mw, a.B, w_rows, a.K, a.ldb, CF::B_ROWS))
+    return -1;
   Params p{};
   p.M = a.M;
   p.N = a.N;
@@ -659,7 +785,19 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   p.ksplit = (num_k + p.kb_per - 1) / p.kb_per;
   p.ws = a.ws;
   const int units = p.num_tiles * p.ksplit;
-  const int pairs = units < num_sms / 2 ? units : num_sms / 2;
+  int pairs = units < num_sms / 2 ? units : num_sms / 2;
+  if constexpr (EPI == EPI_RESIDUAL_AR) {
+    if (!a.ar || BN != 256 || p.ksplit != 1) return -1;
+    p.ar = *a.ar;
+    if (n_emul > 1) {  // every emulated rank's pairs resident at once (their owners wait on each other)
+      pairs = std::min(units, num_sms / 2 / n_emul);
+      if (pairs < 1) return -1;
+      p.ar_xrows = a.M;
+      p.ar_wrows = a.N;
+    }
+    p.ar_ppr = pairs;
+    pairs *= n_emul;
+  }
   launch_pdl(gemm2_kernel<EPI, BN, PROD>, 2 * pairs, THREADS + (PROD - 1) * 32, CF::SMEM, st, mx, mw, p);
   if (p.ksplit > 1) {
     if constexpr (EPI == EPI_STORE || EPI == EPI_RESIDUAL) {
@@ -677,14 +815,17 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
 // split-K 66.5 us (profiles/r02_gemm2_tile_ab.txt).  DUET_GEMM2_BN = 128 / 256 forces one width (A/B).
 template <int EPI>
 static int launch_w(const GemmArgs& a, int num_sms, cudaStream_t st) {
-  static const int force = getenv("DUET_GEMM2_BN") ? atoi(getenv("DUET_GEMM2_BN")) : 0;
-  const bool narrow = force == 128;
-  // DUET_GEMM2_PROD = 1 / 2 / 4: producer warps (A/B); default 2 (4 measured equal, 1 within 1 %)
-  static const int prod = getenv("DUET_GEMM2_PROD") ? atoi(getenv("DUET_GEMM2_PROD")) : 2;
-  if (prod == 1) return narrow ? launch<EPI, 128, 1>(a, num_sms, st) : launch<EPI, 256, 1>(a, num_sms, st);
-  if (prod == 4) return narrow ? launch<EPI, 128, 4>(a, num_sms, st) : launch<EPI, 256, 4>(a, num_sms, st);
-  if (prod == 2) return narrow ? launch<EPI, 128, 2>(a, num_sms, st) : launch<EPI, 256, 2>(a, num_sms, st);
-  return narrow ? launch<EPI, 128, 2>(a, num_sms, st) : launch<EPI, 256, 2>(a, num_sms, st);
+  if constexpr (EPI == EPI_RESIDUAL_AR) {
+    return launch<EPI, 256, 2>(a, num_sms, st);  // 256 x 256 receive slots
+  } else {
+    static const int force = getenv("DUET_GEMM2_BN") ? atoi(getenv("DUET_GEMM2_BN")) : 0;
+    const bool narrow = force == 128;
+    // DUET_GEMM2_PROD = 1 / 2 / 4: producer warps (A/B); default 2 (4 measured equal, 1 within 1 %)
+    static const int prod = getenv("DUET_GEMM2_PROD") ? atoi(getenv("DUET_GEMM2_PROD")) : 2;
+    if (prod == 1) return narrow ? launch<EPI, 128, 1>(a, num_sms, st) : launch<EPI, 256, 1>(a, num_sms, st);
+    if (prod == 4) return narrow ? launch<EPI, 128, 4>(a, num_sms, st) : launch<EPI, 256, 4>(a, num_sms, st);
+    return narrow ? launch<EPI, 128, 2>(a, num_sms, st) : launch<EPI, 256, 2>(a, num_sms, st);
+  }
 }
 
 }  // namespace tc2
@@ -703,10 +844,24 @@ size_t gemm2_splitk_need(int M, int N, int K, int epi) {
   return need;
 }
 
+size_t gemm_ar_slot_floats(int M, int N, int n) {
+  const size_t tiles = (size_t)((M + tc2::PAIR_M - 1) / tc2::PAIR_M) * ((N + 255) / 256);
+  return ((tiles + n - 1) / n) * n * tc2::PAIR_M * 256;
+}
+size_t gemm_ar_counters(int M, int N, int n) {
+  const size_t tiles = (size_t)((M + tc2::PAIR_M - 1) / tc2::PAIR_M) * ((N + 255) / 256);
+  return ((tiles + n - 1) / n) * 8;
+}
+
 bool gemm2_supported(const GemmArgs& a, int num_sms) {
   static const bool on = !getenv("DUET_GEMM2") || atoi(getenv("DUET_GEMM2")) != 0;  // A/B switch
   auto mis = [](const void* p) { return ((uintptr_t)p & 15) != 0; };  // TMA / 16-B epilogue alignment
   if (mis(a.A) || mis(a.B) || mis(a.C) || mis(a.R) || mis(a.R2) || mis(a.C2)) return false;
+  if (a.epi == EPI_RESIDUAL_AR) {
+    if (!a.ar || a.ar->n < 1 || a.ar->n > kMaxTp || !a.R || a.N % 32 || a.row_split < a.M || a.C2 || a.R2) return false;
+    for (int r = 0; r < a.ar->n; ++r)
+      if (!a.ar->slots[r] || !a.ar->cnt[r] || !a.ar->done[r] || !a.ar->out[r] || mis(a.ar->out[r])) return false;
+  }
   return on && a.M > 128 && num_sms >= 2 && a.K % tc2::BK == 0 && a.lda % 8 == 0 && a.ldb % 8 == 0 &&
          a.ldc % 8 == 0 && (!a.R || a.ldr % 8 == 0) && (a.epi != EPI_SWIGLU || a.N % 128 == 0) &&
          (a.epi != EPI_QKV_ROPE || a.N % 128 == 0);
@@ -716,6 +871,7 @@ int launch_gemm2(const GemmArgs& a, int num_sms, cudaStream_t st) {
   if (a.epi == EPI_QKV_ROPE) return a.rope ? tc2::launch_w<EPI_QKV_ROPE>(a, num_sms, st) : -1;
   if (a.epi == EPI_SWIGLU) return tc2::launch_w<EPI_SWIGLU>(a, num_sms, st);
   if (a.epi == EPI_RESIDUAL) return tc2::launch_w<EPI_RESIDUAL>(a, num_sms, st);
+  if (a.epi == EPI_RESIDUAL_AR) return tc2::launch_w<EPI_RESIDUAL_AR>(a, num_sms, st);
   return tc2::launch_w<EPI_STORE>(a, num_sms, st);
 }
 
