@@ -331,6 +331,18 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def open_fused_allreduce(ctx, group=None):
+    """f3 plumbing over torch.distributed: all-gather every rank's fused-allreduce arena handle
+    (duet_ctx_ar_handle, 64 bytes) in rank order and map the peers' arenas (duet_ctx_ar_open).
+    Collective over the group; every rank's ctx must have its communicators set."""
+    import torch.distributed as dist
+    h = ctx.ar_handle()
+    hs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(hs, h, group=group)
+    ctx.ar_open(hs)
+    return hs
+
+
 class Ctx:
     """Owns a duet_ctx.  Device tensors are torch tensors (plumbing only)."""
 

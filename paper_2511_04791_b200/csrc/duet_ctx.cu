@@ -1494,7 +1494,8 @@ static void ar_fill_groups(duet_ctx* c) {
     g.n = n;
     g.rank = c->tp_rank;
     g.emul = 0;
-    const size_t ncnt = gemm_ar_counters(std::max(sides[i]->cap_rows, 1), d, n);
+    g.slot_tiles = gemm_ar_slot_tiles(std::max(sides[i]->cap_rows, 1), d, n, c->total_sms);
+    const size_t ncnt = gemm_ar_counters(std::max(sides[i]->cap_rows, 1), d, n, c->total_sms);
     for (int r = 0; r < n; ++r) {
       char* b = c->ar_peer[r];
       g.slots[r] = (float*)(b + L.off_slots);
@@ -1521,9 +1522,9 @@ extern "C" duet_status duet_ctx_ar_handle(duet_ctx* c, void* out, int32_t len) {
       const int R = std::max(sides[i]->cap_rows, 1);
       auto& L = c->ar_lay[i];
       L.off_slots = off;
-      off = align256(off + gemm_ar_slot_floats(R, d, n) * sizeof(float));
+      off = align256(off + gemm_ar_slot_floats(R, d, n, c->total_sms) * sizeof(float));
       L.off_cnt = off;
-      off = align256(off + (gemm_ar_counters(R, d, n) + 1) * sizeof(unsigned));
+      off = align256(off + (gemm_ar_counters(R, d, n, c->total_sms) + 1) * sizeof(unsigned));
       L.off_out0 = off;
       off = align256(off + (size_t)R * d * 2);
       L.off_out1 = off;
@@ -1581,7 +1582,8 @@ extern "C" duet_status duet_op_gemm_ar_emul(duet_ctx* c, int32_t n_ranks, const 
     DUET_FAIL(DUET_ERR_OUT_OF_RANGE, "shape M=%d N=%d K=%d (M > 128, N %% 32 == 0, K %% 64 == 0)", M, N, K);
   if (n_ranks > c->total_sms / 2) DUET_FAIL(DUET_ERR_UNSUPPORTED, "%d ranks need >= %d SMs", n_ranks, 2 * n_ranks);
   CUDA_TRY(cudaSetDevice(c->device));
-  const size_t sf = gemm_ar_slot_floats(M, N, n_ranks), cn = gemm_ar_counters(M, N, n_ranks) + 1;
+  const size_t sf = gemm_ar_slot_floats(M, N, n_ranks, c->total_sms),
+               cn = gemm_ar_counters(M, N, n_ranks, c->total_sms) + 1;
   if (sf * n_ranks > c->emu_slot_floats) {
     if (c->emu_slots) CUDA_TRY(cudaFree(c->emu_slots));
     c->emu_slots = nullptr;
@@ -1601,6 +1603,7 @@ extern "C" duet_status duet_op_gemm_ar_emul(duet_ctx* c, int32_t n_ranks, const 
   ar.n = n_ranks;
   ar.rank = 0;
   ar.emul = 1;
+  ar.slot_tiles = gemm_ar_slot_tiles(M, N, n_ranks, c->total_sms);
   for (int r = 0; r < n_ranks; ++r) {
     ar.slots[r] = c->emu_slots + (size_t)r * sf;
     ar.cnt[r] = c->emu_cnt + (size_t)r * cn;

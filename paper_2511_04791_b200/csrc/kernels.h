@@ -23,8 +23,8 @@ inline size_t dt_size(DT t) { return t == DT::BF16 ? 2 : 4; }
 //                inside the epilogue over peer memory (GemmAr; CTA-pair kernel only)
 enum { EPI_STORE = 0, EPI_RESIDUAL = 1, EPI_SWIGLU = 2, EPI_QKV_ROPE = 3, EPI_RESIDUAL_AR = 4 };
 
-// Fused GEMM + allreduce (EPI_RESIDUAL_AR).  Tile t (256 x 256 outputs, grouped order of the CTA-pair
-// kernel) is owned by rank t % n.  Every non-owner pushes its fp32 partial tile into the owner's receive
+// Fused GEMM + allreduce (EPI_RESIDUAL_AR).  Each 256 x 256 output tile has one owner rank (rotating along
+// every CTA pair's tile sequence, identical on all ranks).  Every non-owner pushes its fp32 partial tile into the owner's receive
 // slot and releases a per-(tile, warp) arrival counter there; the owner sums the n partials in rank order
 // 0..n-1 (its own from TMEM), adds R, rounds once to bf16 and stores the rows into every rank's output
 // (all-gather by push), releasing each rank's completion counter; one CTA per rank waits for its
@@ -36,14 +36,17 @@ struct GemmAr {
   int n = 1;              // ranks (<= kMaxTp)
   int rank = 0;           // this rank (emul = 0)
   int emul = 0;           // 1: all n ranks run in this one grid (one GPU; A / B stacked per rank)
-  float* slots[kMaxTp];   // rank r's receive slots [owned tile][sender][256][256] fp32
+  float* slots[kMaxTp];   // rank r's receive slots [owned tile][sender][256 cols][256 rows] fp32
   void* out[kMaxTp];      // rank r's output C (same pitch ldc on every rank)
   unsigned* cnt[kMaxTp];  // rank r's arrival counters [owned tile][8], zero between launches
   unsigned* done[kMaxTp]; // rank r's completion counter, zero between launches
+  size_t slot_tiles = 0;  // owned-tile capacity of every rank's slots / counters (gemm_ar_slot_tiles)
 };
-// receive-slot floats / counters one rank needs for an M x N output over n ranks
-size_t gemm_ar_slot_floats(int M, int N, int n);
-size_t gemm_ar_counters(int M, int N, int n);
+// owned-tile slots, receive-slot floats and counters one rank needs for an M x N output over n ranks on
+// any grid of <= num_sms / 2 CTA pairs
+size_t gemm_ar_slot_tiles(int M, int N, int n, int num_sms);
+size_t gemm_ar_slot_floats(int M, int N, int n, int num_sms);
+size_t gemm_ar_counters(int M, int N, int n, int num_sms);
 
 struct GemmArgs {
   const void* A;

@@ -432,24 +432,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
         }
       }
       if constexpr (EPI == EPI_RESIDUAL_AR) {
-        // f3: tile t belongs to rank t % n.  This warp's 32 rows x 256 columns of the partial either go to
+        // f3: each tile belongs to one owner rank.  This warp's 32 rows x 256 columns of the partial either go to
         // the owner's receive slot (sender) or are summed with the n - 1 received partials (owner).
-        const int E = p.ar.n, owner = t % E, ot = t / E;
+        // ownership rotates along each pair's unit sequence (owner = (i + pair) mod E), so every pair — on
+        // every rank — does the owner's reduction on 1 / E of its tiles (owner = t mod E would leave a pair
+        // owning all or none of its tiles whenever E divides the pair count); ot indexes the owner's slots
+        const int E = p.ar.n, owner = (i + pair) % E, ot = (i / E) * n_pairs + pair;
         const int wslot = (int)rank * 4 + quad;       // 8 (CTA, warp) row groups per tile
         const int trow = (int)rank * BM + lane_row;   // row within the 256-row tile
         if (owner != ar_r) {
-          float* dst = p.ar.slots[owner] + (((size_t)ot * E + ar_r) * PAIR_M + trow) * BN;
+          // slot layout [column][row] (column-major tile): for each column the warp's 32 rows are one
+          // coalesced 128-B segment, on the store here and on the owner's load
+          float* dst = p.ar.slots[owner] + ((size_t)ot * E + ar_r) * PAIR_M * BN + trow;
 #pragma unroll 1
           for (int c = 0; c < BN; c += 32) {
             float v[32];
             tmem_ld32(tbase + c, v);
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              __stcg(reinterpret_cast<float4*>(dst + c + 4 * q), make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+            for (int e = 0; e < 32; ++e) __stcg(dst + (size_t)(c + e) * PAIR_M, v[e]);
           }
-          __threadfence_system();  // this lane's partial rows before the warp's release
+          // the warp's rows are ordered before lane 0's system-scope fence by the warp barrier (cumulativity),
+          // one fence per warp and tile instead of one per lane
           __syncwarp();
-          if (lane == 0) red_release_sys(p.ar.cnt[owner] + (size_t)ot * 8 + wslot, 1u);
+          if (lane == 0) {
+            __threadfence_system();
+            red_release_sys(p.ar.cnt[owner] + (size_t)ot * 8 + wslot, 1u);
+          }
         } else {
           unsigned* cnt = p.ar.cnt[ar_r] + (size_t)ot * 8 + wslot;
           if (lane == 0) {
@@ -459,7 +467,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
           }
           __syncwarp();
           const bool row_ok = row < p.M;
-          const float* slot0 = p.ar.slots[ar_r] + ((size_t)ot * E * PAIR_M + trow) * BN;
+          const float* slot0 = p.ar.slots[ar_r] + (size_t)ot * E * PAIR_M * BN + trow;
 #pragma unroll 1
           for (int c = 0; c < BN; c += 32) {
             float v[32], sum[32];
@@ -471,18 +479,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
 #pragma unroll
                 for (int e = 0; e < 32; ++e) sum[e] += v[e];
               } else {
-                const float* src = slot0 + (size_t)sr * PAIR_M * BN + c;
+                const float* src = slot0 + (size_t)sr * PAIR_M * BN + (size_t)c * PAIR_M;
+                float f[32];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  const float4 f = __ldcg(reinterpret_cast<const float4*>(src + 4 * q));
-                  sum[4 * q] += f.x;
-                  sum[4 * q + 1] += f.y;
-                  sum[4 * q + 2] += f.z;
-                  sum[4 * q + 3] += f.w;
-                }
+                for (int e = 0; e < 32; ++e) f[e] = __ldcg(src + (size_t)e * PAIR_M);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) sum[e] += f[e];
               }
             }
-            if (row_ok && n0 + c < p.N) {  // N % 32 == 0 (gemm2_supported)
+            const bool col_ok = row_ok && n0 + c < p.N;  // N % 32 == 0 (gemm2_supported)
+            if (col_ok) {
               const bf16* rsrc = p.R + (size_t)row * p.ldr + n0 + c;
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
@@ -503,10 +509,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
               }
             }
           }
-          __threadfence_system();
           __syncwarp();
-          if (lane == 0)
+          if (lane == 0) {
+            __threadfence_system();
             for (int dr = 0; dr < E; ++dr) red_release_sys(p.ar.done[dr], 1u);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -789,6 +796,9 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
   if constexpr (EPI == EPI_RESIDUAL_AR) {
     if (!a.ar || BN != 256 || p.ksplit != 1) return -1;
     p.ar = *a.ar;
+    const int per_rank = n_emul > 1 ? std::min(units, num_sms / 2 / n_emul) : pairs;
+    const int upp = (units + per_rank - 1) / per_rank;  // units of the busiest pair
+    if ((size_t)((upp + a.ar->n - 1) / a.ar->n) * per_rank > a.ar->slot_tiles) return -1;  // owned-slot capacity
     if (n_emul > 1) {  // every emulated rank's pairs resident at once (their owners wait on each other)
       pairs = std::min(units, num_sms / 2 / n_emul);
       if (pairs < 1) return -1;
@@ -844,14 +854,16 @@ size_t gemm2_splitk_need(int M, int N, int K, int epi) {
   return need;
 }
 
-size_t gemm_ar_slot_floats(int M, int N, int n) {
+size_t gemm_ar_slot_tiles(int M, int N, int n, int num_sms) {
+  // the owner's slot index is (i / n) * pairs + pair for unit i of a pair: < ceil(ceil(tiles / P) / n) * P,
+  // bounded over every grid size P <= num_sms / 2 by ceil(tiles / n) + 2 P
   const size_t tiles = (size_t)((M + tc2::PAIR_M - 1) / tc2::PAIR_M) * ((N + 255) / 256);
-  return ((tiles + n - 1) / n) * n * tc2::PAIR_M * 256;
+  return (tiles + n - 1) / n + (size_t)num_sms;
 }
-size_t gemm_ar_counters(int M, int N, int n) {
-  const size_t tiles = (size_t)((M + tc2::PAIR_M - 1) / tc2::PAIR_M) * ((N + 255) / 256);
-  return ((tiles + n - 1) / n) * 8;
+size_t gemm_ar_slot_floats(int M, int N, int n, int num_sms) {
+  return gemm_ar_slot_tiles(M, N, n, num_sms) * n * tc2::PAIR_M * 256;
 }
+size_t gemm_ar_counters(int M, int N, int n, int num_sms) { return gemm_ar_slot_tiles(M, N, n, num_sms) * 8; }
 
 bool gemm2_supported(const GemmArgs& a, int num_sms) {
   static const bool on = !getenv("DUET_GEMM2") || atoi(getenv("DUET_GEMM2")) != 0;  // A/B switch

@@ -100,3 +100,46 @@ def test_tp_head_sharded_oracle_equals_unsharded_gloo():
     for p in procs:
         p.join(timeout=120)
     assert err < 1e-12, err
+
+
+class _FakeArCtx:
+    """Stands in for D.Ctx in the f3 handle exchange (no GPU): a rank-specific 64-byte handle."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.opened = None
+
+    def ar_handle(self):
+        return bytes([65 + self.rank]) * 64
+
+    def ar_open(self, handles):
+        self.opened = list(handles)
+
+
+def _ar_worker(rank, ws, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    from paper_2511_04791_b200._native import open_fused_allreduce
+    c = _FakeArCtx(rank)
+    open_fused_allreduce(c)
+    q.put((rank, c.opened))
+    dist.destroy_process_group()
+
+
+def test_fused_allreduce_handle_exchange_gloo():
+    """f3 plumbing (D.open_fused_allreduce): every rank opens the group with all ranks' arena handles in
+    rank order — the layout duet_ctx_ar_open indexes its peer tables by (world size 2, gloo)."""
+    ws = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ar_worker, args=(r, ws, port, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(ws))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [bytes([65 + r]) * 64 for r in range(ws)]
+    assert res[0] == want and res[1] == want

@@ -1,6 +1,7 @@
 """Worker of tests/test_gpu_tp2.py (one process per GPU, launched by torch.distributed.run): rank r runs
 its head shard of a cfg2-mini mixed iteration (synth.tp: h_q/2 query heads, h_kv/2 kv heads, ffn/2
-columns) through libduet.so with real NCCL communicators, in temporal and spatial mode; the
+columns) through libduet.so with real NCCL communicators, in temporal and spatial mode, with the NCCL
+allreduce and with the fused GEMM + allreduce (f3, IPC-mapped peer arenas); the
 all-reduced layer outputs must equal the UNSHARDED oracle on every rank (§8 a9)."""
 import os
 import sys
@@ -32,7 +33,7 @@ def main():
     ids = [D.nccl_unique_id(), D.nccl_unique_id()] if rank == 0 else [None, None]
     dist.broadcast_object_list(ids, src=0)
     worst = 0.0
-    for mode in ("temporal", "spatial"):
+    for mode, fused in (("temporal", False), ("spatial", False), ("temporal", True), ("spatial", True)):
         src = wl1 if mode == "temporal" else wl
         g = GpuWorkload(src, "bf16")
         g.W = [TP.shard_layer_weights(w, m.n_q_heads, m.n_kv_heads, m.head_dim, m.ffn_dim, rank, ws) for w in g.W]
@@ -40,6 +41,8 @@ def main():
         g.V = [TP.shard_kv_pool(p, m.n_kv_heads, rank, ws) for p in g.V]
         ctx = make_ctx(replace(src, cfg=replace(src.cfg, model=replace(m, tp=ws))), "bf16")
         ctx.set_comms(rank, ids[0], ids[1])
+        if fused:  # f3: O / down + allreduce fused over peer memory (IPC-mapped arenas)
+            D.open_fused_allreduce(ctx)
         parts, total = ctx.partitions()
         split = D.split_struct(D.DUET_MODE_TEMPORAL, total, 0, 1) if mode == "temporal" else \
             D.split_struct(D.DUET_MODE_SPATIAL, total - parts[len(parts) // 2], parts[len(parts) // 2], 2)
@@ -50,7 +53,7 @@ def main():
         e = rel_err(g.y_pre.float().cpu().numpy(), yp)
         for j in range(src.k):
             e = max(e, rel_err(g.y_dec[j].float().cpu().numpy(), yd[j]))
-        print(f"rank {rank} {mode}: rel_err {e:.3e}", flush=True)
+        print(f"rank {rank} {mode}{' fused' if fused else ''}: rel_err {e:.3e}", flush=True)
         worst = max(worst, e)
         ctx.close()
     dist.destroy_process_group()
