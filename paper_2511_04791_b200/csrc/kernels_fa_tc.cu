@@ -24,6 +24,7 @@
 // zero-filled (cp.async src-size 0) and masked.  An odd last head of a group runs alone (has_b = 0).
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -199,11 +200,44 @@ struct Params {
   const int* cpre;
   const int* seq_row;
   const int* table;
-  int max_pages, hq, hkv, n_qtiles, n_pairs, trace;
+  int max_pages, hq, hkv, n_qtiles, n_pairs, trace, n_seqs;
   bf16* o;
   const bf16* k_pool;
   const bf16* v_pool;
 };
+
+// Work item = (sequence, 128-row query tile, GQA head pair).  Items are ordered heavy first (query tile
+// from the last, then sequence, then pair); a persistent CTA takes items k = 0, 1, ... of a snake order
+// over the grid (round r gives CTA b the item r G + b for even r, r G + G - 1 - b for odd r), so the heavy
+// and light items of consecutive rounds balance; with G = the item count every CTA takes one item (the
+// one-item-per-CTA launch).  Every warp role walks the same sequence and skips the same empty items.
+struct Item {
+  int s_id, qt, pair, qlen, row0, cpre, q0, kvh, head_a, n_heads, kv_end, n_kt;
+  const int* tab;
+};
+__device__ __forceinline__ bool item_at(const Params& p, int k, Item& it, bool& live) {
+  const int G = gridDim.x, T = p.n_qtiles * p.n_seqs * p.n_pairs;
+  const int idx = k * G + ((k & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
+  if (idx >= T) return false;
+  it.pair = idx % p.n_pairs;
+  it.s_id = (idx / p.n_pairs) % p.n_seqs;
+  it.qt = p.n_qtiles - 1 - idx / (p.n_pairs * p.n_seqs);
+  it.qlen = p.qlen[it.s_id];
+  live = it.qt * BQ < it.qlen;
+  if (!live) return true;
+  const int Gq = p.hq / p.hkv, ppg = (Gq + 1) / 2;
+  it.kvh = it.pair / ppg;
+  it.head_a = it.kvh * Gq + (it.pair % ppg) * 2;
+  it.n_heads = it.head_a + 1 < (it.kvh + 1) * Gq ? 2 : 1;
+  it.row0 = p.row0[it.s_id];
+  it.cpre = p.cpre[it.s_id];
+  it.tab = p.table + (size_t)p.seq_row[it.s_id] * p.max_pages;
+  it.q0 = it.qt * BQ;
+  const int q_last = min(it.q0 + BQ, it.qlen) - 1;
+  it.kv_end = it.cpre + q_last + 1;
+  it.n_kt = (it.kv_end + BKV - 1) / BKV;
+  return true;
+}
 
 template <int K_STAGES, int V_STAGES>
 __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant__ CUtensorMap map_q, Params p) {
@@ -219,30 +253,15 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   uint64_t* v_empty = v_full + V_STAGES;
   uint64_t* s_full = v_empty + V_STAGES;    // [head]
   uint64_t* p_full = s_full + 2;            // [head]
-  uint64_t* o_done = p_full + 2;            // [head]: the last PV
-  uint32_t* tmem_slot = (uint32_t*)(o_done + 2);
+  uint64_t* o_done = p_full + 2;            // [head]: the last PV of a work item
+  uint64_t* q_empty = o_done + 2;           // 1: the item's last S MMAs completed (Q tiles reusable)
+  uint32_t* tmem_slot = (uint32_t*)(q_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pair = blockIdx.x;
-  const int qt = p.n_qtiles - 1 - blockIdx.y;  // heavy (late) tiles first, all pairs of a tile together
-  const int s_id = blockIdx.z;
-  const int qlen = p.qlen[s_id];
-  if (qt * BQ >= qlen) return;
-  const int G = p.hq / p.hkv;
-  const int pairs_per_group = (G + 1) / 2;
-  const int kvh = pair / pairs_per_group;
-  const int head_a = kvh * G + (pair % pairs_per_group) * 2;
-  const bool has_b = head_a + 1 < (kvh + 1) * G;
-  const int n_heads = has_b ? 2 : 1;
-  const int row0 = p.row0[s_id], cpre = p.cpre[s_id];
-  const int* tab = p.table + (size_t)p.seq_row[s_id] * p.max_pages;
-  const int q0 = qt * BQ;
-  const int q_last = min(q0 + BQ, qlen) - 1;
-  const int kv_end = cpre + q_last + 1;
-  const int n_kt = (kv_end + BKV - 1) / BKV;
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < K_STAGES; ++i) {
       mbar_init(&k_full[i], 64);  // one cp.async-tracked (noinc) arrive per loader thread of the tensor
       mbar_init(&k_empty[i], 1);
@@ -270,7 +289,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   pdl_wait();  // set-up above overlaps the previous kernel's tail
   // timeline debugging (DUET_FA_TRACE=1): event e of tile j, clock() relative to kernel start
   uint32_t* trace = (uint32_t*)(smem + OFF_TRACE);
-  const bool tr = (p.trace & 1) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  bool tr = (p.trace & 1) && blockIdx.x == 0;  // CTA 0's first work item
   const uint32_t t_start = (uint32_t)clock();
   auto stamp = [&](int e, int j) {
     if (tr && lane == 0 && j < TRACE_MAXJ) trace[e * TRACE_MAXJ + j] = (uint32_t)clock() - t_start;
@@ -281,11 +300,20 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
 
   if (warp == 0) {
     if (lane == 0) {
-      // ------------------------------------------------ Q tiles (TMA, two 64-column boxes per head)
-      mbar_expect_tx(q_full, n_heads * Q_BYTES);
-      for (int h = 0; h < n_heads; ++h) {
-        tma_load_2d(&map_q, q_full, smem + OFF_Q + h * Q_BYTES, (head_a + h) * DH, row0 + q0);
-        tma_load_2d(&map_q, q_full, smem + OFF_Q + h * Q_BYTES + Q_SUB, (head_a + h) * DH + 64, row0 + q0);
+      // ------------------------------------------------ Q tiles (TMA, two 64-column boxes per head); the
+      // next item's tiles load as soon as the current item's last S MMAs have read them
+      int ni = 0;
+      Item it;
+      bool live;
+      for (int k = 0; item_at(p, k, it, live); ++k) {
+        if (!live) continue;
+        mbar_wait(q_empty, (ni & 1) ^ 1);
+        mbar_expect_tx(q_full, it.n_heads * Q_BYTES);
+        for (int h = 0; h < it.n_heads; ++h) {
+          tma_load_2d(&map_q, q_full, smem + OFF_Q + h * Q_BYTES, (it.head_a + h) * DH, it.row0 + it.q0);
+          tma_load_2d(&map_q, q_full, smem + OFF_Q + h * Q_BYTES + Q_SUB, (it.head_a + h) * DH + 64, it.row0 + it.q0);
+        }
+        ++ni;
       }
     }
   } else if (warp >= 10) {
@@ -304,10 +332,17 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
     // The per-thread address pattern is hoisted: per tile only the 8 page-table entries are read.
     const int ch = lt & 15, r0 = lt >> 4;
     const uint32_t so0 = (uint32_t)((ch >> 3) * KV_SUB);
-    const size_t col_off = (size_t)kvh * PAGE * DH + ch * 8;
-    for (int j = 0; j < n_kt; ++j) {
-      const int st = j % nst;
-      mbar_wait(&empty[st], ((j / nst) & 1) ^ 1);
+    int g = 0;  // tiles streamed by this CTA so far (ring position across work items)
+    Item it;
+    bool live;
+    for (int k = 0; item_at(p, k, it, live); ++k) {
+     if (!live) continue;
+     const int kv_end = it.kv_end;
+     const int* tab = it.tab;
+     const size_t col_off = (size_t)it.kvh * PAGE * DH + ch * 8;
+     for (int j = 0; j < it.n_kt; ++j, ++g) {
+      const int st = g % nst;
+      mbar_wait(&empty[st], ((g / nst) & 1) ^ 1);
       if (warp == 10) stamp(0, j);
       const uint32_t dst = smem_u32(smem + off_ring + st * KV_BYTES) + so0;
       if (p.trace & 2) {  // timing experiment only (DUET_FA_TRACE=noload): no K/V traffic, garbage result
@@ -333,72 +368,98 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
       }
       // the barrier phase completes when every loader thread's copies of this tile have landed
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[st])) : "memory");
+     }
+     tr = false;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     // tcgen05.mma from one thread executes in issue order: S_{j+1}^h (written over P_j^h) is issued right
     // after PV_j^h (which reads P_j^h), and a commit tracks every earlier MMA, so s_full also
-    // certifies that PV_{j-1} has completed.
+    // certifies that PV_{j-1} has completed.  Across work items: S_0 of the next item follows the last
+    // PV of the current one (the softmax warps drain O meanwhile; the next item's PV_0, which overwrites
+    // O, waits for p_full, which those warps arrive on only after their epilogue read O).
     constexpr uint32_t ID_S = idesc(BKV, false), ID_PV = idesc(DH, true);
-    mbar_wait(q_full, 0);
-    auto wait_k = [&](int j) {
-      mbar_wait(&k_full[j % K_STAGES], (j / K_STAGES) & 1);
-      stamp(1, j);
-      fence_async_smem();  // the loaders' cp.async (generic proxy) writes -> visible to the MMA (async proxy)
-      tc_after();
-    };
-    auto issue_s = [&](int j, int h) {  // S_j^h = Q^h K_j^T
-      if (lane == 0) {
-        const uint32_t sk = smem_u32(smem + OFF_K + (j % K_STAGES) * KV_BYTES);
-        const uint32_t sq = smem_u32(smem + OFF_Q + h * Q_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          umma(T_S(h), desc_k(sq + (kk >> 2) * Q_SUB + (kk & 3) * 32), desc_k(sk + (kk >> 2) * KV_SUB + (kk & 3) * 32),
-               ID_S, kk > 0);
-        umma_commit(&s_full[h]);
-        if (h == n_heads - 1) umma_commit(&k_empty[j % K_STAGES]);
-      }
-      __syncwarp();
-    };
-    wait_k(0);
-    for (int h = 0; h < n_heads; ++h) issue_s(0, h);
-    stamp(2, 0);
-    for (int j = 0; j < n_kt; ++j) {
-      const int st = j % V_STAGES;
-      mbar_wait(&v_full[st], (j / V_STAGES) & 1);
-      fence_async_smem();
-      const uint32_t sv = smem_u32(smem + OFF_V + st * KV_BYTES);
-      if (j + 1 < n_kt) wait_k(j + 1);
-      for (int h = 0; h < n_heads; ++h) {
-        mbar_wait(&p_full[h], j & 1);
+    int ni = 0, gk = 0, gv = 0;      // items, K tiles, V tiles consumed by this CTA
+    int gp[2] = {0, 0};              // P tiles per head
+    Item it;
+    bool live;
+    for (int k = 0; item_at(p, k, it, live); ++k) {
+      if (!live) continue;
+      const int n_kt = it.n_kt, n_heads = it.n_heads;
+      mbar_wait(q_full, ni & 1);
+      auto wait_k = [&](int j) {
+        mbar_wait(&k_full[gk % K_STAGES], (gk / K_STAGES) & 1);
+        stamp(1, j);
+        fence_async_smem();  // the loaders' cp.async (generic proxy) writes -> visible to the MMA (async proxy)
         tc_after();
+      };
+      auto issue_s = [&](int j, int h) {  // S_j^h = Q^h K_j^T
         if (lane == 0) {
+          const uint32_t sk = smem_u32(smem + OFF_K + (gk % K_STAGES) * KV_BYTES);
+          const uint32_t sq = smem_u32(smem + OFF_Q + h * Q_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk)  // 16 keys per UMMA k-step: A = P (TMEM, 8 columns), B = V
-            umma_ts(T_O(h), T_S(h) + kk * 8, desc_mn(sv + kk * 16 * 128), ID_PV, (j > 0 || kk > 0));
-          if (j == n_kt - 1) umma_commit(&o_done[h]);
-          if (h == n_heads - 1) umma_commit(&v_empty[st]);
+          for (int kk = 0; kk < DH / 16; ++kk)
+            umma(T_S(h), desc_k(sq + (kk >> 2) * Q_SUB + (kk & 3) * 32), desc_k(sk + (kk >> 2) * KV_SUB + (kk & 3) * 32),
+                 ID_S, kk > 0);
+          umma_commit(&s_full[h]);
+          if (h == n_heads - 1) {
+            umma_commit(&k_empty[gk % K_STAGES]);
+            if (j == n_kt - 1) umma_commit(q_empty);  // the item's last S: its Q tiles may be replaced
+          }
         }
         __syncwarp();
-        if (j + 1 < n_kt) issue_s(j + 1, h);
+      };
+      wait_k(0);
+      for (int h = 0; h < n_heads; ++h) issue_s(0, h);
+      ++gk;
+      stamp(2, 0);
+      for (int j = 0; j < n_kt; ++j, ++gv) {
+        const int st = gv % V_STAGES;
+        mbar_wait(&v_full[st], (gv / V_STAGES) & 1);
+        fence_async_smem();
+        const uint32_t sv = smem_u32(smem + OFF_V + st * KV_BYTES);
+        if (j + 1 < n_kt) wait_k(j + 1);
+        for (int h = 0; h < n_heads; ++h) {
+          mbar_wait(&p_full[h], gp[h] & 1);
+          ++gp[h];
+          tc_after();
+          if (lane == 0) {
+#pragma unroll
+            for (int kk = 0; kk < BKV / 16; ++kk)  // 16 keys per UMMA k-step: A = P (TMEM, 8 columns), B = V
+              umma_ts(T_O(h), T_S(h) + kk * 8, desc_mn(sv + kk * 16 * 128), ID_PV, (j > 0 || kk > 0));
+            if (j == n_kt - 1) umma_commit(&o_done[h]);
+            if (h == n_heads - 1) umma_commit(&v_empty[st]);
+          }
+          __syncwarp();
+          if (j + 1 < n_kt) issue_s(j + 1, h);
+        }
+        if (j + 1 < n_kt) ++gk;
+        stamp(3, j);
+        if (j + 1 < n_kt) stamp(2, j + 1);
       }
-      stamp(3, j);
-      if (j + 1 < n_kt) stamp(2, j + 1);
+      ++ni;
+      if (tr && lane == 0) trace[10 * TRACE_MAXJ] = (uint32_t)n_kt;  // the traced item's key tiles
+      tr = false;
     }
   } else {
     // ------------------------------------------------ softmax warps: one thread per query row
     const int h = (warp - 2) >> 2;  // head A (warps 2..5) or B (6..9)
-    if (h < n_heads) {
-      const int quad = warp & 3;
-      const int r = quad * 32 + lane;                          // row in tile = TMEM lane
-      const int pos = min(cpre + q0 + r, kv_end - 1);          // clamp rows past the chunk
-      const float sc = rsqrtf((float)DH) * 1.4426950408889634f;
-      const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-      const uint32_t t_s = T_S(h) + lane_base;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;                          // row in tile = TMEM lane
+    const float sc = rsqrtf((float)DH) * 1.4426950408889634f;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const uint32_t t_s = T_S(h) + lane_base;
+    int gs = 0, ni_h = 0;  // S tiles and work items of this head so far
+    Item it;
+    bool live;
+    for (int k = 0; item_at(p, k, it, live); ++k) {
+      if (!live || h >= it.n_heads) continue;  // an odd last head of a group runs alone (no head B)
+      const int n_kt = it.n_kt, q0 = it.q0, qlen = it.qlen, row0 = it.row0, head_a = it.head_a;
+      const int pos = min(it.cpre + q0 + r, it.kv_end - 1);  // clamp rows past the chunk
       float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < n_kt; ++j) {
-        mbar_wait(&s_full[h], j & 1);
+      for (int j = 0; j < n_kt; ++j, ++gs) {
+        mbar_wait(&s_full[h], gs & 1);
         if (warp == 2) stamp(4, j);
         if (warp == 6) stamp(7, j);
         tc_after();
@@ -415,19 +476,18 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
         for (int c = 0; c < 2; ++c) {
           uint32_t v0[32], v1[32], pk[32];
           tmem_ld32x2(t_s + c * 64, t_s + c * 64 + 32, v0, v1);
-          float mx = -INFINITY;
-          if (full_tile) {
-#pragma unroll
-            for (int e = 0; e < 32; e += 2)
-              mx = fmaxf(mx, fmaxf(fmaxf(__uint_as_float(v0[e]), __uint_as_float(v0[e + 1])),
-                                   fmaxf(__uint_as_float(v1[e]), __uint_as_float(v1[e + 1]))));
-          } else {
+          if (!full_tile) {  // keys past the row's causal end -> -inf: exp2 gives 0, the max ignores them
 #pragma unroll
             for (int e = 0; e < 32; ++e) {
-              if (c * 64 + e <= lim) mx = fmaxf(mx, __uint_as_float(v0[e]));
-              if (c * 64 + 32 + e <= lim) mx = fmaxf(mx, __uint_as_float(v1[e]));
+              if (c * 64 + e > lim) v0[e] = 0xff800000u;
+              if (c * 64 + 32 + e > lim) v1[e] = 0xff800000u;
             }
           }
+          float mx = -INFINITY;
+#pragma unroll
+          for (int e = 0; e < 32; e += 2)
+            mx = fmaxf(mx, fmaxf(fmaxf(__uint_as_float(v0[e]), __uint_as_float(v0[e + 1])),
+                                 fmaxf(__uint_as_float(v1[e]), __uint_as_float(v1[e + 1]))));
           const float m_new = fmaxf(m_used, mx * sc);  // sc > 0: the max commutes with the scaling
           const bool mine = m_new > m_used + RESCALE_THRESHOLD;
           if (__any_sync(0xffffffffu, mine)) {  // rare after the first chunk of a row
@@ -458,41 +518,26 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
             }
             if (mine) m_used = m_new;
           }
-          if (full_tile) {
-            const uint64_t sc2 = pack_f2(sc, sc), nm2 = pack_f2(-m_used, -m_used);
-            uint64_t acc2 = pack_f2(0.f, 0.f);
+          // the chunk's 64 exponentials, packed f32x2 (masked keys hold -inf: p = 0, a row's first chunk
+          // always has its key 0 visible, so m_used is finite whenever a -inf is exponentiated)
+          const uint64_t sc2 = pack_f2(sc, sc), nm2 = pack_f2(-m_used, -m_used);
+          uint64_t acc2 = pack_f2(0.f, 0.f);
 #pragma unroll
-            for (int e = 0; e < 64; e += 2) {
-              const uint32_t* src = e < 32 ? v0 : v1;
-              const int ee = e & 31;
-              const uint64_t t2 = ffma2(pack_f2(__uint_as_float(src[ee]), __uint_as_float(src[ee + 1])), sc2, nm2);
-              float t0, t1;
-              unpack_f2(t2, t0, t1);
-              const float p0 = fast_exp2(t0), p1 = fast_exp2(t1);
-              acc2 = fadd2(acc2, pack_f2(p0, p1));
-              __nv_bfloat162 t = __floats2bfloat162_rn(p0, p1);
-              pk[e / 2] = *reinterpret_cast<uint32_t*>(&t);
-            }
-            float a0, a1;
-            unpack_f2(acc2, a0, a1);
-            l0 += a0;
-            l1 += a1;
-          } else {
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-              for (int e = 0; e < 32; e += 2) {
-                const float s0 = __uint_as_float(hh ? v1[e] : v0[e]), s1 = __uint_as_float(hh ? v1[e + 1] : v0[e + 1]);
-                const int k0 = c * 64 + hh * 32 + e;
-                const float p0 = (k0 <= lim) ? fast_exp2(fmaf(s0, sc, -m_used)) : 0.f;
-                const float p1 = (k0 + 1 <= lim) ? fast_exp2(fmaf(s1, sc, -m_used)) : 0.f;
-                l0 += p0;
-                l1 += p1;
-                __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
-                pk[hh * 16 + e / 2] = *reinterpret_cast<uint32_t*>(&t2);
-              }
-            }
+          for (int e = 0; e < 64; e += 2) {
+            const uint32_t* src = e < 32 ? v0 : v1;
+            const int ee = e & 31;
+            const uint64_t t2 = ffma2(pack_f2(__uint_as_float(src[ee]), __uint_as_float(src[ee + 1])), sc2, nm2);
+            float t0, t1;
+            unpack_f2(t2, t0, t1);
+            const float p0 = fast_exp2(t0), p1 = fast_exp2(t1);
+            acc2 = fadd2(acc2, pack_f2(p0, p1));
+            __nv_bfloat162 t = __floats2bfloat162_rn(p0, p1);
+            pk[e / 2] = *reinterpret_cast<uint32_t*>(&t);
           }
+          float a0, a1;
+          unpack_f2(acc2, a0, a1);
+          l0 += a0;
+          l1 += a1;
           tmem_st32(t_s + c * 32, pk);
         }
         l += l0 + l1;
@@ -504,9 +549,16 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
         if (warp == 2) stamp(6, j);
         if (warp == 6) stamp(9, j);
       }
-      pdl_trigger();  // only the epilogue is left
+      {  // the CTA's last work item: only its epilogue is left
+        Item nx;
+        bool nlive = false;
+        int kk = k + 1;
+        while (item_at(p, kk, nx, nlive) && !nlive) ++kk;
+        if (!nlive) pdl_trigger();
+      }
       // epilogue: O / l -> bf16 -> global
-      mbar_wait(&o_done[h], 0);
+      mbar_wait(&o_done[h], ni_h & 1);
+      ++ni_h;
       tc_after();
       const bool row_ok = q0 + r < qlen;
       const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -525,11 +577,13 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
           }
         }
       }
+      tr = false;
     }
   }
   tc_before();
   __syncthreads();
-  if (tr && threadIdx.x == 0) {
+  if ((p.trace & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int n_kt = (int)trace[10 * TRACE_MAXJ];
     printf("FA_TRACE n_kt=%d (clock cycles; ev: 0 load-issue 1 kv_full 2 S-issued 3 PV-issued 4 s_full 5 exps-done 6 P-published)\n", n_kt);
     for (int j = 0; j < n_kt && j < TRACE_MAXJ; ++j)
       printf("FA_TRACE j=%2d %8u %8u %8u %8u | A %8u %8u %8u | B %8u %8u %8u\n", j, trace[j], trace[TRACE_MAXJ + j],
@@ -589,16 +643,22 @@ int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   }
   CUtensorMap mq;
   if (!fatc::make_map(&mq, a.q, (uint64_t)a.total_rows, (uint64_t)a.q_stride, (uint64_t)a.q_stride, 128)) return -1;
-  fatc::Params p{a.row0, a.qlen, a.cpre, a.seq_row, a.table, a.max_pages, a.hq, a.hkv, 0, 0, 0,
+  fatc::Params p{a.row0, a.qlen, a.cpre, a.seq_row, a.table, a.max_pages, a.hq, a.hkv, 0, 0, 0, 0,
                  (bf16*)a.o, (const bf16*)a.k_pool, (const bf16*)a.v_pool};
   const int G = a.hq / a.hkv;
   p.n_qtiles = (a.max_q + fatc::BQ - 1) / fatc::BQ;
   p.n_pairs = a.hkv * ((G + 1) / 2);
+  p.n_seqs = a.n_seqs;
   static const char* trace = getenv("DUET_FA_TRACE");
   // DUET_FA_TRACE: any value prints the timeline of CTA (0,0,0); "noload" skips the K/V loads instead
   // (timing experiment, garbage output); "tn" does both
   p.trace = trace ? (trace[0] == 'n' ? 2 : (trace[0] == 't' && trace[1] == 'n' ? 3 : 1)) : 0;
-  dim3 grid(p.n_pairs, p.n_qtiles, a.n_seqs);
+  // persistent: one CTA per SM of the partition walks a snake order of the work items (the next item's Q
+  // load, first K / V tiles and S_0 overlap the current item's last PV and epilogue); DUET_FA_PERSIST=0
+  // launches one CTA per item (the round-1 grid, A/B)
+  static const bool persist = !getenv("DUET_FA_PERSIST") || atoi(getenv("DUET_FA_PERSIST")) != 0;
+  const int items = p.n_qtiles * a.n_seqs * p.n_pairs;
+  dim3 grid(persist ? std::min(items, std::max(a.num_sms, 1)) : items);
   if (ks == 2 && vs == 3) launch_pdl(fatc::fa_tc_kernel<2, 3>, grid, fatc::THREADS, fatc::Ring<2, 3>::SMEM, st, mq, p);
   else launch_pdl(fatc::fa_tc_kernel<3, 2>, grid, fatc::THREADS, fatc::Ring<3, 2>::SMEM, st, mq, p);
   return 1;
