@@ -194,6 +194,17 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_st32_nowait(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
 struct Params {
   const int* row0;
   const int* qlen;
@@ -506,6 +517,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
               }
             }
             if (c == 1) {  // the first chunk's P (bf16 pairs in columns 0..31) against the new reference
+              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
               uint32_t v[32];
               tmem_ld32(t_s, v);
 #pragma unroll
@@ -538,8 +550,9 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
           unpack_f2(acc2, a0, a1);
           l0 += a0;
           l1 += a1;
-          tmem_st32(t_s + c * 32, pk);
+          tmem_st32_nowait(t_s + c * 32, pk);  // completion awaited once, before p_full
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         l += l0 + l1;
         if (warp == 2) stamp(5, j);
         if (warp == 6) stamp(8, j);
