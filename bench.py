@@ -853,9 +853,12 @@ def main():
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "profile_tables": {"sms": [parts[0], parts[len(parts) // 2], total],
-                               "tflops": [fl[parts[0]] / 1e12, fl[parts[len(parts) // 2]] / 1e12, fl[total] / 1e12],
-                               "hbm_gbs": [bw[parts[0]] / 1e9, bw[parts[len(parts) // 2]] / 1e9, bw[total] / 1e9]},
+            # the calibrated Pi_SM(S) / B_HBM(S) tables Alg. 1 ran on (every calibrated partition size;
+            # SURVEY §8(d) calibration inputs)
+            "profile_tables": {"sms": [S for S in range(1, total + 1) if fl[S] > 0 and bw[S] > 0],
+                               "tflops": [round(fl[S] / 1e12, 3) for S in range(1, total + 1) if fl[S] > 0 and bw[S] > 0],
+                               "hbm_gbs": [round(bw[S] / 1e9, 2) for S in range(1, total + 1) if fl[S] > 0 and bw[S] > 0],
+                               "source": f"duet_calibrate{'_corun' if args.calibration == 'corun' else ''} on this box"},
         }
         print(json.dumps(line), flush=True)
     ctx.close()
