@@ -821,6 +821,8 @@ def main():
         cpu["oracle_optimizer_ms"] = (time.perf_counter() - t0_) * 1e3
 
     if rank == 0:
+        # the partition sizes a split can use (each decode size and its complement) and the full device
+        cal_sizes = sorted({S for p in parts for S in (p, total - p)} | {total})
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if tp > 1 else "weak",
@@ -855,9 +857,9 @@ def main():
             "cpu_baseline": cpu,
             # the calibrated Pi_SM(S) / B_HBM(S) tables Alg. 1 ran on (every calibrated partition size;
             # SURVEY §8(d) calibration inputs)
-            "profile_tables": {"sms": [S for S in range(1, total + 1) if fl[S] > 0 and bw[S] > 0],
-                               "tflops": [round(fl[S] / 1e12, 3) for S in range(1, total + 1) if fl[S] > 0 and bw[S] > 0],
-                               "hbm_gbs": [round(bw[S] / 1e9, 2) for S in range(1, total + 1) if fl[S] > 0 and bw[S] > 0],
+            "profile_tables": {"sms": cal_sizes,
+                               "tflops": [round(fl[S] / 1e12, 3) for S in cal_sizes],
+                               "hbm_gbs": [round(bw[S] / 1e9, 2) for S in cal_sizes],
                                "source": f"duet_calibrate{'_corun' if args.calibration == 'corun' else ''} on this box"},
         }
         print(json.dumps(line), flush=True)
