@@ -207,6 +207,18 @@ def layer_forward(m: Model, w: dict, layer: int, x: np.ndarray, pos: np.ndarray,
     return x1 + (part if allreduce is None else allreduce(part))
 
 
+def row_parallel_allreduce(a_shards, w_shards, residual) -> np.ndarray:
+    """A row-parallel linear and its allreduce (§4.1 Communication Operators; steps 6 and 8 of
+    ``layer_forward`` with the ``allreduce`` hook, reading #13): rank r holds the input columns
+    a_r [n][k_r] and the matching weight columns w_r [d_out][k_r], computes its partial a_r w_r^T, the
+    allreduce sums the N partials, and the residual is added once:  residual + sum_r a_r w_r^T.
+    The reference for SURVEY §8(f) f3 (the fused GEMM + allreduce kernel)."""
+    out = np.array(residual, dtype=np.float64, copy=True)
+    for a, w in zip(a_shards, w_shards):
+        out = out + np.asarray(a, dtype=np.float64) @ np.asarray(w, dtype=np.float64).T
+    return out
+
+
 def prefill_forward(m: Model, weights: list, x: np.ndarray, seqs: list, tables: np.ndarray,
                     kv: PagedKV) -> np.ndarray:
     """All layers over the prefill rows.  seqs = [(q_s, c_s)], rows grouped by sequence in order;

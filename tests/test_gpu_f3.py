@@ -4,7 +4,8 @@ In a head-sharded TP block the O and FFN-down projections are row-parallel: rank
 A_r of the activation and the rows B_r of the weight's input dimension, and the layer needs
 R + sum_r A_r B_r^T on every rank — the allreduce after O and down.  `duet_op_gemm_ar_emul`
 runs the fused kernel with n ranks emulated in one grid on this GPU (the ranks' owner warps wait on
-each other, so they must share a launch: B200_PROFILING); the reference is that definition in float64.
+each other, so they must share a launch: B200_PROFILING); the reference is oracle.layer.row_parallel_allreduce
+(float64 numpy, pinned on CPU by tests/test_oracle_layer.py).
 The ctx-level tests open the fused path on a single-rank group (tp = 1: the same kernel with one
 owner) and compare the layer stack with the oracle.
 """
@@ -15,11 +16,20 @@ import torch
 import paper_2511_04791_b200 as D
 from synth import configs, workload
 from tests.gpu_helpers import GpuWorkload, make_ctx
+from oracle.layer import row_parallel_allreduce
 from tests.oracle_run import rel_err, run
 
 pytestmark = pytest.mark.gpu
 
 TOL = 2e-2
+
+
+def _ref(A, B, R):
+    """oracle.layer.row_parallel_allreduce on the bf16 operands (exact in float64)"""
+    n = A.shape[0]
+    return torch.from_numpy(row_parallel_allreduce([A[r].double().cpu().numpy() for r in range(n)],
+                                                   [B[r].double().cpu().numpy() for r in range(n)],
+                                                   R.double().cpu().numpy())).cuda()
 
 
 def _ctx_for_ops(M):
@@ -31,7 +41,7 @@ def _ctx_for_ops(M):
 @pytest.mark.parametrize("n,M,N,K", [(1, 300, 512, 384), (2, 300, 512, 384), (4, 1000, 768, 256),
                                      (8, 257, 256, 128), (2, 2112, 4096, 2048), (4, 2112, 4096, 1024)])
 def test_gemm_allreduce_emulated_ranks(n, M, N, K):
-    """Every emulated rank's output equals R + sum_r A_r B_r^T (float64) within the bf16 tolerance and all
+    """Every emulated rank's output equals the oracle's R + sum_r A_r B_r^T within the bf16 tolerance and all
     ranks hold bitwise the same rows (one owner computes each tile and pushes it to every rank).  Ragged
     M (a partial last 256-row tile), tiles not divisible by n, and the cfg2 O / down shapes
     (M = 2112, N = d = 4096) split over 2 and 4 ranks."""
@@ -43,7 +53,7 @@ def test_gemm_allreduce_emulated_ranks(n, M, N, K):
     C = torch.full((n, M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
     ctx.op_gemm_ar_emul(A, B, R, C)
     torch.cuda.synchronize()
-    ref = R.double() + sum(A[r].double() @ B[r].double().T for r in range(n))
+    ref = _ref(A, B, R)
     for r in range(n):
         assert not torch.isnan(C[r]).any(), f"rank {r}: rows never written"
         e = (C[r].double() - ref).abs().max().item() / ref.abs().max().item()
@@ -55,7 +65,7 @@ def test_gemm_allreduce_emulated_ranks(n, M, N, K):
         C2 = torch.empty_like(C)
         ctx.op_gemm_ar_emul(A2, B, R, C2)
         torch.cuda.synchronize()
-        ref2 = R.double() + sum(A2[r].double() @ B[r].double().T for r in range(n))
+        ref2 = _ref(A2, B, R)
         e = (C2[0].double() - ref2).abs().max().item() / ref2.abs().max().item()
         assert e < 1e-2, (it, e)
         assert all(torch.equal(C2[r], C2[0]) for r in range(n))
@@ -86,7 +96,7 @@ def test_gemm_allreduce_emulated_in_cuda_graph():
         C.zero_()
         g.replay()
         torch.cuda.synchronize()
-        ref = R.double() + sum(A[r].double() @ B[r].double().T for r in range(n))
+        ref = _ref(A, B, R)
         e = (C[1].double() - ref).abs().max().item() / ref.abs().max().item()
         assert e < 1e-2, (it, e)
         assert torch.equal(C[0], C[1])
@@ -104,8 +114,8 @@ def test_gemm_allreduce_sensitivity():
     C = torch.empty(n, M, N, device="cuda", dtype=torch.bfloat16)
     ctx.op_gemm_ar_emul(A, B, R, C)
     torch.cuda.synchronize()
-    full = sum(A[r].double() @ B[r].double().T for r in range(n))
-    only0 = A[0].double() @ B[0].double().T
+    full = _ref(A, B, R)
+    only0 = _ref(A[:1], B[:1], R)
     e_ok = (C[0].double() - full).abs().max().item() / full.abs().max().item()
     e_bad = (only0 - full).abs().max().item() / full.abs().max().item()
     assert e_ok < 1e-2 < e_bad

@@ -368,3 +368,23 @@ def test_decode_window_feedback_chains_outputs():
     OL.decode_window(m, wl.weights, wl.x_dec, wl.dec_ctx, wl.dec_tables, kv_x, 1)
     y2_x = OL.decode_window(m, wl.weights, wl.x_dec, [c + 1 for c in wl.dec_ctx], wl.dec_tables, kv_x, 1)
     assert not np.allclose(y[1], y2_x[0], rtol=0, atol=1e-3)   # feeding x again is a different result
+
+
+def test_row_parallel_allreduce_equals_unsharded_linear():
+    """f3 reference (oracle.layer.row_parallel_allreduce): splitting the contraction dimension of one
+    linear over N ranks and summing the partials is the unsharded linear — checked exactly on integer
+    matrices (every product and sum exact in float64) for uneven shard widths."""
+    rng = np.random.default_rng(11)
+    n, k, dout = 37, 96, 40
+    A = rng.integers(-8, 9, size=(n, k)).astype(np.float64)
+    W = rng.integers(-8, 9, size=(dout, k)).astype(np.float64)
+    R = rng.integers(-8, 9, size=(n, dout)).astype(np.float64)
+    for cuts in ([48], [16, 64], [8, 40, 72]):   # N = 2, 3, 4 ranks, uneven widths
+        edges = [0] + cuts + [k]
+        a_sh = [A[:, edges[i]:edges[i + 1]] for i in range(len(edges) - 1)]
+        w_sh = [W[:, edges[i]:edges[i + 1]] for i in range(len(edges) - 1)]
+        got = OL.row_parallel_allreduce(a_sh, w_sh, R)
+        want = R + np.einsum("ik,jk->ij", A, W)
+        assert np.array_equal(got, want)
+    # dropping a rank's partial is caught
+    assert not np.array_equal(OL.row_parallel_allreduce(a_sh[:-1], w_sh[:-1], R), want)
