@@ -471,7 +471,10 @@ static int decode_attn(duet_ctx* c, Side& S, const AttnPlan& ap, const void* q, 
 static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms, int n_rows, const void* x_in,
                               void* y_final, const duet_layer_weights* w, const duet_kv_pages* kv, const AttnPlan& ap,
                               int* kernels, const void* x_in2 = nullptr, void* y_final2 = nullptr,
-                              int row_split = 1 << 30) {
+                              int row_split = 1 << 30, const int* n_dev = nullptr) {
+  // n_dev (nullable): the rows live on the device (meta) and n_rows is the side's capacity — the kernels
+  // are launched for the capacity and read the row count themselves, so a captured graph of this stack
+  // replays for any prefill shape (f4; the spatial prefill side's graphs)
   const auto& sp = c->spec;
   const DT dt = c->dt;
   const size_t es = dt_size(dt);
@@ -540,13 +543,14 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     // 1. h = RMSNorm(x) g1
     TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e,
           launch_rmsnorm(dt, X, W.g_norm1, S.h, n_rows, d, eps, st, l == 0 ? x_in2 : nullptr,
-                         l == 0 ? row_split : 1 << 30));
+                         l == 0 ? row_split : 1 << 30, n_dev));
     // 2. qkv = h W_qkv^T (+ b);  3. RoPE + paged KV append (before attention) — fused into the
     // CTA-pair GEMM's epilogue when it runs (k and v never round-trip through the qkv buffer)
     RopeKvArgs ra{S.qkv, nullptr, n_rows, hq, hkv, dh, S.pos(), S.tok(), S.table(), S.pitch, kPageSize,
                   kv->k_pool[l], kv->v_pool[l], c->rope};
     GemmArgs g{S.h, W.w_qkv, S.qkv, nullptr, W.b_qkv, n_rows, nqkv, d, d, d, nqkv, 0, EPI_STORE};
     with_ws(g);
+    g.m_dev = n_dev;
     static const bool fuse_env = !getenv("DUET_FUSE_ROPE") || atoi(getenv("DUET_FUSE_ROPE")) != 0;
     const bool fuse_rope = fuse_env && dt == DT::BF16 && dh == 128 && kPageSize == 16 && gemm2_supported(g, num_sms);
     if (fuse_rope) {
@@ -554,6 +558,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       g.rope = &ra;
     }
     TIMED(DUET_KCLASS_GEMM, gemm_fl(nqkv, d), gemm_by(nqkv, d, nqkv, false), launch_gemm(dt, g, num_sms, st));
+    if (!fuse_rope && n_dev) DUET_FAIL(DUET_ERR_UNSUPPORTED, "device-side row counts need the fused RoPE epilogue");
     if (!fuse_rope)
       TIMED(DUET_KCLASS_OTHER, 6.0 * n * (hq + hkv) * dh, n * (nqkv + (hq + 2.0 * hkv) * dh) * e,
             launch_rope_kv(dt, ra, st));
@@ -607,6 +612,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     GemmArgs go{S.o, W.w_o, S.x1, lead ? X : nullptr, nullptr, n_rows, d, hq * dh, hq * dh, hq * dh, d, d,
                 lead ? EPI_RESIDUAL : EPI_STORE};
     with_ws(go);
+    go.m_dev = n_dev;
     if (l == 0 && row_split < n_rows) {
       go.R2 = x_in2;
       go.row_split = row_split;
@@ -614,7 +620,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     }
     const void* x1 = S.x1;
     bool fused_o = false;
-    if (ar_side && !(l == 0 && row_split < n_rows)) {  // f3: O projection + allreduce in one kernel
+    if (ar_side && !n_dev && !(l == 0 && row_split < n_rows)) {  // f3: O projection + allreduce in one kernel
       GemmArgs ga{S.o, W.w_o, nullptr, X, nullptr, n_rows, d, hq * dh, hq * dh, hq * dh, d, d, EPI_RESIDUAL_AR};
       ga.ar = &ar_o;
       if (gemm2_supported(ga, num_sms)) {
@@ -626,22 +632,25 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     TIMED(DUET_KCLASS_GEMM, gemm_fl(d, hq * dh), gemm_by(d, hq * dh, d, true), launch_gemm(dt, go, num_sms, st));
     if (comm && !fused_o) TIMED(DUET_KCLASS_OTHER, 0.0, 2.0 * n * d * e, allreduce(S.x1, n_rows));
     // 6. h2 = RMSNorm(x1) g2
-    TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e, launch_rmsnorm(dt, x1, W.g_norm2, S.h2, n_rows, d, eps, st));
+    TIMED(DUET_KCLASS_OTHER, 4.0 * n * d, 2.0 * n * d * e,
+          launch_rmsnorm(dt, x1, W.g_norm2, S.h2, n_rows, d, eps, st, nullptr, 1 << 30, n_dev));
     // 7. act = silu(h2 W_g^T) * (h2 W_u^T)
     GemmArgs gg{S.h2, W.w_gate_up, S.act, nullptr, nullptr, n_rows, m, d, d, d, m, 0, EPI_SWIGLU};
     with_ws(gg);
+    gg.m_dev = n_dev;
     TIMED(DUET_KCLASS_GEMM, gemm_fl(2.0 * m, d), gemm_by(2.0 * m, d, m, false), launch_gemm(dt, gg, num_sms, st));
     // 8. y = x1 + act W_d^T
     GemmArgs gd{S.act, W.w_down, Y, lead ? x1 : nullptr, nullptr, n_rows, d, m, m, m, d, d,
                 lead ? EPI_RESIDUAL : EPI_STORE};
     with_ws(gd);
+    gd.m_dev = n_dev;
     if (l == sp.n_layers - 1 && row_split < n_rows) {
       gd.C2 = y_final2;
       gd.R2 = lead ? (const char*)x1 + (size_t)row_split * d * es : nullptr;
       gd.row_split = row_split;
     }
     bool fused_d = false;
-    if (ar_side && !(l == sp.n_layers - 1 && row_split < n_rows)) {  // f3: down projection + allreduce
+    if (ar_side && !n_dev && !(l == sp.n_layers - 1 && row_split < n_rows)) {  // f3: down projection + allreduce
       GemmArgs ga{S.act, W.w_down, nullptr, x1, nullptr, n_rows, d, m, m, m, d, d, EPI_RESIDUAL_AR};
       ga.ar = &ar_d;
       if (gemm2_supported(ga, num_sms)) {
@@ -1029,6 +1038,8 @@ static size_t build_meta(duet_ctx* c, const Side& S, int* img, const duet_prefil
     }
   }
   img[S.o_step] = 0;
+  img[S.o_step + 1] = n_pre + n_dec;  // the side's rows, read on the device by shape-agnostic prefill graphs (f4)
+  for (int s = n_seqs; s < S.cap_seqs; ++s) img[S.o_qlen + s] = 0;  // no work items past the batch
   {
     const double hq = c->spec.n_q_heads, hkv = c->spec.n_kv_heads, dh = c->spec.head_dim, e = (double)dt_size(c->dt);
     double fl = 0, by = 0;
@@ -1328,9 +1339,22 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
     const bool pre_graph = !(c->lim.flags & (DUET_CTX_NO_GRAPH | DUET_CTX_NO_PREFILL_GRAPH)) &&
                            !(c->prof_on && (c->prof_mask & kPreClasses));
     GraphEntry* ge = nullptr;
+    // shape-agnostic capture (f4, "device-side shapes"): the kernels are launched for the side's capacity
+    // and read the chunk's row count and per-sequence lengths from the metadata, so ONE graph per
+    // partition and buffer set serves every prefill shape (bf16 CTA-pair path with the fused RoPE
+    // epilogue, no TP; DUET_PREFILL_DEVSHAPE=0 keeps the per-shape graphs)
+    static const bool devshape_env = !getenv("DUET_PREFILL_DEVSHAPE") || atoi(getenv("DUET_PREFILL_DEVSHAPE")) != 0;
+    const bool dev_shape = pre_graph && devshape_env && c->dt == DT::BF16 && c->spec.head_dim == 128 &&
+                           !c->comm_pre && !c->ar_on && c->pre.cap_rows > 128;
+    AttnPlan ap_cap = ap;  // the plan the shape-agnostic graph is launched with
+    if (dev_shape) {
+      ap_cap.n_pre = c->pre.cap_rows;
+      ap_cap.n_seqs = c->pre.cap_seqs;
+      ap_cap.max_q = c->pre.cap_rows;
+    }
     if (pre_graph) {
-      const PreKey key{(uint64_t)P->s_d, (uint64_t)ap.n_pre, (uint64_t)ap.n_seqs, (uint64_t)ap.max_q,
-                       (uint64_t)ap.max_len_pre,
+      const PreKey key{(uint64_t)P->s_d, dev_shape ? ~0ull : (uint64_t)ap.n_pre, dev_shape ? 0 : (uint64_t)ap.n_seqs,
+                       dev_shape ? 0 : (uint64_t)ap.max_q, dev_shape ? 0 : (uint64_t)ap.max_len_pre,
                        hash_ptrs(w, c->spec.n_layers, kv, pre->y, 0) ^ ((uint64_t)(uintptr_t)pre->x * 0x9E3779B97F4A7C15ull)};
       auto it = c->pre_graphs.find(key);
       if (it == c->pre_graphs.end()) {
@@ -1340,7 +1364,9 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
           int nk = 0;
           CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
           c->capturing = true;
-          duet_status sc = run_layers(c, c->pre, st, P->s_p, ap.n_pre, pre->x, pre->y, w, kv, ap, &nk);
+          duet_status sc = dev_shape ? run_layers(c, c->pre, st, P->s_p, ap_cap.n_pre, pre->x, pre->y, w, kv, ap_cap,
+                                                  &nk, nullptr, nullptr, 1 << 30, c->pre.step() + 1)
+                                     : run_layers(c, c->pre, st, P->s_p, ap.n_pre, pre->x, pre->y, w, kv, ap, &nk);
           c->capturing = false;
           cudaError_t e = cudaStreamEndCapture(st, &graph);
           if (sc != DUET_OK) return sc;
@@ -1368,6 +1394,9 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
       ge->last_use = ++c->graph_clock;
       CUDA_TRY(cudaGraphLaunch(ge->exec, st));
       kernels += ge->kernels;
+    } else if (dev_shape) {  // the same launches the graph holds (its first run is bitwise the replays)
+      DUET_TRY(run_layers(c, c->pre, st, P->s_p, ap_cap.n_pre, pre->x, pre->y, w, kv, ap_cap, &kernels, nullptr,
+                          nullptr, 1 << 30, c->pre.step() + 1));
     } else {
       DUET_TRY(run_layers(c, c->pre, st, P->s_p, ap.n_pre, pre->x, pre->y, w, kv, ap, &kernels));
     }

@@ -71,6 +71,9 @@ struct GemmArgs {
   const struct RopeKvArgs* rope = nullptr;
   // EPI_RESIDUAL_AR: the tp group (C is ignored: outputs go to ar->out[r])
   const struct GemmAr* ar = nullptr;
+  // nullable device int: the rows of this launch, read on the device (M is then the buffers' capacity;
+  // CTA-pair kernel only, never split-K) — graphs that replay for any row count (f4)
+  const int* m_dev = nullptr;
 };
 // fp32 partial floats a split-K launch of this shape needs (0 when it runs unsplit)
 size_t gemm_tc_splitk_need(int M, int N, int K, int epi);
@@ -90,7 +93,8 @@ int launch_gemm2(const GemmArgs& a, int num_sms, cudaStream_t st);
 // ---------------------------------------------------------------- RMSNorm
 // h[n][d] = x * rsqrt(mean(x^2) + eps) * g     (reading #1)
 int launch_rmsnorm(DT dt, const void* x, const void* g, void* h, int n, int d, float eps, cudaStream_t st,
-                   const void* x2 = nullptr, int row_split = 1 << 30);  // rows >= row_split from x2
+                   const void* x2 = nullptr, int row_split = 1 << 30,  // rows >= row_split from x2
+                   const int* n_dev = nullptr);  // nullable: rows on the device (n is then the capacity)
 
 // ---------------------------------------------------------------- RoPE + paged KV append
 // qkv rows [n][(hq + 2 hkv) dh]; row i at position pos[i], page-table row tok_row[i].

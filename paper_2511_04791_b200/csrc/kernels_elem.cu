@@ -11,11 +11,12 @@ namespace duet {
 template <typename T, int THREADS>
 __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const T* __restrict__ x, const T* __restrict__ g,
                                                           T* __restrict__ h, int d, float eps, const T* __restrict__ x2,
-                                                          int row_split) {
+                                                          int row_split, const int* __restrict__ n_dev) {
   constexpr int E = 16 / sizeof(T);
   constexpr int VPT = 4;  // rows of up to THREADS * VPT vectors stay in registers: x is read once
   pdl_wait();
   const int row = blockIdx.x;
+  if (n_dev && row >= *n_dev) return;  // a launch sized for the capacity (device-side row count)
   const T* xr = row < row_split ? x + (size_t)row * d : x2 + (size_t)(row - row_split) * d;
   T* hr = h + (size_t)row * d;
   const int nv = d / E;
@@ -76,14 +77,14 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const T* __restrict__ 
 }
 
 int launch_rmsnorm(DT dt, const void* x, const void* g, void* h, int n, int d, float eps, cudaStream_t st,
-                   const void* x2, int row_split) {
+                   const void* x2, int row_split, const int* n_dev) {
   if (n <= 0) return 0;
   if (dt == DT::BF16)
     launch_pdl(rmsnorm_kernel<bf16, 256>, n, 256, 0, st, (const bf16*)x, (const bf16*)g, (bf16*)h, d, eps,
-               (const bf16*)x2, row_split);
+               (const bf16*)x2, row_split, n_dev);
   else
     rmsnorm_kernel<float, 256><<<n, 256, 0, st>>>((const float*)x, (const float*)g, (float*)h, d, eps,
-                                                  (const float*)x2, row_split);
+                                                  (const float*)x2, row_split, n_dev);
   return 1;
 }
 

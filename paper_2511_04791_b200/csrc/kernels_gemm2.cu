@@ -155,6 +155,7 @@ struct Params {
   // reads its operands at X rows r * xrows and W rows r * wrows of the stacked inputs
   GemmAr ar;
   int ar_ppr, ar_xrows, ar_wrows;
+  const int* m_dev;  // nullable: rows from device memory (M is then the capacity)
 };
 
 // system-scope release / acquire on the counters of the fused allreduce (peer memory over NVLink)
@@ -226,7 +227,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
     }
   }
   const int num_k = p.K / BK;
-  const int num_units = p.num_tiles * p.ksplit;
+  // device-side row count (the prefill side's graph replays for any chunk size, f4; Params.m_dev): p.M is
+  // then the buffers' capacity (TMA maps, grid), the rows this launch covers are read after the previous
+  // kernels' writes are visible
+  int M_ = p.M, num_m2_ = p.num_m2, num_tiles_ = p.num_tiles;
+  if (p.m_dev) {
+    pdl_wait();
+    M_ = *p.m_dev;
+    num_m2_ = (M_ + PAIR_M - 1) / PAIR_M;
+    num_tiles_ = num_m2_ * p.num_n;
+  }
+  const int num_units = num_tiles_ * p.ksplit;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -275,9 +286,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
       int s = 0;
       uint32_t ph = 0, g = 0;
       for (int u = pair; u < num_units; u += n_pairs) {
-        const int t = u % p.num_tiles, kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
+        const int t = u % num_tiles_, kb0 = (u / num_tiles_) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
         int mp, nb;
-        tile_coords(t, p.num_m2, p.num_n, mp, nb);
+        tile_coords(t, num_m2_, p.num_n, mp, nb);
         const int row_x = xoff + mp * PAIR_M + (int)rank * BM;
         const int row_w = w_row_of(nb);
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
@@ -308,12 +319,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
       };
       int pre = 0;
 #ifndef DUET_NO_WPREFETCH
-      if (pair < num_units) {  // fresh ring: the first STAGES stages are free
-        const int kb00 = (pair / p.num_tiles) * p.kb_per;
+      if (pair < num_units && !p.m_dev) {  // fresh ring: the first STAGES stages are free
+        const int kb00 = (pair / num_tiles_) * p.kb_per;
         const int nkb0 = min(num_k, kb00 + p.kb_per) - kb00;
         pre = nkb0 < STAGES ? nkb0 : STAGES;
         int mp0, nb0;
-        tile_coords(pair % p.num_tiles, p.num_m2, p.num_n, mp0, nb0);
+        tile_coords(pair % num_tiles_, num_m2_, p.num_n, mp0, nb0);
         const int row_w0 = w_row(nb0);
         for (int i = 0; i < pre; ++i) {
           if (leader) mbar_expect_tx(&full[i], 2 * STAGE_BYTES);
@@ -325,9 +336,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
       int s = 0;
       uint32_t ph = 0;
       for (int u = pair; u < num_units; u += n_pairs) {
-        const int t = u % p.num_tiles, kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
+        const int t = u % num_tiles_, kb0 = (u / num_tiles_) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
         int mp, nb;
-        tile_coords(t, p.num_m2, p.num_n, mp, nb);
+        tile_coords(t, num_m2_, p.num_n, mp, nb);
         const int row_x = xoff + mp * PAIR_M + (int)rank * BM;
         const int row_w = w_row(nb);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -355,7 +366,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
       uint32_t ph = 0;
       int i = 0;
       for (int u = pair; u < num_units; u += n_pairs, ++i) {
-        const int kb0 = (u / p.num_tiles) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
+        const int kb0 = (u / num_tiles_) * p.kb_per, kb1 = min(num_k, kb0 + p.kb_per);
         const int acc = i & 1;
         mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -383,16 +394,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
     const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
     int i = 0;
     for (int u = pair; u < num_units; u += n_pairs, ++i) {
-      const int t = u % p.num_tiles, sk = u / p.num_tiles;
+      const int t = u % num_tiles_, sk = u / num_tiles_;
       const int acc = i & 1;
       int mp, nb;
-      tile_coords(t, p.num_m2, p.num_n, mp, nb);
+      tile_coords(t, num_m2_, p.num_n, mp, nb);
       // EPI_QKV_ROPE: this row's position, KV page and cos/sin row are fetched while the tile's MMAs
       // still run (the dependent pos -> table / rope loads are off the epilogue's critical path)
       int r_pos = 0, r_page = 0;
       if constexpr (EPI == EPI_QKV_ROPE) {
         const int row_ = mp * PAIR_M + (int)rank * BM + quad * 32 + lane;
-        if (row_ < p.M) {
+        if (row_ < M_) {
           r_pos = p.pos[row_];
           r_page = p.table[(size_t)p.tok_row[row_] * p.max_pages + (r_pos >> 4)];
           const char* cs_ = reinterpret_cast<const char*>(p.rope + (size_t)r_pos * 64);
@@ -412,8 +423,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
           for (int c = 0; c < OUT_COLS; c += 32) {
             float v[32];
             tmem_ld32(tbase + c, v);
-            if (row < p.M && n0 + c < p.N) {
-              float* dst = p.ws + ((size_t)sk * p.M + row) * p.N + n0 + c;
+            if (row < M_ && n0 + c < p.N) {
+              float* dst = p.ws + ((size_t)sk * M_ + row) * p.N + n0 + c;
               if (n0 + c + 32 <= p.N) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
@@ -466,7 +477,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
             st_relaxed_sys(cnt, 0u);  // re-armed: no sender touches it again before this grid ends
           }
           __syncwarp();
-          const bool row_ok = row < p.M;
+          const bool row_ok = row < M_;
           const float* slot0 = p.ar.slots[ar_r] + (size_t)ot * E * PAIR_M * BN + trow;
 #pragma unroll 1
           for (int c = 0; c < BN; c += 32) {
@@ -524,7 +535,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
         // the tile's BN columns are BN / 128 whole heads (d_h = 128): rotate (i, i + 64) pairs of q and k
         // heads at this row's position; q stays in C, k and v go to their KV slots
         {  // tcgen05.ld is warp-collective: every lane loads, only rows < M store
-          const bool row_ok = row < p.M;
+          const bool row_ok = row < M_;
           const int pos = r_pos;
           const int page = r_page;
           const int slot = pos & 15;
@@ -597,7 +608,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = silu_f(v[e]) * u[e];
         }
-        if (row < p.M && n0 + c < p.N) {
+        if (row < M_ && n0 + c < p.N) {
           const bool hi = row >= p.row_split;
           const int rrow = hi ? row - p.row_split : row;
           bf16* dst = (hi ? p.C2 : p.C) + (size_t)rrow * p.ldc + n0 + c;
@@ -653,7 +664,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS + (PROD - 1)
     // (pushed by the tiles' owners), then re-arms the counter for the next launch
     if (warp == 2 && lane == 0 && rank == 0 && pair == 0) {
       unsigned* d = p.ar.done[ar_r];
-      while (ld_acquire_sys(d) < (unsigned)(p.num_tiles * 8)) {
+      while (ld_acquire_sys(d) < (unsigned)(num_tiles_ * 8)) {
       }
       st_relaxed_sys(d, 0u);
     }
@@ -787,7 +798,8 @@ static int launch(const GemmArgs& a, int num_sms, cudaStream_t st) {
     p.rope = a.rope->rope;
   }
   const int num_k = a.K / BK;
-  const int ks = splitk_count(EPI, p.num_tiles, num_k, a.M, a.N, a.ws, a.ws_floats);
+  p.m_dev = a.m_dev;
+  const int ks = a.m_dev ? 1 : splitk_count(EPI, p.num_tiles, num_k, a.M, a.N, a.ws, a.ws_floats);
   p.kb_per = (num_k + ks - 1) / ks;
   p.ksplit = (num_k + p.kb_per - 1) / p.kb_per;
   p.ws = a.ws;

@@ -87,7 +87,7 @@ int launch_gemm_simt(DT dt, const GemmArgs& a, cudaStream_t st) {
 
 // Dispatcher: bf16 shapes the tcgen05 kernel tiles go there; everything else is SIMT.
 int launch_gemm(DT dt, const GemmArgs& a, int num_sms, cudaStream_t st) {
-  if (a.row_split < a.M || a.epi == EPI_QKV_ROPE || a.epi == EPI_RESIDUAL_AR) {  // CTA-pair kernel only (the caller checked)
+  if (a.row_split < a.M || a.epi == EPI_QKV_ROPE || a.epi == EPI_RESIDUAL_AR || a.m_dev) {  // CTA-pair kernel only
     if (dt == DT::BF16 && gemm2_supported(a, num_sms)) return launch_gemm2(a, num_sms, st);
     return -1000000;
   }

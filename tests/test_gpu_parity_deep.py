@@ -23,7 +23,7 @@ from oracle import layer as OL
 from dataclasses import replace as dc_replace
 
 from synth import S_XPRE, configs, counter_values, counter_values_torch, head_weights, page_tables, workload, x_rows
-from tests.gpu_helpers import GpuWorkload, make_ctx
+from tests.gpu_helpers import GpuWorkload, make_ctx, spec_of
 from tests.oracle_run import make_kv, rel_err, run
 from tests.test_gpu_parity import TOL, _check_kv, _check_outputs
 
@@ -300,6 +300,59 @@ def test_prefill_graph_capture_and_replay(cfg_name):
         g.step(ctx, split)
         torch.cuda.synchronize()
         assert ctx.last_step_times()["prefill_graph"] == 0
+    ctx.close()
+
+
+def test_prefill_graph_replays_across_shapes():
+    """f4 "graph-captured prefill via device-side shapes": the spatial prefill side's kernels are
+    launched for the side's capacity and read the chunk's row count and per-sequence lengths from the
+    step's metadata, so the graph captured on one prefill shape replays for another (different row count,
+    sequence count and prefixes) — each step against the oracle, KV slots included, and no new capture
+    (one graph per partition and buffer set)."""
+    cfg = configs.get_config("cfg2-mini")
+    shapes = [[(200, 37), (77, 0)], [(150, 0)], [(64, 300), (33, 17), (129, 0)]]
+    n_cap = max(sum(q for q, _ in sh) for sh in shapes)
+    wls = [workload.build(cfg, pre_seqs=sh, k=2, n_layers=2) for sh in shapes]
+    mp = max(max(wl.pre_tables.shape[1], wl.dec_tables.shape[1]) for wl in wls)
+    mpos = max(max([c + q for q, c in wl.pre_seqs] + [c + wl.k for c in wl.dec_ctx]) for wl in wls) + 32
+    ctx = D.Ctx(spec_of(wls[0].cfg.model, "bf16"), n_cap, max(len(sh) for sh in shapes), len(wls[0].dec_ctx), 2,
+                mp, mpos, D.DUET_DTYPE_BF16)                # capacity for the largest chunk / most sequences
+    parts, total = ctx.partitions()
+    s_d = parts[len(parts) // 2]
+    split = D.split_struct(D.DUET_MODE_SPATIAL, total - s_d, s_d, 2)
+    tol = TOL["bf16"]
+    # the graph is keyed by the buffers (weights, KV pools, the caller's x / y): keep them fixed — pools
+    # sized for the largest workload, each step's history copied in (poison elsewhere), x / y views
+    g0 = GpuWorkload(wls[0], "bf16")
+    n_pages = max(wl.n_pages for wl in wls)
+    m = cfg.model
+    Ks = [torch.empty((n_pages, m.n_kv_heads, 16, m.head_dim), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    Vs = [torch.empty_like(Ks[0]) for _ in range(2)]
+    x_buf = torch.zeros((n_cap, m.d_model), dtype=torch.bfloat16, device="cuda")
+    y_buf = torch.zeros_like(x_buf)
+    seen = []
+    for idx in [0, 0, 1, 2, 0]:
+        wl = wls[idx]
+        y_pre, y_dec, kv_o = run(wl)
+        g = GpuWorkload(wl, "bf16")
+        for l in range(2):
+            Ks[l].fill_(float("nan"))
+            Vs[l].fill_(float("nan"))
+            Ks[l][:wl.n_pages].copy_(g.K[l])
+            Vs[l][:wl.n_pages].copy_(g.V[l])
+        g.K = [Ks[l][:wl.n_pages] for l in range(2)]
+        g.V = [Vs[l][:wl.n_pages] for l in range(2)]
+        g.W = g0.W
+        n_p = sum(q for q, _ in wl.pre_seqs)
+        x_buf[:n_p].copy_(g.x_pre)
+        g.x_pre = x_buf[:n_p]
+        g.y_pre = y_buf[:n_p]
+        g.step(ctx, split)
+        torch.cuda.synchronize()
+        seen.append(ctx.last_step_times()["prefill_graph"])
+        _check_outputs(g, y_pre, y_dec, tol)
+        _check_kv(g, kv_o, tol)
+    assert seen == [0, 1, 1, 1, 1], seen   # direct, capture, then replays across three shapes
     ctx.close()
 
 
