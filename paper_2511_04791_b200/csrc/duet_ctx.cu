@@ -144,15 +144,17 @@ struct Side {
   int cap_rows = 0, cap_seqs = 0, cap_table_rows = 0, pitch = 0;
   void *xa = nullptr, *xb = nullptr, *h = nullptr, *qkv = nullptr, *o = nullptr, *x1 = nullptr, *h2 = nullptr,
        *act = nullptr, *xin = nullptr, *ylast = nullptr;
-  int* meta = nullptr;  // [pos | tok_row | row0 | qlen | cpre | seq_row | step | table]
+  int* meta = nullptr;  // [pos | tok_row | row0 | qlen | cpre | seq_row | step | order | table]
   float *part_o = nullptr, *part_ml = nullptr;
   int part_rows = 0;
   void* logits = nullptr;    // LM head (f1): [decode rows][vocab]
   float* gemm_ws = nullptr;  // split-K partials of the weight-streaming GEMMs (kernels.h GemmArgs)
   size_t gemm_ws_floats = 0;
   // offsets into meta (ints)
-  size_t o_pos = 0, o_tok = 0, o_row0 = 0, o_qlen = 0, o_cpre = 0, o_seqrow = 0, o_step = 0, o_table = 0, n_meta = 0;
+  size_t o_pos = 0, o_tok = 0, o_row0 = 0, o_qlen = 0, o_cpre = 0, o_seqrow = 0, o_step = 0, o_order = 0, o_table = 0,
+         n_meta = 0;
   int* pos() const { return meta + o_pos; }
+  int* order() const { return meta + o_order; }  // decode rows, longest context first
   int* tok() const { return meta + o_tok; }
   int* row0() const { return meta + o_row0; }
   int* qlen() const { return meta + o_qlen; }
@@ -331,6 +333,7 @@ static duet_status side_alloc(duet_ctx* c, Side& s, int cap_rows, int cap_seqs, 
   s.o_cpre = off; off += cap_seqs + 1;
   s.o_seqrow = off; off += cap_seqs + 1;
   s.o_step = off; off += 4;
+  s.o_order = off; off += R;
   s.o_table = off; off += (size_t)std::max(cap_table_rows, 1) * s.pitch;
   s.n_meta = off;
   CUDA_TRY(cudaMalloc(&s.meta, s.n_meta * sizeof(int)));
@@ -463,6 +466,8 @@ static int decode_attn(duet_ctx* c, Side& S, const AttnPlan& ap, const void* q, 
   da.max_len = ((ap.max_len_dec + 1023) / 1024) * 1024;  // same bucket in both modes
   da.n_pages = n_pages;
   da.dev_timer = dev_timer;
+  static const bool ordered = !getenv("DUET_DECODE_ORDER") || atoi(getenv("DUET_DECODE_ORDER")) != 0;
+  da.order = ordered ? S.order() : nullptr;  // DUET_DECODE_ORDER=0: request order as given (A/B)
   return launch_decode_attn(c->dt, da, st);
 }
 
@@ -1036,6 +1041,12 @@ static size_t build_meta(duet_ctx* c, const Side& S, int* img, const duet_prefil
             j < dec->max_pages ? dec->page_table[(size_t)r * dec->max_pages + j] : 0;
       max_len_dec = std::max(max_len_dec, dec->c[r] + 1);
     }
+    // the decode attention's CTAs take the requests longest context first (a stable sort): the last
+    // wave holds the shortest requests, not the longest (the cfg3 ramp put them last)
+    std::vector<int> ord(n_dec);
+    for (int r = 0; r < n_dec; ++r) ord[r] = r;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return dec->c[a] > dec->c[b]; });
+    for (int r = 0; r < n_dec; ++r) img[S.o_order + r] = ord[r];
   }
   img[S.o_step] = 0;
   img[S.o_step + 1] = n_pre + n_dec;  // the side's rows, read on the device by shape-agnostic prefill graphs (f4)

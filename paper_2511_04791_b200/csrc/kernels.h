@@ -138,6 +138,9 @@ struct DecodeAttnArgs {
   // [1] latest CTA end (%globaltimer ns), [2] CTAs done, [3] sum of launch durations (ns), [4] launches;
   // the last CTA of a launch adds end - start to [3] and re-arms [0..2].  nullptr = off.
   unsigned long long* dev_timer = nullptr;
+  // nullable device [n]: the request each CTA column z takes (longest first: a shorter last wave); the
+  // results do not depend on it (every request is computed by its own CTAs)
+  const int* order = nullptr;
 };
 int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st);
 bool decode_tc_supported(const DecodeAttnArgs& a);

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   pdl_wait();
   if (a.dev_timer && threadIdx.x == 0) dev_timer_start(a.dev_timer);
-  const int split = blockIdx.x, kvh = blockIdx.y, r = blockIdx.z;
+  const int split = blockIdx.x, kvh = blockIdx.y, r = a.order ? a.order[blockIdx.z] : (int)blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.hq / a.hkv;
   const int len = a.pos[r] + 1;
