@@ -261,6 +261,10 @@ duet_status duet_nccl_unique_id(void* out, int32_t len);
 duet_status duet_ctx_set_comms(duet_ctx* ctx, int32_t rank, const void* id_decode, const void* id_prefill);
 duet_status duet_calibrate_allreduce(duet_ctx* ctx, double* alpha_s, double* bw_bytes_s);
 duet_status duet_ctx_check_comms(duet_ctx* ctx);
+/* 1 if the last temporal duet_step ran a layer's two attentions as the fused POD launch (SURVEY §8(f) f4,
+ * prefill-attention and decode-attention CTAs in one grid instead of the green-context co-run;
+ * opt-in with DUET_POD=1, used whenever the co-run model splits the step), else 0. */
+int32_t duet_ctx_last_pod(duet_ctx* ctx);
 
 /* ----------------------------------------------------------------- fused GEMM + allreduce (f3)
  * SURVEY §8(f) f3; P:233-236 (§4.1 Communication Operators: in a head-sharded TP block the O and FFN-down

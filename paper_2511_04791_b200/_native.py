@@ -135,6 +135,7 @@ _SIGS = {
     "duet_ctx_set_comms": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "duet_calibrate_allreduce": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "duet_ctx_check_comms": (C.c_int, [C.c_void_p]),
+    "duet_ctx_last_pod": (C.c_int32, [C.c_void_p]),
     "duet_ctx_ar_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "duet_ctx_ar_open": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "duet_op_gemm_ar_emul": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -434,6 +435,10 @@ class Ctx:
         a = C.create_string_buffer(bytes(id_decode), 128)
         b = C.create_string_buffer(bytes(id_prefill), 128)
         _check(lib().duet_ctx_set_comms(self.h, int(rank), a, b))
+
+    def last_pod(self) -> bool:
+        """Did the last temporal step run its attentions as the fused POD launch (duet_ctx_last_pod)?"""
+        return bool(lib().duet_ctx_last_pod(self.h))
 
     def check_comms(self):
         """Raises DuetError(NCCL) when a communicator reports an asynchronous error (duet_ctx_check_comms)."""

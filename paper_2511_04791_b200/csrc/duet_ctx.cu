@@ -216,6 +216,7 @@ struct duet_ctx {
   uint64_t graph_clock = 0;
   // last step
   int last_mode = -1, last_k = 0, last_kernels = 0, last_corun = 0;
+  bool last_pod = false;  // the last temporal step ran its attentions as the fused POD launch (f4)
   bool last_pre_graph = false;  // the last spatial step's prefill side replayed a graph
   bool last_has_dec = false, last_has_pre = false;
   // live kernel timing
@@ -408,7 +409,7 @@ static Partition* corun_pick(duet_ctx* c, const AttnPlan& ap) {
 // duet_step and of duet_op_prefill_attn.  Returns the kernels launched (<= 0: could not launch).
 static int prefill_attn(duet_ctx* c, Side& S, const AttnPlan& ap, const void* q, int q_stride, void* o,
                         int total_rows, const void* k_pool, const void* v_pool, int n_pages, int num_sms,
-                        cudaStream_t st) {
+                        cudaStream_t st, PrefillAttnArgs* args_only = nullptr) {
   const auto& sp = c->spec;
   PrefillAttnArgs pa{};
   pa.q = q;
@@ -435,6 +436,10 @@ static int prefill_attn(duet_ctx* c, Side& S, const AttnPlan& ap, const void* q,
   pa.max_len = ap.max_len_pre;
   pa.n_pages = n_pages;
   pa.total_rows = total_rows;
+  if (args_only) {  // the fused POD launch takes the arguments
+    *args_only = pa;
+    return 1;
+  }
   return launch_prefill_attn(c->dt, pa, st);
 }
 
@@ -442,7 +447,7 @@ static int prefill_attn(duet_ctx* c, Side& S, const AttnPlan& ap, const void* q,
 // ap.n_pre prefill rows in side S's metadata; q / o point at the first decode row.
 static int decode_attn(duet_ctx* c, Side& S, const AttnPlan& ap, const void* q, int q_stride, void* o,
                        const void* k_pool, const void* v_pool, int n_pages, int num_sms, cudaStream_t st,
-                       unsigned long long* dev_timer = nullptr) {
+                       unsigned long long* dev_timer = nullptr, DecodeAttnArgs* args_only = nullptr) {
   const auto& sp = c->spec;
   DecodeAttnArgs da{};
   da.q = q;
@@ -468,6 +473,10 @@ static int decode_attn(duet_ctx* c, Side& S, const AttnPlan& ap, const void* q, 
   da.dev_timer = dev_timer;
   static const bool ordered = !getenv("DUET_DECODE_ORDER") || atoi(getenv("DUET_DECODE_ORDER")) != 0;
   da.order = ordered ? S.order() : nullptr;  // DUET_DECODE_ORDER=0: request order as given (A/B)
+  if (args_only) {
+    *args_only = da;
+    return 1;
+  }
   return launch_decode_attn(c->dt, da, st);
 }
 
@@ -570,6 +579,30 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     // 4. attention; with a co-run partition the two attentions run side by side (compute-bound
     // prefill on the remainder, HBM-bound decode on S_d SMs) and the O GEMM waits for both
     Partition* cp = (c->corun && ap.n_pre > 0 && ap.n_dec > 0 && !c->capturing) ? c->corun : nullptr;
+    // f4 POD-style fused attention (kernels_pod.cu): the co-run split as ONE launch on the full-device
+    // stream — prefill-attention CTAs and S_d decode-attention CTAs in one grid, no fork / join.  Opt-in
+    // (DUET_POD=1): measured 1-2 % slower per cfg2 step than the two launches on the green-context pair
+    // (profiles/r02_pod_ab.txt), which stay the default
+    static const bool pod_env = getenv("DUET_POD") && atoi(getenv("DUET_POD")) != 0;
+    if (cp && pod_env && dt == DT::BF16 && dh == 128) {
+      PrefillAttnArgs pa{};
+      DecodeAttnArgs da{};
+      prefill_attn(c, S, ap, S.qkv, nqkv, S.o, n_rows, kv->k_pool[l], kv->v_pool[l], kv->n_pages, num_sms, st, &pa);
+      decode_attn(c, S, ap, (const char*)S.qkv + (size_t)ap.n_pre * nqkv * es, nqkv,
+                  (char*)S.o + (size_t)ap.n_pre * hq * dh * es, kv->k_pool[l], kv->v_pool[l], kv->n_pages, num_sms, st,
+                  nullptr, &da);
+      if (fa_tc_supported(pa) && decode_tc_supported(da)) {
+        const int pi = prof_begin(c, st, DUET_KCLASS_PREFILL_ATTN);
+        const int r = launch_pod_attn(dt, pa, da, cp->s_d, st);
+        if (r <= 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "layer %d: fused prefill + decode attention could not be launched", l);
+        prof_end(c, st, pi, DUET_KCLASS_PREFILL_ATTN, ap.attn_flops_pre, ap.attn_bytes_pre);
+        nk += r;
+        cp = nullptr;
+        c->last_pod = true;
+        goto attention_done;
+      }
+    }
+    {
     cudaStream_t st_pa = st, st_da = st;
     int sms_pa = num_sms, sms_da = num_sms;
     if (cp) {
@@ -611,6 +644,8 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       CUDA_TRY(cudaStreamWaitEvent(st, c->ev_ca, 0));
       CUDA_TRY(cudaStreamWaitEvent(st, c->ev_cb, 0));
     }
+    }
+  attention_done:
     // 5. x1 = x + o W_o^T
     // TP: the O projection of this rank's heads is a partial sum; rank 0 adds the
     // residual and the partials are all-reduced over the side's communicator
@@ -1223,6 +1258,7 @@ extern "C" duet_status duet_step(duet_ctx* c, const duet_layer_weights* w, const
       }
     }
     c->last_corun = c->corun ? c->corun->s_d : 0;
+    c->last_pod = false;
     if (n_rows > 0 && !(has_pre && has_dec)) {  // one phase only: its own buffers, whatever the GEMM path
       DUET_TRY(run_layers(c, c->pre, st, c->total_sms, n_rows, has_pre ? pre->x : dec->x, has_pre ? pre->y : dec->y,
                           w, kv, ap, &kernels));
@@ -1658,6 +1694,8 @@ extern "C" duet_status duet_op_gemm_ar_emul(duet_ctx* c, int32_t n_ranks, const 
   DUET_TRY(check_launch("gemm_ar_emul"));
   return DUET_OK;
 }
+
+extern "C" int32_t duet_ctx_last_pod(duet_ctx* c) { return c && c->last_pod ? 1 : 0; }
 
 extern "C" duet_status duet_ctx_check_comms(duet_ctx* c) {
   clear_error();

@@ -179,6 +179,12 @@ bool fa_prefill_supported(const PrefillAttnArgs& a);
 int launch_fa_prefill(const PrefillAttnArgs& a, cudaStream_t st);
 bool fa_tc_supported(const PrefillAttnArgs& a);
 int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st);
+// POD-style fused prefill + decode attention (f4, kernels_pod.cu): one launch, the first CTAs run the
+// persistent tcgen05 prefill attention, the last n_dec_ctas the paged decode attention (+ the LSE combine
+// as a second kernel when the batch splits); bf16, d_h 128.  Returns kernels launched, < 0 if unsupported.
+int launch_pod_attn(DT dt, const PrefillAttnArgs& pa, const DecodeAttnArgs& da, int n_dec_ctas, cudaStream_t st);
+int launch_pod_tc(const PrefillAttnArgs& pa, const DecodeAttnArgs& da, int pps, int n_splits, int n_dec_ctas,
+                  cudaStream_t st);
 // CTA-pair (cta_group::2) version, opt-in with DUET_FA2=1 (measured slower than the one-CTA kernel)
 bool fa2_tc_supported(const PrefillAttnArgs& a);
 int launch_fa2_tc(const PrefillAttnArgs& a, cudaStream_t st);

@@ -209,21 +209,41 @@ static void dispatch_g(const DecodeAttnArgs& a, dim3 grid, int pps, int ns, cuda
   }
 }
 
-int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st) {
-  if (a.n <= 0) return 0;
+// split plan of a decode batch: (pages per split, splits) from the batch shape only
+static void decode_split_plan(const DecodeAttnArgs& a, int* pps_out, int* ns_out) {
   const int max_pages = (a.max_len + kPage - 1) / kPage;
   const int base = a.n * a.hkv;
-  // The split count depends only on the batch shape (never on the partition size), so a
-  // request's result is bitwise identical whichever SM split or mode runs it.
   const int target = 148 * 4;
   int ns = (target + base - 1) / base;
   ns = ns < 1 ? 1 : ns;
-  const int cap_pages = (max_pages + 3) / 4;  // at least ~4 pages (one per warp) per split
+  const int cap_pages = (max_pages + 3) / 4;
   if (ns > cap_pages) ns = cap_pages;
   if (ns > a.max_splits) ns = a.max_splits;
   if (ns < 1) ns = 1;
   const int pps = (max_pages + ns - 1) / ns;
-  ns = (max_pages + pps - 1) / pps;
+  *ns_out = (max_pages + pps - 1) / pps;
+  *pps_out = pps;
+}
+
+// f4 fused launch (kernels_pod.cu) + the LSE combine when the decode batch splits
+int launch_pod_attn(DT dt, const PrefillAttnArgs& pa, const DecodeAttnArgs& da, int n_dec_ctas, cudaStream_t st) {
+  if (dt != DT::BF16 || pa.total_q <= 0 || da.n <= 0) return -1;
+  int pps, ns;
+  decode_split_plan(da, &pps, &ns);
+  if (launch_pod_tc(pa, da, pps, ns, n_dec_ctas, st) <= 0) return -1;
+  if (ns > 1) {
+    launch_pdl(attn_combine_kernel<bf16>, da.n * da.hq, 128, 0, st, da, ns);
+    return 2;
+  }
+  return 1;
+}
+
+int launch_decode_attn(DT dt, const DecodeAttnArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return 0;
+  // The split count depends only on the batch shape (never on the partition size), so a
+  // request's result is bitwise identical whichever SM split or mode runs it.
+  int pps, ns;
+  decode_split_plan(a, &pps, &ns);
   dim3 grid(ns, a.hkv, a.n);
   bool ok = true;
   if (dt == DT::BF16 && decode_tc_supported(a)) {

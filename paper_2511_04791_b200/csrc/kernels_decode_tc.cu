@@ -115,17 +115,25 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 // WARPS consumer warps per CTA, NST-stage ring per warp; TMA = pages fetched by TMA boxes (lane 0),
 // else by cp.async from all 32 lanes (cheaper to issue on small SM partitions).
+// One work item (split of the pages, kv head, request column z) by a group of WARPS warps — the body of
+// decode_tc_kernel (the CTA is one group, one item per CTA) and of the decode part of the fused POD launch
+// (kernels_pod.cu: three 4-warp groups per CTA, each the standalone kernel's CTA, items strided over the
+// groups — so the results are bitwise those of the standalone launch).  smem: the group's rings (1 KiB
+// aligned), tid: thread index in the group, bar: 0 = the whole CTA is the group (__syncthreads), else the
+// named barrier the group's WARPS * 32 threads use.  Ends with a barrier-separated merge through the rings.
 template <int WARPS, int NST, bool TMA>
-__global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_constant__ CUtensorMap map_k,
-                                                                const __grid_constant__ CUtensorMap map_v,
-                                                                DecodeAttnArgs a, int pps, int n_splits) {
+__device__ __forceinline__ void decode_tc_item(const CUtensorMap* mk_, const CUtensorMap* mv_, const DecodeAttnArgs& a,
+                                               int pps, int n_splits, const int split, const int kvh, const int zc,
+                                               uint8_t* smem, const int tid, const int bar) {
+  const CUtensorMap& map_k = *mk_;
+  const CUtensorMap& map_v = *mv_;
   constexpr int WARP_BYTES = NST * STAGE_BYTES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  pdl_wait();
-  if (a.dev_timer && threadIdx.x == 0) dev_timer_start(a.dev_timer);
-  const int split = blockIdx.x, kvh = blockIdx.y, r = a.order ? a.order[blockIdx.z] : (int)blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto group_sync = [&]() {
+    if (bar == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(WARPS * 32) : "memory");
+  };
+  const int r = a.order ? a.order[zc] : zc;
+  const int warp = tid >> 5, lane = tid & 31;
   const int G = a.hq / a.hkv;
   const int len = a.pos[r] + 1;
   const int n_pages = (len + PAGE - 1) / PAGE;
@@ -317,7 +325,7 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
     l[h] += __shfl_xor_sync(0xffffffffu, l[h], 8);
     l[h] += __shfl_xor_sync(0xffffffffu, l[h], 16);
   }
-  __syncthreads();
+  group_sync();
   pdl_trigger();  // only the merge is left
   // merge the warps (heads h < G); the rings are no longer needed
   float* sm_o = reinterpret_cast<float*>(smem);  // [WARPS][8 heads][DH]
@@ -336,8 +344,8 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
     sm_o[(warp * 8 + 2 * t4) * DH + d0 + 8] = o[mt][2];
     sm_o[(warp * 8 + 2 * t4 + 1) * DH + d0 + 8] = o[mt][3];
   }
-  __syncthreads();
-  for (int t = threadIdx.x; t < G * DH; t += blockDim.x) {
+  group_sync();
+  for (int t = tid; t < G * DH; t += WARPS * 32) {
     const int h = t / DH, dim = t % DH;
     float M = -INFINITY;
 #pragma unroll
@@ -364,11 +372,25 @@ __global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_cons
       }
     }
   }
+}
+
+template <int WARPS, int NST, bool TMA>
+__global__ void __launch_bounds__(WARPS * 32) decode_tc_kernel(const __grid_constant__ CUtensorMap map_k,
+                                                                const __grid_constant__ CUtensorMap map_v,
+                                                                DecodeAttnArgs a, int pps, int n_splits) {
+  pdl_wait();
+  if (a.dev_timer && threadIdx.x == 0) dev_timer_start(a.dev_timer);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  decode_tc_item<WARPS, NST, TMA>(&map_k, &map_v, a, pps, n_splits, (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z,
+                                  smem, (int)threadIdx.x, 0);
   if (a.dev_timer) {
     __syncthreads();
     if (threadIdx.x == 0) dev_timer_end(a.dev_timer);
   }
 }
+
+#ifndef DUET_BODIES_ONLY
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -397,7 +419,9 @@ static bool pool_map(CUtensorMap* m, const void* pool, uint64_t rows) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+#endif  // DUET_BODIES_ONLY
 }  // namespace dtc
+#ifndef DUET_BODIES_ONLY
 
 bool decode_tc_supported(const DecodeAttnArgs& a) {
   const int G = a.hq / a.hkv;
@@ -442,4 +466,5 @@ int launch_decode_tc(const DecodeAttnArgs& a, int pps, int n_splits, cudaStream_
   return 1;
 }
 
+#endif  // DUET_BODIES_ONLY
 }  // namespace duet

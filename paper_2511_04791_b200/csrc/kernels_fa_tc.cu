@@ -226,9 +226,11 @@ struct Item {
   int s_id, qt, pair, qlen, row0, cpre, q0, kvh, head_a, n_heads, kv_end, n_kt;
   const int* tab;
 };
-__device__ __forceinline__ bool item_at(const Params& p, int k, Item& it, bool& live) {
-  const int G = gridDim.x, T = p.n_qtiles * p.n_seqs * p.n_pairs;
-  const int idx = k * G + ((k & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
+// cta / n_ctas: this CTA among the CTAs running prefill attention (the grid, or the prefill part of the
+// fused POD launch, kernels_pod.cu)
+__device__ __forceinline__ bool item_at(const Params& p, int k, Item& it, bool& live, int cta, int n_ctas) {
+  const int G = n_ctas, T = p.n_qtiles * p.n_seqs * p.n_pairs;
+  const int idx = k * G + ((k & 1) ? G - 1 - cta : cta);
   if (idx >= T) return false;
   it.pair = idx % p.n_pairs;
   it.s_id = (idx / p.n_pairs) % p.n_seqs;
@@ -251,7 +253,7 @@ __device__ __forceinline__ bool item_at(const Params& p, int k, Item& it, bool& 
 }
 
 template <int K_STAGES, int V_STAGES>
-__global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant__ CUtensorMap map_q, Params p) {
+__device__ __forceinline__ void fa_tc_body(const CUtensorMap* mq, const Params& p, const int cta, const int n_ctas) {
   using RG = Ring<K_STAGES, V_STAGES>;
   constexpr int OFF_V = RG::OFF_V, OFF_BAR = RG::OFF_BAR, OFF_TRACE = RG::OFF_TRACE;
   extern __shared__ uint8_t smem_raw[];
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   pdl_wait();  // set-up above overlaps the previous kernel's tail
   // timeline debugging (DUET_FA_TRACE=1): event e of tile j, clock() relative to kernel start
   uint32_t* trace = (uint32_t*)(smem + OFF_TRACE);
-  bool tr = (p.trace & 1) && blockIdx.x == 0;  // CTA 0's first work item
+  bool tr = (p.trace & 1) && cta == 0;  // CTA 0's first work item
   const uint32_t t_start = (uint32_t)clock();
   auto stamp = [&](int e, int j) {
     if (tr && lane == 0 && j < TRACE_MAXJ) trace[e * TRACE_MAXJ + j] = (uint32_t)clock() - t_start;
@@ -316,13 +318,13 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
       int ni = 0;
       Item it;
       bool live;
-      for (int k = 0; item_at(p, k, it, live); ++k) {
+      for (int k = 0; item_at(p, k, it, live, cta, n_ctas); ++k) {
         if (!live) continue;
         mbar_wait(q_empty, (ni & 1) ^ 1);
         mbar_expect_tx(q_full, it.n_heads * Q_BYTES);
         for (int h = 0; h < it.n_heads; ++h) {
-          tma_load_2d(&map_q, q_full, smem + OFF_Q + h * Q_BYTES, (it.head_a + h) * DH, it.row0 + it.q0);
-          tma_load_2d(&map_q, q_full, smem + OFF_Q + h * Q_BYTES + Q_SUB, (it.head_a + h) * DH + 64, it.row0 + it.q0);
+          tma_load_2d(mq, q_full, smem + OFF_Q + h * Q_BYTES, (it.head_a + h) * DH, it.row0 + it.q0);
+          tma_load_2d(mq, q_full, smem + OFF_Q + h * Q_BYTES + Q_SUB, (it.head_a + h) * DH + 64, it.row0 + it.q0);
         }
         ++ni;
       }
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
     int g = 0;  // tiles streamed by this CTA so far (ring position across work items)
     Item it;
     bool live;
-    for (int k = 0; item_at(p, k, it, live); ++k) {
+    for (int k = 0; item_at(p, k, it, live, cta, n_ctas); ++k) {
      if (!live) continue;
      const int kv_end = it.kv_end;
      const int* tab = it.tab;
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
     int gp[2] = {0, 0};              // P tiles per head
     Item it;
     bool live;
-    for (int k = 0; item_at(p, k, it, live); ++k) {
+    for (int k = 0; item_at(p, k, it, live, cta, n_ctas); ++k) {
       if (!live) continue;
       const int n_kt = it.n_kt, n_heads = it.n_heads;
       mbar_wait(q_full, ni & 1);
@@ -464,7 +466,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
     int gs = 0, ni_h = 0;  // S tiles and work items of this head so far
     Item it;
     bool live;
-    for (int k = 0; item_at(p, k, it, live); ++k) {
+    for (int k = 0; item_at(p, k, it, live, cta, n_ctas); ++k) {
       if (!live || h >= it.n_heads) continue;  // an odd last head of a group runs alone (no head B)
       const int n_kt = it.n_kt, q0 = it.q0, qlen = it.qlen, row0 = it.row0, head_a = it.head_a;
       const int pos = min(it.cpre + q0 + r, it.kv_end - 1);  // clamp rows past the chunk
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
         Item nx;
         bool nlive = false;
         int kk = k + 1;
-        while (item_at(p, kk, nx, nlive) && !nlive) ++kk;
+        while (item_at(p, kk, nx, nlive, cta, n_ctas) && !nlive) ++kk;
         if (!nlive) pdl_trigger();
       }
       // epilogue: O / l -> bf16 -> global
@@ -595,7 +597,7 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   }
   tc_before();
   __syncthreads();
-  if ((p.trace & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+  if ((p.trace & 1) && cta == 0 && threadIdx.x == 0) {
     const int n_kt = (int)trace[10 * TRACE_MAXJ];
     printf("FA_TRACE n_kt=%d (clock cycles; ev: 0 load-issue 1 kv_full 2 S-issued 3 PV-issued 4 s_full 5 exps-done 6 P-published)\n", n_kt);
     for (int j = 0; j < n_kt && j < TRACE_MAXJ; ++j)
@@ -609,6 +611,12 @@ __global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant
   }
 }
 
+template <int K_STAGES, int V_STAGES>
+__global__ void __launch_bounds__(THREADS, 1) fa_tc_kernel(const __grid_constant__ CUtensorMap map_q, Params p) {
+  fa_tc_body<K_STAGES, V_STAGES>(&map_q, p, (int)blockIdx.x, (int)gridDim.x);
+}
+
+#ifndef DUET_BODIES_ONLY
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -636,7 +644,9 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t c
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+#endif  // DUET_BODIES_ONLY
 }  // namespace fatc
+#ifndef DUET_BODIES_ONLY
 
 bool fa_tc_supported(const PrefillAttnArgs& a) {
   return a.dh == fatc::DH && a.page_size == fatc::PAGE && a.q_stride % 8 == 0 && fatc::encode_fn() != nullptr &&
@@ -677,4 +687,5 @@ int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   return 1;
 }
 
+#endif  // DUET_BODIES_ONLY
 }  // namespace duet

@@ -284,6 +284,11 @@ def test_parity_cfg2_full_layer_temporal_and_optimizer_split():
     # f4: at this size the attention co-run model picks an SM split; the same kernels on fewer SMs
     # give the same function as the one-after-the-other temporal step (NO_CORUN context)
     assert ctx.last_step_times()["corun_s_d"] > 0
+    # f4 with DUET_POD=1 (test_fused_pod_attention_parity_subprocess): the co-run split runs as ONE fused POD
+    # launch (prefill-attention and decode-attention CTAs in one grid) — bitwise the one-after-the-other
+    # step too, since each role runs the same per-item algorithm as its standalone kernel
+    import os
+    assert ctx.last_pod() == (os.environ.get("DUET_POD", "0") not in ("", "0"))
     g_seq, ctx_seq = _run_split(wl, "bf16", lambda c: D.split_struct(D.DUET_MODE_TEMPORAL, 148, 0, 1),
                                 D.DUET_CTX_NO_CORUN)
     assert ctx_seq.last_step_times()["corun_s_d"] == 0
@@ -458,6 +463,23 @@ def test_forced_attention_corun_parity_subprocess():
                         "-k", "llama_shapes or qwen or running_max"], env=env, capture_output=True, text=True,
                        timeout=900, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "3 passed" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.skipif(bool(__import__("os").environ.get("DUET_POD")), reason="already the POD run")
+def test_fused_pod_attention_parity_subprocess():
+    """f4 POD-style fused attention (DUET_POD=1, read once per process: a fresh process): the two attentions
+    of a temporal step as ONE launch — the cfg2 layer at BASELINE size bitwise equal to the one-after-the-
+    other step and against the oracle, and the forced 16-SM co-run cases (ragged Llama prefixes, Qwen GQA-5 +
+    bias, running-max re-base) against the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for extra, k, n in (({}, "cfg2_full", 1), ({"DUET_CORUN": "16"}, "llama_shapes or qwen or running_max", 3)):
+        env = dict(os.environ, DUET_POD="1", **extra)
+        r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                            "-k", k], env=env, capture_output=True, text=True, timeout=900, cwd=root)
+        assert r.returncode == 0 and f"{n} passed" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 @pytest.mark.skipif(bool(__import__("os").environ.get("DUET_GEMM2_BN")), reason="already the forced-width run")
