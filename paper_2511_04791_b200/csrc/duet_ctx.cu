@@ -584,6 +584,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
     // (DUET_POD=1): measured 1-2 % slower per cfg2 step than the two launches on the green-context pair
     // (profiles/r02_pod_ab.txt), which stay the default
     static const bool pod_env = getenv("DUET_POD") && atoi(getenv("DUET_POD")) != 0;
+    bool pod_done = false;
     if (cp && pod_env && dt == DT::BF16 && dh == 128) {
       PrefillAttnArgs pa{};
       DecodeAttnArgs da{};
@@ -599,53 +600,52 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
         nk += r;
         cp = nullptr;
         c->last_pod = true;
-        goto attention_done;
+        pod_done = true;
       }
     }
-    {
-    cudaStream_t st_pa = st, st_da = st;
-    int sms_pa = num_sms, sms_da = num_sms;
-    if (cp) {
-      CUDA_TRY(cudaEventRecord(c->ev_cf, st));
-      CUDA_TRY(cudaStreamWaitEvent(cp->s_pre, c->ev_cf, 0));
-      CUDA_TRY(cudaStreamWaitEvent(cp->s_dec, c->ev_cf, 0));
-      st_pa = cp->s_pre;
-      sms_pa = cp->s_p;
-      st_da = cp->s_dec;
-      sms_da = cp->s_d;
-    }
-    if (ap.n_pre > 0) {
-      const int pi = prof_begin(c, st_pa, DUET_KCLASS_PREFILL_ATTN);
-      const int r = prefill_attn(c, S, ap, S.qkv, nqkv, S.o, n_rows, kv->k_pool[l], kv->v_pool[l], kv->n_pages,
-                                 sms_pa, st_pa);
-      if (r <= 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "layer %d: prefill attention could not be launched", l);
-      prof_end(c, st_pa, pi, DUET_KCLASS_PREFILL_ATTN, ap.attn_flops_pre, ap.attn_bytes_pre);
-      if (dbg_sync && !c->capturing) {
-        fprintf(stderr, "[duet] layer %d: prefill attention ...", l);
-        fprintf(stderr, " %s\n", cudaGetErrorString(cudaStreamSynchronize(st_pa)));
+    if (!pod_done) {  // the two attentions as two launches (sequential, or co-run on the green-context pair)
+      cudaStream_t st_pa = st, st_da = st;
+      int sms_pa = num_sms, sms_da = num_sms;
+      if (cp) {
+        CUDA_TRY(cudaEventRecord(c->ev_cf, st));
+        CUDA_TRY(cudaStreamWaitEvent(cp->s_pre, c->ev_cf, 0));
+        CUDA_TRY(cudaStreamWaitEvent(cp->s_dec, c->ev_cf, 0));
+        st_pa = cp->s_pre;
+        sms_pa = cp->s_p;
+        st_da = cp->s_dec;
+        sms_da = cp->s_d;
       }
-      nk += r;
+      if (ap.n_pre > 0) {
+        const int pi = prof_begin(c, st_pa, DUET_KCLASS_PREFILL_ATTN);
+        const int r = prefill_attn(c, S, ap, S.qkv, nqkv, S.o, n_rows, kv->k_pool[l], kv->v_pool[l], kv->n_pages,
+                                   sms_pa, st_pa);
+        if (r <= 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "layer %d: prefill attention could not be launched", l);
+        prof_end(c, st_pa, pi, DUET_KCLASS_PREFILL_ATTN, ap.attn_flops_pre, ap.attn_bytes_pre);
+        if (dbg_sync && !c->capturing) {
+          fprintf(stderr, "[duet] layer %d: prefill attention ...", l);
+          fprintf(stderr, " %s\n", cudaGetErrorString(cudaStreamSynchronize(st_pa)));
+        }
+        nk += r;
+      }
+      if (ap.n_dec > 0) {
+        const int pi = prof_begin(c, st_da, DUET_KCLASS_DECODE_ATTN);
+        // inside a graph capture the class is timed on the device (no events in graphs)
+        unsigned long long* dt_ = c->capturing && c->prof_on && (c->prof_mask & (1 << DUET_KCLASS_DECODE_ATTN))
+                                      ? c->dev_timer : nullptr;
+        const int r = decode_attn(c, S, ap, (const char*)S.qkv + (size_t)ap.n_pre * nqkv * es, nqkv,
+                                  (char*)S.o + (size_t)ap.n_pre * hq * dh * es, kv->k_pool[l], kv->v_pool[l],
+                                  kv->n_pages, sms_da, st_da, dt_);
+        if (r <= 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "layer %d: decode attention could not be launched", l);
+        prof_end(c, st_da, pi, DUET_KCLASS_DECODE_ATTN, ap.attn_flops_dec, ap.attn_bytes_dec);
+        nk += r;
+      }
+      if (cp) {
+        CUDA_TRY(cudaEventRecord(c->ev_ca, cp->s_pre));
+        CUDA_TRY(cudaEventRecord(c->ev_cb, cp->s_dec));
+        CUDA_TRY(cudaStreamWaitEvent(st, c->ev_ca, 0));
+        CUDA_TRY(cudaStreamWaitEvent(st, c->ev_cb, 0));
+      }
     }
-    if (ap.n_dec > 0) {
-      const int pi = prof_begin(c, st_da, DUET_KCLASS_DECODE_ATTN);
-      // inside a graph capture the class is timed on the device (no events in graphs)
-      unsigned long long* dt_ = c->capturing && c->prof_on && (c->prof_mask & (1 << DUET_KCLASS_DECODE_ATTN))
-                                    ? c->dev_timer : nullptr;
-      const int r = decode_attn(c, S, ap, (const char*)S.qkv + (size_t)ap.n_pre * nqkv * es, nqkv,
-                                (char*)S.o + (size_t)ap.n_pre * hq * dh * es, kv->k_pool[l], kv->v_pool[l],
-                                kv->n_pages, sms_da, st_da, dt_);
-      if (r <= 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "layer %d: decode attention could not be launched", l);
-      prof_end(c, st_da, pi, DUET_KCLASS_DECODE_ATTN, ap.attn_flops_dec, ap.attn_bytes_dec);
-      nk += r;
-    }
-    if (cp) {
-      CUDA_TRY(cudaEventRecord(c->ev_ca, cp->s_pre));
-      CUDA_TRY(cudaEventRecord(c->ev_cb, cp->s_dec));
-      CUDA_TRY(cudaStreamWaitEvent(st, c->ev_ca, 0));
-      CUDA_TRY(cudaStreamWaitEvent(st, c->ev_cb, 0));
-    }
-    }
-  attention_done:
     // 5. x1 = x + o W_o^T
     // TP: the O projection of this rank's heads is a partial sum; rank 0 adds the
     // residual and the partials are all-reduced over the side's communicator
