@@ -38,8 +38,9 @@ def _ctx_for_ops(M):
     return make_ctx(wl, "bf16", extra_tokens=M)
 
 
-@pytest.mark.parametrize("n,M,N,K", [(1, 300, 512, 384), (2, 300, 512, 384), (4, 1000, 768, 256),
-                                     (8, 257, 256, 128), (2, 2112, 4096, 2048), (4, 2112, 4096, 1024)])
+@pytest.mark.parametrize("n,M,N,K", [(1, 300, 512, 384), (2, 300, 512, 384), (3, 520, 1024, 192),
+                                     (4, 1000, 768, 256), (8, 257, 256, 128), (2, 2112, 4096, 2048),
+                                     (4, 2112, 4096, 1024)])
 def test_gemm_allreduce_emulated_ranks(n, M, N, K):
     """Every emulated rank's output equals the oracle's R + sum_r A_r B_r^T within the bf16 tolerance and all
     ranks hold bitwise the same rows (one owner computes each tile and pushes it to every rank).  Ragged
