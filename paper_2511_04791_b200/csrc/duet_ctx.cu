@@ -409,7 +409,7 @@ static Partition* corun_pick(duet_ctx* c, const AttnPlan& ap) {
 // duet_step and of duet_op_prefill_attn.  Returns the kernels launched (<= 0: could not launch).
 static int prefill_attn(duet_ctx* c, Side& S, const AttnPlan& ap, const void* q, int q_stride, void* o,
                         int total_rows, const void* k_pool, const void* v_pool, int n_pages, int num_sms,
-                        cudaStream_t st, PrefillAttnArgs* args_only = nullptr) {
+                        cudaStream_t st, PrefillAttnArgs* args_only = nullptr, const int* shape_dev = nullptr) {
   const auto& sp = c->spec;
   PrefillAttnArgs pa{};
   pa.q = q;
@@ -436,6 +436,7 @@ static int prefill_attn(duet_ctx* c, Side& S, const AttnPlan& ap, const void* q,
   pa.max_len = ap.max_len_pre;
   pa.n_pages = n_pages;
   pa.total_rows = total_rows;
+  pa.shape_dev = shape_dev;
   if (args_only) {  // the fused POD launch takes the arguments
     *args_only = pa;
     return 1;
@@ -618,7 +619,7 @@ static duet_status run_layers(duet_ctx* c, Side& S, cudaStream_t st, int num_sms
       if (ap.n_pre > 0) {
         const int pi = prof_begin(c, st_pa, DUET_KCLASS_PREFILL_ATTN);
         const int r = prefill_attn(c, S, ap, S.qkv, nqkv, S.o, n_rows, kv->k_pool[l], kv->v_pool[l], kv->n_pages,
-                                   sms_pa, st_pa);
+                                   sms_pa, st_pa, nullptr, n_dev);  // n_dev: the step's shape in the metadata
         if (r <= 0) DUET_FAIL(DUET_ERR_UNSUPPORTED, "layer %d: prefill attention could not be launched", l);
         prof_end(c, st_pa, pi, DUET_KCLASS_PREFILL_ATTN, ap.attn_flops_pre, ap.attn_bytes_pre);
         if (dbg_sync && !c->capturing) {
@@ -1084,7 +1085,9 @@ static size_t build_meta(duet_ctx* c, const Side& S, int* img, const duet_prefil
     for (int r = 0; r < n_dec; ++r) img[S.o_order + r] = ord[r];
   }
   img[S.o_step] = 0;
-  img[S.o_step + 1] = n_pre + n_dec;  // the side's rows, read on the device by shape-agnostic prefill graphs (f4)
+  img[S.o_step + 1] = n_pre + n_dec;  // the side's rows, sequences and longest chunk, read on the device by
+  img[S.o_step + 2] = n_seqs;         // shape-agnostic prefill graphs (f4)
+  img[S.o_step + 3] = max_q;
   for (int s = n_seqs; s < S.cap_seqs; ++s) img[S.o_qlen + s] = 0;  // no work items past the batch
   {
     const double hq = c->spec.n_q_heads, hkv = c->spec.n_kv_heads, dh = c->spec.head_dim, e = (double)dt_size(c->dt);

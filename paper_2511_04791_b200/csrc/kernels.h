@@ -173,6 +173,9 @@ struct PrefillAttnArgs {
   // tensor-core path: pool extent and rows of the q buffer (TMA maps)
   int n_pages;
   int total_rows;
+  // nullable device [rows, sequences, longest chunk]: a launch sized for the capacity (n_seqs, max_q) reads
+  // the step's own shape (shape-agnostic prefill graphs, f4; tcgen05 kernel)
+  const int* shape_dev = nullptr;
 };
 int launch_prefill_attn(DT dt, const PrefillAttnArgs& a, cudaStream_t st);
 bool fa_prefill_supported(const PrefillAttnArgs& a);

@@ -212,6 +212,7 @@ struct Params {
   const int* seq_row;
   const int* table;
   int max_pages, hq, hkv, n_qtiles, n_pairs, trace, n_seqs;
+  const int* shape_dev;  // nullable: [rows, sequences, longest chunk] on the device (n_qtiles, n_seqs: capacity)
   bf16* o;
   const bf16* k_pool;
   const bf16* v_pool;
@@ -229,12 +230,16 @@ struct Item {
 // cta / n_ctas: this CTA among the CTAs running prefill attention (the grid, or the prefill part of the
 // fused POD launch, kernels_pod.cu)
 __device__ __forceinline__ bool item_at(const Params& p, int k, Item& it, bool& live, int cta, int n_ctas) {
-  const int G = n_ctas, T = p.n_qtiles * p.n_seqs * p.n_pairs;
+  // a launch sized for the capacity (device-side shapes, f4) enumerates the step's own sequences and query
+  // tiles: shape_dev = [rows, sequences, longest chunk] of the step's metadata
+  const int n_seqs = p.shape_dev ? p.shape_dev[1] : p.n_seqs;
+  const int n_qtiles = p.shape_dev ? (p.shape_dev[2] + BQ - 1) / BQ : p.n_qtiles;
+  const int G = n_ctas, T = n_qtiles * n_seqs * p.n_pairs;
   const int idx = k * G + ((k & 1) ? G - 1 - cta : cta);
   if (idx >= T) return false;
   it.pair = idx % p.n_pairs;
-  it.s_id = (idx / p.n_pairs) % p.n_seqs;
-  it.qt = p.n_qtiles - 1 - idx / (p.n_pairs * p.n_seqs);
+  it.s_id = (idx / p.n_pairs) % n_seqs;
+  it.qt = n_qtiles - 1 - idx / (p.n_pairs * n_seqs);
   it.qlen = p.qlen[it.s_id];
   live = it.qt * BQ < it.qlen;
   if (!live) return true;
@@ -666,12 +671,13 @@ int launch_fa_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   }
   CUtensorMap mq;
   if (!fatc::make_map(&mq, a.q, (uint64_t)a.total_rows, (uint64_t)a.q_stride, (uint64_t)a.q_stride, 128)) return -1;
-  fatc::Params p{a.row0, a.qlen, a.cpre, a.seq_row, a.table, a.max_pages, a.hq, a.hkv, 0, 0, 0, 0,
+  fatc::Params p{a.row0, a.qlen, a.cpre, a.seq_row, a.table, a.max_pages, a.hq, a.hkv, 0, 0, 0, 0, nullptr,
                  (bf16*)a.o, (const bf16*)a.k_pool, (const bf16*)a.v_pool};
   const int G = a.hq / a.hkv;
   p.n_qtiles = (a.max_q + fatc::BQ - 1) / fatc::BQ;
   p.n_pairs = a.hkv * ((G + 1) / 2);
   p.n_seqs = a.n_seqs;
+  p.shape_dev = a.shape_dev;
   static const char* trace = getenv("DUET_FA_TRACE");
   // DUET_FA_TRACE: any value prints the timeline of CTA (0,0,0); "noload" skips the K/V loads instead
   // (timing experiment, garbage output); "tn" does both

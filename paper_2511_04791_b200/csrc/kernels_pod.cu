@@ -91,12 +91,13 @@ int launch_pod_tc(const PrefillAttnArgs& a, const DecodeAttnArgs& da, int pps, i
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return -1;
   }
-  fatc::Params p{a.row0, a.qlen, a.cpre, a.seq_row, a.table, a.max_pages, a.hq, a.hkv, 0, 0, 0, 0,
+  fatc::Params p{a.row0, a.qlen, a.cpre, a.seq_row, a.table, a.max_pages, a.hq, a.hkv, 0, 0, 0, 0, nullptr,
                  (bf16*)a.o, (const bf16*)a.k_pool, (const bf16*)a.v_pool};
   const int G = a.hq / a.hkv;
   p.n_qtiles = (a.max_q + fatc::BQ - 1) / fatc::BQ;
   p.n_pairs = a.hkv * ((G + 1) / 2);
   p.n_seqs = a.n_seqs;
+  p.shape_dev = a.shape_dev;
   const int fa_items = p.n_qtiles * a.n_seqs * p.n_pairs;
   const int n_fa = std::min(a.num_sms - n_dec_ctas, fa_items);
   const int dec_items = n_splits * da.hkv * da.n;
