@@ -29,18 +29,24 @@ static_assert(SMEM <= 227 * 1024, "smem");
 
 __global__ void __launch_bounds__(THREADS, 1)
     pod_attn_kernel(const __grid_constant__ CUtensorMap map_q, fatc::Params fp, const __grid_constant__ CUtensorMap map_k,
-                    const __grid_constant__ CUtensorMap map_v, DecodeAttnArgs da, int pps, int n_splits, int n_fa) {
-  if ((int)blockIdx.x < n_fa) {
-    fatc::fa_tc_body<3, 2>(&map_q, fp, (int)blockIdx.x, n_fa);
+                    const __grid_constant__ CUtensorMap map_v, DecodeAttnArgs da, int pps, int n_splits, int n_fa,
+                    int dec_first) {
+  // role by block index: prefill CTAs first (default) or decode CTAs first (DUET_POD_DEC_FIRST=1, A/B: which
+  // SMs the block scheduler hands each role)
+  const int n_dec_ctas = (int)gridDim.x - n_fa;
+  const int fa_idx = dec_first ? (int)blockIdx.x - n_dec_ctas : (int)blockIdx.x;
+  if (fa_idx >= 0 && fa_idx < n_fa) {
+    fatc::fa_tc_body<3, 2>(&map_q, fp, fa_idx, n_fa);
     return;
   }
+  const int dec_idx = dec_first ? (int)blockIdx.x : (int)blockIdx.x - n_fa;
   pdl_wait();
   const int group = (int)threadIdx.x / (DEC_WARPS * 32);
   if (group >= DEC_GROUPS) return;  // warps 12-13 of a decode CTA idle
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023) + group * DEC_GROUP_BYTES;
   const int tid = (int)threadIdx.x - group * DEC_WARPS * 32;
-  const int slot = ((int)blockIdx.x - n_fa) * DEC_GROUPS + group, n_slots = ((int)gridDim.x - n_fa) * DEC_GROUPS;
+  const int slot = dec_idx * DEC_GROUPS + group, n_slots = n_dec_ctas * DEC_GROUPS;
   const int items = n_splits * da.hkv * da.n;
   for (int it = slot; it < items; it += n_slots) {  // split fastest, then kv head, then request (as the grid)
     const int split = it % n_splits, kvh = (it / n_splits) % da.hkv, z = it / (n_splits * da.hkv);
@@ -102,7 +108,9 @@ int launch_pod_tc(const PrefillAttnArgs& a, const DecodeAttnArgs& da, int pps, i
   const int n_fa = std::min(a.num_sms - n_dec_ctas, fa_items);
   const int dec_items = n_splits * da.hkv * da.n;
   const int n_dec = std::min(n_dec_ctas, (dec_items + pod::DEC_GROUPS - 1) / pod::DEC_GROUPS);
-  launch_pdl(pod::pod_attn_kernel, n_fa + n_dec, pod::THREADS, pod::SMEM, st, mq, p, mz, mz, da, pps, n_splits, n_fa);
+  static const int dec_first = getenv("DUET_POD_DEC_FIRST") ? atoi(getenv("DUET_POD_DEC_FIRST")) : 0;
+  launch_pdl(pod::pod_attn_kernel, n_fa + n_dec, pod::THREADS, pod::SMEM, st, mq, p, mz, mz, da, pps, n_splits, n_fa,
+             dec_first);
   return 1;
 }
 
